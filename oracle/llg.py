@@ -1,0 +1,74 @@
+"""Eq. (3) and the renormalised explicit Euler step, fp64.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Eq. (3):  dM/dt = -gamma/(1+alpha^2) (M x mu0 H)
+                          - alpha gamma/((1+alpha^2) Ms) M x (M x mu0 H).
+Reading Q1: the argument ``gamma0`` is gamma*mu0 in m/(A s) (muMAG SP4 value
+2.211e5), so H stays in A/m and no mu0 appears.  Reading Q2: the equation is
+used as written (no small-alpha expansion).
+
+"The time integration of the LLG equation is implemented with Euler method"
+(P:L55): M* = M + dt dM/dt(M, H_eff(M)), with H_eff evaluated once at the
+pre-step M (reading Q17), then M <- Ms M*/|M*| (reading Q16).
+A non-finite result aborts with the step index and cell.
+"""
+import numpy as np
+
+from .fields import heff as _heff
+
+
+class NonFinite(RuntimeError):
+    def __init__(self, step, cell):
+        super().__init__(f"non-finite magnetisation at step {step}, cell {cell}")
+        self.step = step
+        self.cell = cell
+
+
+def llg_rhs(M, H, alpha, gamma0, Ms):
+    """Eq. (3) per cell; M, H: [3, ...]."""
+    MxH = np.cross(M, H, axis=0)
+    MxMxH = np.cross(M, MxH, axis=0)
+    a = gamma0 / (1.0 + alpha * alpha)
+    return -a * MxH - (alpha * a / Ms) * MxMxH
+
+
+def renormalize(M, Ms):
+    """Scale every cell to |M| = Ms."""
+    n = np.sqrt(M[0] * M[0] + M[1] * M[1] + M[2] * M[2])
+    return Ms * M / n
+
+
+class Sim:
+    """State + parameters of one fp64 run (the oracle twin of a grace context)."""
+
+    def __init__(self, M, demag_op, Ms, A, Ku, alpha, gamma0, d, hext=(0.0, 0.0, 0.0)):
+        self.M = np.array(M, dtype=np.float64)
+        self.demag = demag_op
+        self.Ms, self.A, self.Ku = Ms, A, Ku
+        self.alpha, self.gamma0 = alpha, gamma0
+        self.d = tuple(d)
+        self.hext = tuple(hext)
+        self.step_count = 0
+
+    def heff(self, M=None):
+        M = self.M if M is None else M
+        return _heff(M, self.demag, self.A, self.Ms, self.Ku, self.d, self.hext)
+
+    def euler_step(self, dt):
+        H = self.heff()
+        Mstar = self.M + dt * llg_rhs(self.M, H, self.alpha, self.gamma0, self.Ms)
+        Mn = renormalize(Mstar, self.Ms)
+        bad = ~np.isfinite(Mn).all(axis=0)
+        if bad.any():
+            raise NonFinite(self.step_count, int(np.flatnonzero(bad.ravel())[0]))
+        self.M = Mn
+        self.step_count += 1
+
+    def run(self, n, dt):
+        for _ in range(n):
+            self.euler_step(dt)
+
+    def mavg(self):
+        """<M>/Ms, summed in fixed (C) order."""
+        return np.array([self.M[a].sum() for a in range(3)]) / (self.M[0].size * self.Ms)

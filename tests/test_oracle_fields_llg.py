@@ -1,0 +1,190 @@
+"""Pins of oracle/fields.py, oracle/llg.py and oracle/energy.py.
+
+* exchange: exact zero for uniform M; SPEC's 3x1x1 hand stencil
+  (S:L197); Neumann DCT-II modes are exact eigenvectors with eigenvalue
+  -(2 - 2 cos(pi m/n))/Delta^2 (textbook discrete Laplacian); self-adjoint;
+* anisotropy closed forms;
+* fields = -1/(mu0 V) dE/dM of the separately written Eq. (1) energy, per term,
+  by central differences (S:L225, S:L498 acceptance 5);
+* Eq. (3) sign and magnitude examples;
+* Euler + renormalisation: exact discrete precession map theta = atan(gamma0 H dt)
+  for one cubic cell (its demag field is parallel to M); |M| = Ms, fixed
+  points, damped energy decrease.
+"""
+import numpy as np
+import pytest
+
+from oracle import MU0
+from oracle.demag import DemagFFT
+from oracle.energy import energy
+from oracle.fields import anisotropy, exchange, heff
+from oracle.llg import NonFinite, Sim, llg_rhs
+from oracle.tensor import tensor_octant
+
+RNG = np.random.default_rng(7)
+MS, A = 8e5, 1.3e-11
+
+
+def test_exchange_uniform_is_exactly_zero():
+    M = np.empty((3, 3, 4, 5))
+    M[:] = np.array([0.3, -0.5, 0.81])[:, None, None, None] * MS
+    assert np.all(exchange(M, A, MS, (1e-9, 2e-9, 3e-9)) == 0.0)
+
+
+def test_exchange_hand_stencil_3x1x1():
+    d = 2e-9
+    M = np.zeros((3, 1, 1, 3))
+    M[0, 0, 0, :] = MS
+    M[:, 0, 0, 1] = (0.0, MS, 0.0)
+    H = exchange(M, A, MS, (d, d, d))
+    c = 2 * A / (MU0 * MS * MS * d * d)
+    np.testing.assert_allclose(H[:, 0, 0, 1], c * np.array([2 * MS, -2 * MS, 0]), rtol=1e-14)
+    np.testing.assert_allclose(H[:, 0, 0, 0], c * np.array([-MS, MS, 0]), rtol=1e-14)
+    np.testing.assert_allclose(H[:, 0, 0, 2], c * np.array([-MS, MS, 0]), rtol=1e-14)
+
+
+@pytest.mark.parametrize("axis,n,m", [(3, 16, 3), (2, 9, 4), (1, 5, 1)])
+def test_exchange_neumann_dct_eigenmodes(axis, n, m):
+    shape = [3, 2, 3, 4]
+    shape[axis] = n
+    d = (1e-9, 2e-9, 3e-9)
+    delta = {3: d[0], 2: d[1], 1: d[2]}[axis]
+    i = np.arange(n)
+    mode = np.cos(np.pi * m * (i + 0.5) / n)
+    sh = [1, 1, 1, 1]
+    sh[axis] = n
+    M = np.zeros(shape)
+    M[1] = MS * mode.reshape(sh[1:])
+    H = exchange(M, A, MS, d)
+    lam = -(2.0 - 2.0 * np.cos(np.pi * m / n)) / (delta * delta)
+    c = 2 * A / (MU0 * MS * MS)
+    np.testing.assert_allclose(H[1], c * lam * M[1], rtol=1e-9, atol=1e-12 * abs(c * lam) * MS)
+    assert np.all(H[0] == 0) and np.all(H[2] == 0)
+
+
+def test_exchange_self_adjoint():
+    d = (1e-9, 1.5e-9, 2e-9)
+    M1 = RNG.standard_normal((3, 3, 4, 5))
+    M2 = RNG.standard_normal((3, 3, 4, 5))
+    a = (M1 * exchange(M2, A, 1.0, d)).sum()
+    b = (M2 * exchange(M1, A, 1.0, d)).sum()
+    assert abs(a - b) <= 1e-12 * abs(a)
+
+
+def test_anisotropy_closed_forms():
+    Ku = 6.2832e4
+    Ms = 1e6
+    Hk = 2 * Ku / (MU0 * Ms)
+    M = np.zeros((3, 1, 1, 2))
+    M[:, 0, 0, 0] = (Ms, 0, 0)
+    M[:, 0, 0, 1] = (0, Ms / np.sqrt(2), Ms / np.sqrt(2))
+    H = anisotropy(M, Ku, Ms)
+    np.testing.assert_allclose(H[:, 0, 0, 0], (Hk, 0, 0), rtol=1e-14)
+    assert np.all(H[:, 0, 0, 1] == 0)
+    assert np.all(anisotropy(M, 0.0, Ms) == 0)
+
+
+def test_fields_are_energy_gradient():
+    nx, ny, nz = 4, 4, 4
+    d = (2e-9, 3e-9, 2.5e-9)
+    Ms, Aex, Ku = 8e5, 1.3e-11, 5e4
+    hext = (1e4, -2e4, 3e4)
+    op = DemagFFT(tensor_octant(nx, ny, nz, *d))
+    M = RNG.standard_normal((3, nz, ny, nx))
+    M = Ms * M / np.sqrt((M * M).sum(0))
+    V = d[0] * d[1] * d[2]
+    # per term: (A, Ku, demag on, hext)
+    terms = {
+        "exchange": dict(A=Aex, Ku=0.0, dem=False, h=(0, 0, 0)),
+        "anisotropy": dict(A=0.0, Ku=Ku, dem=False, h=(0, 0, 0)),
+        "demag": dict(A=0.0, Ku=0.0, dem=True, h=(0, 0, 0)),
+        "zeeman": dict(A=0.0, Ku=0.0, dem=False, h=hext),
+        "all": dict(A=Aex, Ku=Ku, dem=True, h=hext),
+    }
+    zero = lambda M_: np.zeros_like(M_)  # noqa: E731
+    for name, t in terms.items():
+        dem = op if t["dem"] else zero
+        H = heff(M, dem, t["A"], Ms, t["Ku"], d, t["h"])
+        for (a, k, j, i) in [(0, 1, 2, 3), (1, 0, 0, 0), (2, 3, 1, 2), (0, 3, 3, 3)]:
+            hstep = 1e-3 * Ms
+            Mp, Mm = M.copy(), M.copy()
+            Mp[a, k, j, i] += hstep
+            Mm[a, k, j, i] -= hstep
+            Ep, _ = energy(Mp, dem, t["A"], Ms, t["Ku"], d, t["h"])
+            Em, _ = energy(Mm, dem, t["A"], Ms, t["Ku"], d, t["h"])
+            fd = -(Ep - Em) / (2 * hstep) / (MU0 * V)
+            scale = np.abs(H).max()
+            assert abs(fd - H[a, k, j, i]) <= 1e-6 * scale, (name, a, fd, H[a, k, j, i])
+
+
+def test_llg_signs_and_magnitudes():
+    g0, Hm, Ms = 2.211e5, 1e5, 8e5
+    M = np.array([Ms, 0, 0])[:, None]
+    H = np.array([0, 0, Hm])[:, None]
+    np.testing.assert_allclose(llg_rhs(M, H, 0.0, g0, Ms)[:, 0], (0, g0 * Ms * Hm, 0), rtol=1e-15)
+    assert np.all(llg_rhs(M, 3.0 * M, 0.3, g0, Ms) == 0)
+    alpha = 0.1
+    H = np.array([0, Hm, 0])[:, None]
+    r = llg_rhs(M, H, alpha, g0, Ms)[:, 0]
+    a = g0 / (1 + alpha ** 2)
+    np.testing.assert_allclose(r, (0, alpha * a * Ms * Hm, -a * Ms * Hm), rtol=1e-14)
+    Mr = RNG.standard_normal((3, 50))
+    Hr = RNG.standard_normal((3, 50)) * 1e5
+    r = llg_rhs(Mr, Hr, 0.3, g0, 1.0)
+    assert np.abs((Mr * r).sum(0)).max() < 1e-9 * np.abs(r).max()
+
+
+def _one_cube(Ms=8e5):
+    return DemagFFT(tensor_octant(1, 1, 1, 2e-9, 2e-9, 2e-9))
+
+
+@pytest.mark.parametrize("dt", [1e-13, 1e-14])
+def test_euler_exact_precession_map(dt):
+    g0, Hm, Ms = 2.211e5, 1e5, 8e5
+    M0 = np.zeros((3, 1, 1, 1))
+    M0[0] = Ms
+    sim = Sim(M0, _one_cube(), Ms, 0.0, 0.0, 0.0, g0, (2e-9,) * 3, hext=(0, 0, Hm))
+    theta = np.arctan(g0 * Hm * dt)
+    for n in range(1, 501):
+        sim.euler_step(dt)
+        if n % 50 == 0:
+            want = Ms * np.array([np.cos(n * theta), np.sin(n * theta), 0.0])
+            np.testing.assert_allclose(sim.M[:, 0, 0, 0], want, rtol=0, atol=1e-12 * Ms)
+    # Larmor period T = 2 pi (1+alpha^2)/(gamma0 H) is the dt -> 0 limit (reading Q1)
+    T = 2 * np.pi / (g0 * Hm)
+    Td = 2 * np.pi * dt / theta
+    x = g0 * Hm * dt
+    assert abs(Td - T) / T <= x * x / 3 * 1.01
+
+
+def test_norm_fixed_point_and_damped_energy():
+    nx, ny, nz = 6, 5, 2
+    d = (3e-9, 3e-9, 3e-9)
+    op = DemagFFT(tensor_octant(nx, ny, nz, *d))
+    M = RNG.standard_normal((3, nz, ny, nx))
+    M = MS * M / np.sqrt((M * M).sum(0))
+    sim = Sim(M, op, MS, A, 1e4, 0.5, 2.211e5, d, hext=(1e4, 0, 0))
+    E0, _ = energy(sim.M, op, A, MS, 1e4, d, sim.hext)
+    for _ in range(30):
+        sim.euler_step(2e-14)
+        n = np.sqrt((sim.M ** 2).sum(0))
+        assert np.abs(n / MS - 1).max() < 1e-12
+        E1, _ = energy(sim.M, op, A, MS, 1e4, d, sim.hext)
+        assert E1 <= E0 + 1e-12 * abs(E0)
+        E0 = E1
+    # fixed point: uniform M along x in a cube with H_ext along x
+    M = np.zeros((3, 1, 1, 1))
+    M[0] = MS
+    s2 = Sim(M, _one_cube(), MS, A, 1e4, 0.5, 2.211e5, (2e-9,) * 3, hext=(5e4, 0, 0))
+    s2.run(10, 1e-13)
+    assert np.array_equal(s2.M, M)
+
+
+def test_nonfinite_abort_reports_step_and_cell():
+    M = np.zeros((3, 1, 1, 2))
+    M[0] = MS
+    op = DemagFFT(tensor_octant(2, 1, 1, 2e-9, 2e-9, 2e-9))
+    sim = Sim(M, op, MS, A, 0.0, 0.1, 2.211e5, (2e-9,) * 3, hext=(0, np.inf, 0))
+    with pytest.raises(NonFinite) as e:
+        sim.euler_step(1e-13)
+    assert e.value.step == 0 and e.value.cell == 0
