@@ -1,0 +1,140 @@
+/* grace.h -- C-ABI of libgrace: the B200 hot path of Grace (Zhu, arXiv 1411.2565).
+ *
+ * One finite-difference micromagnetic LLG step on a regular nx x ny x nz grid:
+ *   H_eff = H_demag + H_exch + H_anis + H_ext                      (Eq. (2))
+ *   H_demag = -N * M, zero-padded FFT convolution with the
+ *             precomputed cell-averaged demag tensor                 (Sec. 3)
+ *   H_exch  = six-neighbour scheme, Neumann boundaries               (reading Q11)
+ *   H_anis  = (2Ku/(mu0 Ms^2)) Mx x, uniaxial along x                (reading Q4)
+ *   dM/dt   = -g0/(1+a^2) M x H - a g0/((1+a^2) Ms) M x (M x H)      (Eq. (3); reading Q1)
+ *   M      <- Ms (M + dt dM/dt)/|M + dt dM/dt|                       (Euler; reading Q16)
+ * "Qnn" are the readings of DESIGN.md §3 where the paper is silent or garbled.
+ *
+ * Conventions (all functions):
+ *  - Units are SI: metres, A/m, J/m, J/m^3, seconds.  `gamma` is gamma0 = gamma*mu0
+ *    in m/(A s) (muMAG SP4 value 2.211e5), never gamma in rad/(s T) (reading Q1).
+ *  - Host arrays are structure-of-arrays [3][nz][ny][nx] doubles, x fastest: element
+ *    (c, k, j, i) at ((c*nz + k)*ny + j)*nx + i.  They belong to the caller; calls
+ *    copy synchronously and return after the copy completed.
+ *  - The context owns all device memory (allocated in grace_create, freed in
+ *    grace_destroy).  Device state is fp32 except the fp64 tensor setup.
+ *  - Every int-returning call returns GRACE_OK or a negative status; on error the
+ *    outputs are untouched, the context stays usable and grace_last_error()
+ *    describes the failure.  Calls on one context must not run concurrently;
+ *    distinct contexts are independent.
+ *  - Device work is queued on the context's CUDA stream (grace_set_stream);
+ *    calls that return host data synchronise that stream.
+ */
+#ifndef GRACE_H
+#define GRACE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct grace_ctx grace_ctx;
+
+enum {
+  GRACE_OK = 0,
+  GRACE_EINVAL = -1,       /* bad argument (count < 1, non-positive/non-finite length, Ms <= 0, A < 0,
+                              Ku < 0, alpha < 0, gamma <= 0 or > 1e9, dt <= 0, n < 0, NULL pointer) */
+  GRACE_ENOMEM = -2,       /* device allocation failed; message carries the bytes required */
+  GRACE_EZEROCELL = -3,    /* grace_set_m: a cell with |M| = 0 or non-finite; message names the cell */
+  GRACE_ENONFINITE = -4,   /* grace_step: non-finite M; grace_last_nonfinite gives step and cell */
+  GRACE_ECUDA = -5,        /* CUDA runtime error (message has the CUDA error string) */
+  GRACE_EUNSUPPORTED = -6  /* padded FFT length above the compiled maximum (x 8192, y 4096, z 1024) */
+};
+
+/* Create a context and build the demag tensor:
+ * the fp64 real-space octant of the six N_ab (Newell near field within 30 cell
+ * diagonals, point dipole beyond; readings Q5-Q8) and its spectrum
+ * KS = -Re FFT(N)/(Px Py Pz) on the padded grid Pa = smallest power of two
+ * >= 2 na - 1 (Pa = 1 when na = 1; reading Q9), folded to one octant in fp32.
+ * nx, ny, nz >= 1 cells; dx, dy, dz > 0 metres; Ms > 0 A/m; A >= 0 J/m;
+ * Ku >= 0 J/m^3 (easy axis x); alpha >= 0; gamma = gamma0 > 0 m/(A s).
+ * Initial M is uniform Ms along x, H_ext = 0, the step counter 0.
+ * On error *out = NULL. */
+int grace_create(int nx, int ny, int nz, double dx, double dy, double dz, double Ms, double A, double Ku,
+                 double alpha, double gamma, grace_ctx **out);
+
+/* Free all device memory of the context.  NULL-safe. */
+void grace_destroy(grace_ctx *h);
+
+/* Set M from a host array (3 N doubles, A/m).  Each cell is renormalised to |M| = Ms
+ * on the device.  A zero or non-finite cell fails with GRACE_EZEROCELL and
+ * leaves M unchanged.  Does not reset the step counter. */
+int grace_set_m(grace_ctx *h, const double *m);
+
+/* Copy M to a host array (3 N doubles, A/m; fp32 values widened exactly). */
+int grace_get_m(grace_ctx *h, double *m_out);
+
+/* Uniform external (Zeeman) field in A/m, used by every later step / heff. */
+int grace_set_hext(grace_ctx *h, double hx, double hy, double hz);
+
+/* H_eff(current M, H_ext) per Eq. (2) into a host array (3 N doubles, A/m). */
+int grace_heff(grace_ctx *h, double *h_out);
+
+/* Advance n >= 0 explicit Euler steps of size dt > 0 seconds, entirely on the
+ * device (CUDA-graph replay; no host round trip inside).  After the n steps one 8-byte
+ * flag is read back: a non-finite M returns GRACE_ENONFINITE (the first failing step
+ * and cell are kept for grace_last_nonfinite; M then holds non-finite values). */
+int grace_step(grace_ctx *h, int n, double dt);
+
+/* Thread-local text of the last failure on this thread ("" if none). */
+const char *grace_last_error(void);
+
+/* ---- extensions (not in the paper's call list) -------------------------------- */
+
+/* Change the damping constant without rebuilding the tensor (SP4: relax at alpha = 1,
+ * then reverse at 0.02). */
+int grace_set_alpha(grace_ctx *h, double alpha);
+
+/* Queue all device work on `cuda_stream` (a cudaStream_t, e.g. torch's current
+ * stream); NULL restores the context's own stream. */
+int grace_set_stream(grace_ctx *h, void *cuda_stream);
+
+/* Device-pointer variants: fp32 SoA [3][nz][ny][nx] in device memory, no host hop.
+ * set_m_device renormalises like grace_set_m. */
+int grace_set_m_device(grace_ctx *h, const float *d_m);
+int grace_get_m_device(grace_ctx *h, float *d_m_out);
+
+/* <M>/Ms (3 doubles) by a fixed-order two-stage reduction (deterministic). */
+int grace_mavg(grace_ctx *h, double *out3);
+
+/* Steps taken so far (t = steps * dt). */
+int grace_step_count(grace_ctx *h, long long *steps);
+
+/* Step index and linear cell index of the first non-finite value of the last failing
+ * grace_step (-1, -1 if none). */
+int grace_last_nonfinite(grace_ctx *h, long long *step, long long *cell);
+
+/* Geometry: out[0..11] = nx ny nz Px Py Pz Kx Kxp Kyh Kzh KSp kernels_per_step. */
+int grace_geometry(grace_ctx *h, long long *out12);
+
+/* Bytes of device memory the context holds. */
+int grace_device_bytes(grace_ctx *h, size_t *bytes);
+
+/* The real-space demag-tensor octant [6][nz][ny][nx] (components xx xy xz yy yz zz,
+ * entry (c,k,j,i) = N_c at offset (i dx, j dy, k dz)), computed on the device exactly
+ * as grace_create does (S1+S2, fp64) and copied to the host array `out` (6 N doubles).
+ * Standalone: needs no context. */
+int grace_tensor_octant(int nx, int ny, int nz, double dx, double dy, double dz, double *out);
+
+/* Copy the fp32 spectral table KS [6][Kzh][Kyh][KSp] to the host (6*Kzh*Kyh*KSp floats). */
+int grace_kernel_spectrum(grace_ctx *h, float *out);
+
+/* Per-kernel timing.  grace_set_profiling(h, 1) makes grace_step launch the kernels
+ * eagerly with a CUDA event pair around each; grace_kernel_times returns, per kernel
+ * of the step (order K1, K2, K3, K4, K5 or K1, K2', K5), the summed milliseconds and
+ * the launch count since the last reset (reset = 1 clears after reading).  nk in:
+ * capacity of ms[]/launches[]; out: number of kernels per step. */
+int grace_set_profiling(grace_ctx *h, int on);
+int grace_kernel_times(grace_ctx *h, double *ms, long long *launches, int *nk, int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRACE_H */

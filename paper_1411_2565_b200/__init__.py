@@ -1,0 +1,261 @@
+"""Python binding of libgrace (include/grace.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of ``libgrace.so``; this
+module converts numpy arrays / torch tensors to pointers and status codes to
+exceptions.  There is no CPU fallback: if the library or a GPU is missing the
+calls raise.
+
+Functions keep the C names (``grace_create``, ``grace_set_m``, ...); ``Grace``
+is a small object wrapper over them.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgrace.so")
+
+GRACE_OK = 0
+GRACE_EINVAL = -1
+GRACE_ENOMEM = -2
+GRACE_EZEROCELL = -3
+GRACE_ENONFINITE = -4
+GRACE_ECUDA = -5
+GRACE_EUNSUPPORTED = -6
+_NAMES = {-1: "EINVAL", -2: "ENOMEM", -3: "EZEROCELL", -4: "ENONFINITE", -5: "ECUDA", -6: "EUNSUPPORTED"}
+
+# (name, restype, argtypes) of every symbol declared in include/grace.h
+_D = ctypes.c_double
+_I = ctypes.c_int
+_P = ctypes.c_void_p
+_PD = ctypes.POINTER(ctypes.c_double)
+_PF = ctypes.POINTER(ctypes.c_float)
+_PLL = ctypes.POINTER(ctypes.c_longlong)
+SIGNATURES = [
+    ("grace_create", _I, [_I, _I, _I, _D, _D, _D, _D, _D, _D, _D, _D, ctypes.POINTER(_P)]),
+    ("grace_destroy", None, [_P]),
+    ("grace_set_m", _I, [_P, _PD]),
+    ("grace_get_m", _I, [_P, _PD]),
+    ("grace_set_hext", _I, [_P, _D, _D, _D]),
+    ("grace_heff", _I, [_P, _PD]),
+    ("grace_step", _I, [_P, _I, _D]),
+    ("grace_last_error", ctypes.c_char_p, []),
+    ("grace_set_alpha", _I, [_P, _D]),
+    ("grace_set_stream", _I, [_P, _P]),
+    ("grace_set_m_device", _I, [_P, _P]),
+    ("grace_get_m_device", _I, [_P, _P]),
+    ("grace_mavg", _I, [_P, _PD]),
+    ("grace_step_count", _I, [_P, _PLL]),
+    ("grace_last_nonfinite", _I, [_P, _PLL, _PLL]),
+    ("grace_geometry", _I, [_P, _PLL]),
+    ("grace_device_bytes", _I, [_P, ctypes.POINTER(ctypes.c_size_t)]),
+    ("grace_tensor_octant", _I, [_I, _I, _I, _D, _D, _D, _PD]),
+    ("grace_kernel_spectrum", _I, [_P, _PF]),
+    ("grace_set_profiling", _I, [_P, _I]),
+    ("grace_kernel_times", _I, [_P, _PD, _PLL, ctypes.POINTER(_I), _I]),
+]
+
+_lib = None
+
+
+class GraceError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"GRACE_{_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+def load(path=LIB_PATH):
+    """Load libgrace.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise ImportError(f"{path} not built; run __graft_entry__.build() (no CPU fallback exists)")
+        lib = ctypes.CDLL(path)
+        for name, res, args in SIGNATURES:
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _check(code):
+    if code != GRACE_OK:
+        raise GraceError(code, load().grace_last_error().decode())
+
+
+def _f64(a, n=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if n is not None and a.size != n:
+        raise ValueError(f"expected {n} values, got {a.size}")
+    return a
+
+
+def _pd(a):
+    return a.ctypes.data_as(_PD)
+
+
+# ---- C-named functions -------------------------------------------------------
+
+def grace_create(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma):
+    h = _P()
+    _check(load().grace_create(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma, ctypes.byref(h)))
+    return h
+
+
+def grace_destroy(h):
+    load().grace_destroy(h)
+
+
+def grace_set_m(h, m):
+    m = _f64(m)
+    _check(load().grace_set_m(h, _pd(m)))
+
+
+def grace_get_m(h, out):
+    _check(load().grace_get_m(h, _pd(out)))
+    return out
+
+
+def grace_set_hext(h, hx, hy, hz):
+    _check(load().grace_set_hext(h, hx, hy, hz))
+
+
+def grace_heff(h, out):
+    _check(load().grace_heff(h, _pd(out)))
+    return out
+
+
+def grace_step(h, n, dt):
+    _check(load().grace_step(h, int(n), float(dt)))
+
+
+def grace_last_error():
+    return load().grace_last_error().decode()
+
+
+def grace_set_alpha(h, alpha):
+    _check(load().grace_set_alpha(h, alpha))
+
+
+def grace_set_stream(h, stream_ptr):
+    _check(load().grace_set_stream(h, _P(stream_ptr) if stream_ptr else None))
+
+
+def grace_set_m_device(h, dev_ptr):
+    _check(load().grace_set_m_device(h, _P(dev_ptr)))
+
+
+def grace_get_m_device(h, dev_ptr):
+    _check(load().grace_get_m_device(h, _P(dev_ptr)))
+
+
+def grace_mavg(h):
+    out = np.zeros(3)
+    _check(load().grace_mavg(h, _pd(out)))
+    return out
+
+
+def grace_step_count(h):
+    v = ctypes.c_longlong()
+    _check(load().grace_step_count(h, ctypes.byref(v)))
+    return v.value
+
+
+def grace_last_nonfinite(h):
+    s, c = ctypes.c_longlong(), ctypes.c_longlong()
+    _check(load().grace_last_nonfinite(h, ctypes.byref(s), ctypes.byref(c)))
+    return s.value, c.value
+
+
+def grace_geometry(h):
+    out = (ctypes.c_longlong * 12)()
+    _check(load().grace_geometry(h, out))
+    keys = ("nx", "ny", "nz", "Px", "Py", "Pz", "Kx", "Kxp", "Kyh", "Kzh", "KSp", "kernels")
+    return dict(zip(keys, list(out)))
+
+
+def grace_device_bytes(h):
+    v = ctypes.c_size_t()
+    _check(load().grace_device_bytes(h, ctypes.byref(v)))
+    return v.value
+
+
+def grace_tensor_octant(nx, ny, nz, dx, dy, dz):
+    out = np.empty((6, nz, ny, nx), dtype=np.float64)
+    _check(load().grace_tensor_octant(nx, ny, nz, dx, dy, dz, _pd(out)))
+    return out
+
+
+def grace_kernel_spectrum(h):
+    g = grace_geometry(h)
+    out = np.empty((6, g["Kzh"], g["Kyh"], g["KSp"]), dtype=np.float32)
+    _check(load().grace_kernel_spectrum(h, out.ctypes.data_as(_PF)))
+    return out
+
+
+def grace_set_profiling(h, on):
+    _check(load().grace_set_profiling(h, 1 if on else 0))
+
+
+def grace_kernel_times(h, reset=False):
+    cap = 8
+    ms = (ctypes.c_double * cap)()
+    ln = (ctypes.c_longlong * cap)()
+    nk = ctypes.c_int(cap)
+    _check(load().grace_kernel_times(h, ms, ln, ctypes.byref(nk), 1 if reset else 0))
+    return list(ms)[: nk.value], list(ln)[: nk.value]
+
+
+# ---- object wrapper ------------------------------------------------------------
+
+class Grace:
+    """One LLG context on the current GPU (owns its device memory)."""
+
+    def __init__(self, n, d, Ms, A, Ku, alpha, gamma0):
+        self.n = tuple(int(v) for v in n)
+        self.shape = (3, self.n[2], self.n[1], self.n[0])
+        self.h = grace_create(*self.n, *d, Ms, A, Ku, alpha, gamma0)
+
+    def close(self):
+        if self.h:
+            grace_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_m(self, M):
+        grace_set_m(self.h, _f64(M, int(np.prod(self.shape))))
+
+    def get_m(self):
+        out = np.empty(self.shape)
+        return grace_get_m(self.h, out)
+
+    def set_hext(self, h):
+        grace_set_hext(self.h, *[float(v) for v in h])
+
+    def set_alpha(self, a):
+        grace_set_alpha(self.h, float(a))
+
+    def heff(self):
+        out = np.empty(self.shape)
+        return grace_heff(self.h, out)
+
+    def step(self, n, dt):
+        grace_step(self.h, n, dt)
+
+    def mavg(self):
+        return grace_mavg(self.h)
+
+    @property
+    def steps(self):
+        return grace_step_count(self.h)
+
+    @property
+    def geometry(self):
+        return grace_geometry(self.h)

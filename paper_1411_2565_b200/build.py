@@ -1,0 +1,55 @@
+"""Build libgrace.so in-tree with nvcc for sm_100a (called by __graft_entry__.build()).
+
+tensor_setup.cu is compiled with -fmad=false (bit-exact fp64 tensor, DESIGN.md
+reading Q8); the per-step kernels keep FMA contraction.  No fast-math anywhere.
+"""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+ROOT = os.path.dirname(HERE)
+LIB = os.path.join(HERE, "libgrace.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
+UNITS = {
+    "grace_api.cu": [],
+    "step_kernels.cu": ["-Xptxas", "-v"] if os.environ.get("GRACE_PTXAS_V") else [],
+    "tensor_setup.cu": ["-fmad=false"],
+}
+HEADERS = ["fft_engine.cuh", "internal.h"]
+
+
+def _mtime(p):
+    return os.path.getmtime(p) if os.path.exists(p) else 0.0
+
+
+def build(force=False, verbose=False):
+    deps = [os.path.join(CSRC, f) for f in list(UNITS) + HEADERS] + [os.path.join(ROOT, "include", "grace.h")]
+    newest = max(_mtime(p) for p in deps)
+    if not force and _mtime(LIB) > newest:
+        return LIB
+    objs = []
+    procs = []
+    for src, extra in UNITS.items():
+        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
+        cmd = [NVCC, *ARCH, *COMMON, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+        procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+        objs.append(obj)
+    for cmd, p in procs:
+        out, _ = p.communicate()
+        if verbose or p.returncode:
+            sys.stderr.write(out)
+        if p.returncode:
+            raise RuntimeError("nvcc failed: " + " ".join(cmd))
+    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs]
+    subprocess.run(cmd, check=True)
+    for o in objs:
+        os.remove(o)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,71 @@
+// Internal declarations shared by the libgrace translation units (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace grace {
+
+// Device-resident per-step parameters.  Kernel arguments are frozen into the
+// captured CUDA graphs, so everything that may change between grace_step calls
+// (dt, alpha, H_ext, the step index) is read from here; one cudaMemcpyAsync of
+// this block per call updates it.
+struct StepParams {
+  float dt;       // s
+  float c_prec;   // -gamma0/(1+alpha^2)                  (Eq. (3) precession prefactor)
+  float c_damp;   // -alpha gamma0/((1+alpha^2) Ms)       (Eq. (3) damping prefactor)
+  float hext[3];  // A/m
+  long long step; // steps started so far; K1 increments it, K5 reports step - 1
+};
+
+// Geometry and the constant material coefficients (fp32, rounded once from fp64 on the host).
+struct Geom {
+  int nx, ny, nz;
+  int Px, Py, Pz;   // padded FFT sizes (power of two >= 2n-1, 1 for a singleton axis)
+  int Kx;           // Px/2 + 1 complex outputs of the x R2C (1 when Px == 1)
+  int Kxp;          // complex row pitch of X1/X2
+  int Kyh, Kzh;     // Py/2 + 1, Pz/2 + 1 (1 for a singleton axis): folded spectrum extents
+  int KSp;          // float row pitch of the spectral table KS
+  int Lmax;         // length of the twiddle table
+  float cx, cy, cz; // exchange 2A/(mu0 Ms^2 d^2) per axis (0 for a singleton axis)
+  float ck;         // anisotropy 2Ku/(mu0 Ms^2)
+  float Ms;
+};
+
+constexpr unsigned long long kNoFlag = ~0ull;
+
+// Per-step kernel launchers (step_kernels.cu).  All enqueue on `st`.
+// K1 also advances bump->step (nullptr: no step, e.g. grace_heff).
+cudaError_t launch_k1(const Geom& g, const float* M, float2* X1, const float2* tw, StepParams* bump,
+                      cudaStream_t st);
+cudaError_t launch_k2(const Geom& g, const float2* X1, float2* X2, const float2* tw, cudaStream_t st);
+cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* tw, cudaStream_t st);
+cudaError_t launch_k4(const Geom& g, const float2* X2, float2* X1, const float2* tw, cudaStream_t st);
+cudaError_t launch_k2f(const Geom& g, float2* X1, const float* KS, const float2* tw, cudaStream_t st);
+// mode 0: LLG Euler step M -> Mn; mode 1: store H_eff into Hout.
+cudaError_t launch_k5(const Geom& g, int mode, const float2* X1, const float* M, float* Mn, float* Hout,
+                      const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st);
+bool fused_y_path(const Geom& g);  // nz == 1 and the y-pencils of 3 components fit one CTA
+int kernel_count(const Geom& g);   // kernels per step
+
+// Utilities (step_kernels.cu).
+cudaError_t launch_twiddles(float2* tw, int Lmax, cudaStream_t st);
+cudaError_t launch_set_m_f64(const double* src, float* M, long long n, double Ms, unsigned long long* flag,
+                             cudaStream_t st);
+cudaError_t launch_set_m_f32(const float* src, float* M, long long n, float Ms, unsigned long long* flag,
+                             cudaStream_t st);
+cudaError_t launch_mavg(const float* M, long long n, double Ms, double* partial, double* out, cudaStream_t st);
+constexpr int kMavgPartials = 3 * 296;
+cudaError_t launch_fill_uniform_x(float* M, long long n, float Ms, cudaStream_t st);
+cudaError_t launch_widen(const float* src, double* dst, long long n, cudaStream_t st);
+
+// Demag-tensor setup (tensor_setup.cu), fp64.
+// Real-space octant [6][nz][ny][nx] into device memory `oct` (bit-exact with the oracle).
+cudaError_t tensor_octant_device(int nx, int ny, int nz, double dx, double dy, double dz, double* oct,
+                                 cudaStream_t st);
+// Spectral table KS [6][Kzh][Kyh][KSp] fp32 = -Re(FFT(circulant N))/(Px Py Pz), from the octant.
+// `work` must hold Px*Py*Pz double2.
+cudaError_t kernel_spectrum_device(const Geom& g, const double* oct, double2* work, float* KS, cudaStream_t st);
+
+}  // namespace grace
