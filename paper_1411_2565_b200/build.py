@@ -14,6 +14,7 @@ LIB = os.path.join(HERE, "libgrace.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]
+COMMON += os.environ.get("GRACE_NVCC_FLAGS", "").split()  # tuning experiments only
 UNITS = {
     "grace_api.cu": [],
     "step_kernels.cu": ["-Xptxas", "-v"] if os.environ.get("GRACE_PTXAS_V") else [],

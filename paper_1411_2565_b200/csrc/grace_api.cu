@@ -99,11 +99,12 @@ struct grace_ctx {
   }
 
   // One step M[c] -> M[1-c] on stream s (bump: advance the device step counter).
-  cudaError_t enqueue_step(int c, cudaStream_t s, bool timed) {
+  // ev (optional): 2 * kernel_count events, recorded before/after each kernel.
+  cudaError_t enqueue_step(int c, cudaStream_t s, cudaEvent_t* ev = nullptr) {
     cudaError_t e;
     int k = 0;
     auto rec = [&](int idx) {
-      if (timed) cudaEventRecord(ev[idx], s);
+      if (ev) cudaEventRecord(ev[idx], s);
     };
     const int nk = kernel_count(g);
     rec(2 * k);
@@ -141,7 +142,7 @@ struct grace_ctx {
     cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) return e;
     for (int i = 0; i < nsteps; ++i) {
-      e = enqueue_step((c + i) & 1, cap, false);
+      e = enqueue_step((c + i) & 1, cap);
       if (e != cudaSuccess) break;
     }
     cudaError_t e2 = cudaStreamEndCapture(cap, &graph);
@@ -275,7 +276,7 @@ int grace_create(int nx, int ny, int nz, double dx, double dy, double dz, double
   // Dry run of one step (M[0] -> M[1], the spare buffer) so every kernel's
   // shared-memory attribute is set before any graph capture; then restore the
   // device step counter and flags.
-  e = h->enqueue_step(0, s, false);
+  e = h->enqueue_step(0, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(h->flag, 0xff, 2 * sizeof(unsigned long long), s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(h->prm, &h->hprm, sizeof(StepParams), cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -396,23 +397,30 @@ int grace_step(grace_ctx* h, int n, double dt) {
   CUDA_OR(cudaMemcpyAsync(h->prm, &h->hprm, sizeof(StepParams), cudaMemcpyHostToDevice, s));
   const int nk = kernel_count(h->g);
   if (h->profiling) {
+    // eager launches with an event pair around every kernel; events are read in
+    // batches of kProfBatch steps so the host never waits inside a batch
+    constexpr int kProfBatch = 64;
     if (h->ev.empty()) {
-      h->ev.resize(2 * nk);
+      h->ev.resize((size_t)2 * nk * kProfBatch);
       for (auto& e : h->ev) CUDA_OR(cudaEventCreate(&e));
       h->kms.assign(nk, 0.0);
       h->klaunch.assign(nk, 0);
     }
-    for (int i = 0; i < n; ++i) {
-      cudaError_t e = h->enqueue_step(h->cur, s, true);
-      if (e != cudaSuccess) return fail(GRACE_ECUDA, "step launch: %s", cudaGetErrorString(e));
-      CUDA_OR(cudaEventSynchronize(h->ev[2 * nk - 1]));
-      for (int k = 0; k < nk; ++k) {
-        float ms = 0.f;
-        CUDA_OR(cudaEventElapsedTime(&ms, h->ev[2 * k], h->ev[2 * k + 1]));
-        h->kms[k] += ms;
-        h->klaunch[k] += 1;
+    for (int i0 = 0; i0 < n; i0 += kProfBatch) {
+      const int nb = std::min(kProfBatch, n - i0);
+      for (int i = 0; i < nb; ++i) {
+        cudaError_t e = h->enqueue_step(h->cur, s, &h->ev[(size_t)2 * nk * i]);
+        if (e != cudaSuccess) return fail(GRACE_ECUDA, "step launch: %s", cudaGetErrorString(e));
+        h->cur ^= 1;
       }
-      h->cur ^= 1;
+      CUDA_OR(cudaEventSynchronize(h->ev[(size_t)2 * nk * nb - 1]));
+      for (int i = 0; i < nb; ++i)
+        for (int k = 0; k < nk; ++k) {
+          float ms = 0.f;
+          CUDA_OR(cudaEventElapsedTime(&ms, h->ev[(size_t)2 * nk * i + 2 * k], h->ev[(size_t)2 * nk * i + 2 * k + 1]));
+          h->kms[k] += ms;
+          h->klaunch[k] += 1;
+        }
     }
   } else {
     int left = n;

@@ -19,6 +19,9 @@
 
 namespace grace {
 
+// Occupancy target per block size: at most ~64 registers per thread.
+#define GRACE_MINB(NT) ((NT) <= 256 ? 4 : ((NT) <= 512 ? 2 : 1))
+
 // ---------------------------------------------------------------------------
 // k-space tensor-vector multiply at (kz, ky, kx) from the folded real table.
 // KS[c][kz'][ky'][kx], kz' = min(kz, Pz-kz), ky' = min(ky, Py-ky); a folded
@@ -46,12 +49,42 @@ __device__ __forceinline__ void kmul3(float2& a, float2& b, float2& c, const flo
   c = make_float2(nxz * mx.x + nyz * my.x + nzz * mz.x, nxz * mx.y + nyz * my.y + nzz * mz.y);
 }
 
+// The same multiply with this CTA's KS slice staged in shared memory:
+// kss[c][kz'][b] for the CTA's ky' and kx tile (c = 0..5).
+__device__ __forceinline__ void kmul3_s(float2& a, float2& b, float2& c, const float* kss, int Kzh, int B,
+                                        const Geom& g, int kz, int ky, int bcol) {
+  const bool fy = ky > (g.Py >> 1), fz = kz > (g.Pz >> 1);
+  const int kzf = fz ? g.Pz - kz : kz;
+  const int cs = Kzh * B;
+  const float* p = kss + kzf * B + bcol;
+  const float nxx = p[0], nyy = p[3 * cs], nzz = p[5 * cs];
+  const float nxy = fy ? -p[cs] : p[cs];
+  const float nxz = fz ? -p[2 * cs] : p[2 * cs];
+  const float nyz = (fy != fz) ? -p[4 * cs] : p[4 * cs];
+  const float2 mx = a, my = b, mz = c;
+  a = make_float2(nxx * mx.x + nxy * my.x + nxz * mz.x, nxx * mx.y + nxy * my.y + nxz * mz.y);
+  b = make_float2(nxy * mx.x + nyy * my.x + nyz * mz.x, nxy * mx.y + nyy * my.y + nyz * mz.y);
+  c = make_float2(nxz * mx.x + nyz * my.x + nzz * mz.x, nxz * mx.y + nyz * my.y + nzz * mz.y);
+}
+
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 // ---------------------------------------------------------------------------
 // K1: x R2C.  A real row of Px (nx nonzero) is packed as z[n] = x[2n] + i x[2n+1],
 // a length-L = Px/2 complex FFT gives Z, and
 //   X[k] = (Z[k] + conj Z[L-k])/2 - (i/2) w^k (Z[k] - conj Z[L-k]),  w = exp(-2 pi i/Px), k = 0..L.
 template <int L, int B, int NT>
-__global__ void __launch_bounds__(NT) k1_fwd_x(const float* __restrict__ M, float2* __restrict__ X1,
+__global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k1_fwd_x(const float* __restrict__ M, float2* __restrict__ X1,
                                                const float2* __restrict__ tw, Geom g, StepParams* bump) {
   extern __shared__ float2 smem[];
   // The step index lives on the device so captured graphs stay valid: K1 of each
@@ -69,7 +102,8 @@ __global__ void __launch_bounds__(NT) k1_fwd_x(const float* __restrict__ M, floa
       __device__ static constexpr bool kSmem() { return false; }
       const float* M;
       int row0, nrows, nx;
-      __device__ float2 operator()(int b, int i) const {
+      __device__ float2 operator()(int b, int ib, int C) const {
+        const int i = ib + C;
         float2 v = make_float2(0.f, 0.f);
         const int row = row0 + b;
         if (row < nrows) {
@@ -82,7 +116,7 @@ __global__ void __launch_bounds__(NT) k1_fwd_x(const float* __restrict__ M, floa
       }
     } ld{M, row0, nrows, g.nx};
     const int twstride = g.Lmax / L;
-    fft_tile<L, B, NT, false, false>(smem, ld, SmemSt<L, B, false>{smem}, tw, twstride);
+    fft_tile<L, B, NT, false, false, true>(smem, ld, SmemSt<L, B, false>{smem}, tw, twstride);
     __syncthreads();
     const int twpx = g.Lmax / (2 * L);
     for (int u = threadIdx.x; u < B * (L + 1); u += NT) {
@@ -103,7 +137,7 @@ __global__ void __launch_bounds__(NT) k1_fwd_x(const float* __restrict__ M, floa
 // K2 / K4: y pencils.  Columns (kx) are contiguous; a CTA owns NCOL columns of one
 // (component, z) slab.  Forward: ny of L inputs nonzero.  Inverse: keep y < ny.
 template <int L, int NCOL, int NT, bool INV>
-__global__ void __launch_bounds__(NT) k_y(const float2* __restrict__ in, float2* __restrict__ out,
+__global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k_y(const float2* __restrict__ in, float2* __restrict__ out,
                                           const float2* __restrict__ tw, Geom g, int in_rows, int out_rows,
                                           int n_in, int n_out) {
   extern __shared__ float2 smem[];
@@ -113,19 +147,21 @@ __global__ void __launch_bounds__(NT) k_y(const float2* __restrict__ in, float2*
     __device__ static constexpr bool kSmem() { return false; }
     const float2* p;
     int pitch, n_in, ncol_valid;
-    __device__ float2 operator()(int b, int i) const {
-      return (i < n_in && b < ncol_valid) ? __ldg(p + (size_t)i * pitch + b) : make_float2(0.f, 0.f);
+    __device__ float2 operator()(int b, int ib, int C) const {
+      const int i = ib + C;
+      return (i < n_in && b < ncol_valid) ? __ldg(p + (b + i * pitch)) : make_float2(0.f, 0.f);
     }
   } ld{in + slab * in_rows * g.Kxp + kx0, g.Kxp, n_in, g.Kx - kx0};
   struct St {
     __device__ static constexpr bool kSmem() { return false; }
     float2* p;
     int pitch, n_out, ncol_valid;
-    __device__ void operator()(int b, int i, float2 v) const {
-      if (i < n_out && b < ncol_valid) p[(size_t)i * pitch + b] = v;
+    __device__ void operator()(int b, int ib, int C, float2 v) const {
+      const int i = ib + C;
+      if (i < n_out && b < ncol_valid) p[b + i * pitch] = v;
     }
   } st{out + slab * out_rows * g.Kxp + kx0, g.Kxp, n_out, g.Kx - kx0};
-  fft_tile<L, NCOL, NT, true, INV>(smem, ld, st, tw, g.Lmax / L);
+  fft_tile<L, NCOL, NT, true, INV, !INV && (L > 1), INV && (L > 1)>(smem, ld, st, tw, g.Lmax / L);
 }
 
 // ---------------------------------------------------------------------------
@@ -133,54 +169,78 @@ __global__ void __launch_bounds__(NT) k_y(const float2* __restrict__ in, float2*
 // forward z-FFT (nz of L nonzero), H~ = KS . M~, inverse z-FFT, keep z < nz.
 // Processing ky and Py-ky in one CTA reads each folded KS slice once.
 template <int L, int B, int NT>
-__global__ void __launch_bounds__(NT) k3_z(float2* __restrict__ X2, const float* __restrict__ KS,
+__global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k3_z(float2* __restrict__ X2, const float* __restrict__ KS,
                                            const float2* __restrict__ tw, Geom g) {
   extern __shared__ float2 smem[];
   constexpr int NCOL = 3 * B;
   const int kx0 = blockIdx.x * B;
   const int kyf = blockIdx.y;
-  const size_t zstride = (size_t)g.Py * g.Kxp;        // between z planes
+  const int zstride = g.Py * g.Kxp;                   // between z planes
   const size_t cstride = (size_t)g.nz * zstride;      // between components
   const int nvalid = g.Kx - kx0;
   const int nky = (kyf == 0 || 2 * kyf == g.Py) ? 1 : 2;
+  // Stage this CTA's folded KS slice (6 comps x Kzh x B) in smem with cp.async;
+  // it lands while the first forward z-FFT runs and serves both ky and Py-ky.
+  constexpr int KZH = L / 2 + 1;
+  float* kss = reinterpret_cast<float*>(smem + TileIdx<L, NCOL, true>::SMEM_ELEMS);
+  {
+    const size_t csK = (size_t)g.Kzh * g.Kyh * g.KSp;
+    if constexpr (B % 4 == 0) {
+      for (int t = threadIdx.x; t < 6 * KZH * (B / 4); t += NT) {
+        const int ch = t % (B / 4), r = t / (B / 4);
+        const int comp = r / KZH, kz = r - comp * KZH;
+        cp_async16(kss + r * B + 4 * ch, KS + comp * csK + ((size_t)kz * g.Kyh + kyf) * g.KSp + kx0 + 4 * ch);
+      }
+    } else {
+      for (int t = threadIdx.x; t < 6 * KZH * B; t += NT) {
+        const int bb = t % B, r = t / B;
+        const int comp = r / KZH, kz = r - comp * KZH;
+        cp_async4(kss + r * B + bb, KS + comp * csK + ((size_t)kz * g.Kyh + kyf) * g.KSp + kx0 + bb);
+      }
+    }
+  }
   for (int rep = 0; rep < nky; ++rep) {
     const int ky = rep == 0 ? kyf : g.Py - kyf;
     float2* base = X2 + (size_t)ky * g.Kxp + kx0;
     struct Ld {
       __device__ static constexpr bool kSmem() { return false; }
       const float2* p;
-      size_t zs, cs;
+      int zs;
+      size_t cs;
       int nz, nvalid;
-      __device__ float2 operator()(int col, int i) const {
+      __device__ float2 operator()(int col, int ib, int C) const {
+        const int i = ib + C;
         const int c = col / B, b = col - c * B;
-        return (i < nz && b < nvalid) ? __ldg(p + c * cs + (size_t)i * zs + b) : make_float2(0.f, 0.f);
+        return (i < nz && b < nvalid) ? __ldg(p + c * cs + (b + i * zs)) : make_float2(0.f, 0.f);
       }
     } ld{base, zstride, cstride, g.nz, nvalid};
     struct St {
       __device__ static constexpr bool kSmem() { return false; }
       float2* p;
-      size_t zs, cs;
+      int zs;
+      size_t cs;
       int nz, nvalid;
-      __device__ void operator()(int col, int i, float2 v) const {
+      __device__ void operator()(int col, int ib, int C, float2 v) const {
+        const int i = ib + C;
         const int c = col / B, b = col - c * B;
-        if (i < nz && b < nvalid) p[c * cs + (size_t)i * zs + b] = v;
+        if (i < nz && b < nvalid) p[c * cs + (b + i * zs)] = v;
       }
     } st{base, zstride, cstride, g.nz, nvalid};
     if (rep) __syncthreads();
-    fft_tile<L, NCOL, NT, true, false>(smem, ld, SmemSt<L, NCOL, true>{smem}, tw, g.Lmax / L);
+    fft_tile<L, NCOL, NT, true, false, (L > 1)>(smem, ld, SmemSt<L, NCOL, true>{smem}, tw, g.Lmax / L);
+    if (rep == 0) cp_async_wait_all();
     __syncthreads();
     for (int u = threadIdx.x; u < L * B; u += NT) {
       const int kz = u / B, b = u - kz * B;
-      if (b >= nvalid) continue;
-      float2* s = smem + kz * NCOL + b;
+      float2* s = smem + TileIdx<L, NCOL, true>::at(b, kz);
       float2 a = s[0], bb = s[B], c = s[2 * B];
-      kmul3(a, bb, c, KS, g, kz, ky, kx0 + b);
+      kmul3_s(a, bb, c, kss, KZH, B, g, kz, ky, b);
       s[0] = a;
       s[B] = bb;
       s[2 * B] = c;
     }
     __syncthreads();
-    fft_tile<L, NCOL, NT, true, true>(smem, SmemLd<L, NCOL, true>{smem}, st, tw, g.Lmax / L);
+    fft_tile<L, NCOL, NT, true, true, false, (L > 1)>(smem, SmemLd<L, NCOL, true>{smem}, st, tw, g.Lmax / L);
   }
 }
 
@@ -201,7 +261,7 @@ __global__ void k_mul_plane(float2* __restrict__ X2, const float* __restrict__ K
 // ---------------------------------------------------------------------------
 // K2': nz == 1.  y-FFT (ny of L nonzero), multiply, inverse y (keep y < ny), in place on X1.
 template <int L, int B, int NT>
-__global__ void __launch_bounds__(NT) k2f_y_fused(float2* __restrict__ X1, const float* __restrict__ KS,
+__global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k2f_y_fused(float2* __restrict__ X1, const float* __restrict__ KS,
                                                   const float2* __restrict__ tw, Geom g) {
   extern __shared__ float2 smem[];
   constexpr int NCOL = 3 * B;
@@ -214,9 +274,10 @@ __global__ void __launch_bounds__(NT) k2f_y_fused(float2* __restrict__ X1, const
     const float2* p;
     size_t cs;
     int pitch, ny, nvalid;
-    __device__ float2 operator()(int col, int i) const {
+    __device__ float2 operator()(int col, int ib, int C) const {
+      const int i = ib + C;
       const int c = col / B, b = col - c * B;
-      return (i < ny && b < nvalid) ? __ldg(p + c * cs + (size_t)i * pitch + b) : make_float2(0.f, 0.f);
+      return (i < ny && b < nvalid) ? __ldg(p + c * cs + (b + i * pitch)) : make_float2(0.f, 0.f);
     }
   } ld{base, cstride, g.Kxp, g.ny, nvalid};
   struct St {
@@ -224,17 +285,18 @@ __global__ void __launch_bounds__(NT) k2f_y_fused(float2* __restrict__ X1, const
     float2* p;
     size_t cs;
     int pitch, ny, nvalid;
-    __device__ void operator()(int col, int i, float2 v) const {
+    __device__ void operator()(int col, int ib, int C, float2 v) const {
+      const int i = ib + C;
       const int c = col / B, b = col - c * B;
-      if (i < ny && b < nvalid) p[c * cs + (size_t)i * pitch + b] = v;
+      if (i < ny && b < nvalid) p[c * cs + (b + i * pitch)] = v;
     }
   } st{base, cstride, g.Kxp, g.ny, nvalid};
-  fft_tile<L, NCOL, NT, true, false>(smem, ld, SmemSt<L, NCOL, true>{smem}, tw, g.Lmax / L);
+  fft_tile<L, NCOL, NT, true, false, (L > 1)>(smem, ld, SmemSt<L, NCOL, true>{smem}, tw, g.Lmax / L);
   __syncthreads();
   for (int u = threadIdx.x; u < L * B; u += NT) {
     const int ky = u / B, b = u - ky * B;
     if (b >= nvalid) continue;
-    float2* s = smem + ky * NCOL + b;
+    float2* s = smem + TileIdx<L, NCOL, true>::at(b, ky);
     float2 a = s[0], bb = s[B], c = s[2 * B];
     kmul3(a, bb, c, KS, g, 0, ky, kx0 + b);
     s[0] = a;
@@ -242,7 +304,7 @@ __global__ void __launch_bounds__(NT) k2f_y_fused(float2* __restrict__ X1, const
     s[2 * B] = c;
   }
   __syncthreads();
-  fft_tile<L, NCOL, NT, true, true>(smem, SmemLd<L, NCOL, true>{smem}, st, tw, g.Lmax / L);
+  fft_tile<L, NCOL, NT, true, true, false, (L > 1)>(smem, SmemLd<L, NCOL, true>{smem}, st, tw, g.Lmax / L);
 }
 
 // ---------------------------------------------------------------------------
@@ -255,7 +317,7 @@ __device__ __forceinline__ float3 ld3(const float* __restrict__ M, size_t N, siz
 }
 
 template <int L, int B, int NT>
-__global__ void __launch_bounds__(NT) k5_inv_x_llg(const float2* __restrict__ X1, const float* __restrict__ M,
+__global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k5_inv_x_llg(const float2* __restrict__ X1, const float* __restrict__ M,
                                                    float* __restrict__ Mn, float* __restrict__ Hout,
                                                    const float2* __restrict__ tw, Geom g,
                                                    const StepParams* __restrict__ prm,
@@ -281,7 +343,8 @@ __global__ void __launch_bounds__(NT) k5_inv_x_llg(const float2* __restrict__ X1
       const float2* tw;
       size_t cs;
       int row0, nrows, pitch, twpx;
-      __device__ float2 operator()(int col, int k) const {
+      __device__ float2 operator()(int col, int ib, int C) const {
+        const int k = ib + C;
         const int c = col / B, b = col - c * B;
         const int row = row0 + b;
         if (row >= nrows) return make_float2(0.f, 0.f);
@@ -299,91 +362,144 @@ __global__ void __launch_bounds__(NT) k5_inv_x_llg(const float2* __restrict__ X1
       __device__ static constexpr bool kSmem() { return true; }
       float* hs;
       int nx;
-      __device__ void operator()(int col, int n, float2 v) const {
-        float* p = hs + col * (2 * L);
-        if (2 * n < nx) p[2 * n] = v.x;
-        if (2 * n + 1 < nx) p[2 * n + 1] = v.y;
+      __device__ void operator()(int col, int ib, int C, float2 v) const {
+        const int n = ib + C;
+        float* p = hs + col * (2 * L) + 2 * n;
+        if (2 * n + 1 < nx) *reinterpret_cast<float2*>(p) = v;
+        else if (2 * n < nx) p[0] = v.x;
       }
     } st{hs, g.nx};
-    fft_tile<L, NCOL, NT, false, true>(smem, ld, st, tw, g.Lmax / L);
+    fft_tile<L, NCOL, NT, false, true, false, true>(smem, ld, st, tw, g.Lmax / L);
   }
   __syncthreads();
   constexpr int HP = (L == 0) ? 1 : 2 * L;  // row pitch of hs
   const StepParams p = *prm;
-  for (int u = threadIdx.x; u < B * g.nx; u += NT) {
-    const int b = u / g.nx, x = u - b * g.nx;
-    const int row = row0 + b;
-    if (row >= nrows) continue;
-    const int z = row / g.ny, y = row - z * g.ny;
-    const size_t i = (size_t)row * g.nx + x;
-    const float3 m = ld3(M, N, i);
-    // Eq. (2): H_eff = H_demag + H_exch + H_anis + H_ext
-    float hx = hs[(0 * B + b) * HP + x] + p.hext[0] + g.ck * m.x;
-    float hy = hs[(1 * B + b) * HP + x] + p.hext[1];
-    float hz = hs[(2 * B + b) * HP + x] + p.hext[2];
-    // six-neighbour exchange, Neumann: a missing neighbour contributes 0 (reading Q11)
-    float ex = 0.f, ey = 0.f, ez = 0.f;
-    if (x > 0) { const float3 q = ld3(M, N, i - 1); ex += g.cx * (q.x - m.x); ey += g.cx * (q.y - m.y); ez += g.cx * (q.z - m.z); }
-    if (x + 1 < g.nx) { const float3 q = ld3(M, N, i + 1); ex += g.cx * (q.x - m.x); ey += g.cx * (q.y - m.y); ez += g.cx * (q.z - m.z); }
-    if (y > 0) { const float3 q = ld3(M, N, i - g.nx); ex += g.cy * (q.x - m.x); ey += g.cy * (q.y - m.y); ez += g.cy * (q.z - m.z); }
-    if (y + 1 < g.ny) { const float3 q = ld3(M, N, i + g.nx); ex += g.cy * (q.x - m.x); ey += g.cy * (q.y - m.y); ez += g.cy * (q.z - m.z); }
-    const size_t plane = (size_t)g.nx * g.ny;
-    if (z > 0) { const float3 q = ld3(M, N, i - plane); ex += g.cz * (q.x - m.x); ey += g.cz * (q.y - m.y); ez += g.cz * (q.z - m.z); }
-    if (z + 1 < g.nz) { const float3 q = ld3(M, N, i + plane); ex += g.cz * (q.x - m.x); ey += g.cz * (q.y - m.y); ez += g.cz * (q.z - m.z); }
-    hx += ex;
-    hy += ey;
-    hz += ez;
-    if (mode == 1) {
-      Hout[i] = hx;
-      Hout[N + i] = hy;
-      Hout[2 * N + i] = hz;
-      continue;
+  const size_t plane = (size_t)g.nx * g.ny;
+  const int ncell = B * g.nx;
+  // Two cells per thread per iteration with all 42 stencil loads issued before
+  // any use.  A missing neighbour (Neumann) loads the centre cell instead, so its
+  // difference is exactly 0 (reading Q11).
+  constexpr int CPI = 2;
+  for (int u0 = threadIdx.x; u0 < ncell; u0 += CPI * NT) {
+    float3 m[CPI], q[CPI][6];
+    size_t ic[CPI];
+    int bc[CPI], xc[CPI];
+    bool ok[CPI];
+#pragma unroll
+    for (int c = 0; c < CPI; ++c) {
+      const int u = u0 + c * NT;
+      const int b = u / g.nx, x = u - b * g.nx;
+      const int row = row0 + b;
+      ok[c] = u < ncell && row < nrows;
+      const int rr = ok[c] ? row : 0;
+      const int xx = ok[c] ? x : 0;
+      const int z = rr / g.ny, y = rr - z * g.ny;
+      const size_t i = (size_t)rr * g.nx + xx;
+      ic[c] = i;
+      bc[c] = ok[c] ? b : 0;
+      xc[c] = xx;
+      m[c] = ld3(M, N, i);
+      q[c][0] = ld3(M, N, xx > 0 ? i - 1 : i);
+      q[c][1] = ld3(M, N, xx + 1 < g.nx ? i + 1 : i);
+      q[c][2] = ld3(M, N, y > 0 ? i - g.nx : i);
+      q[c][3] = ld3(M, N, y + 1 < g.ny ? i + g.nx : i);
+      q[c][4] = ld3(M, N, z > 0 ? i - plane : i);
+      q[c][5] = ld3(M, N, z + 1 < g.nz ? i + plane : i);
     }
-    // Eq. (3): dM/dt = c_prec (M x H) + c_damp M x (M x H)
-    const float ax = m.y * hz - m.z * hy, ay = m.z * hx - m.x * hz, az = m.x * hy - m.y * hx;
-    const float bx = m.y * az - m.z * ay, by = m.z * ax - m.x * az, bz = m.x * ay - m.y * ax;
-    const float sx = m.x + p.dt * (p.c_prec * ax + p.c_damp * bx);
-    const float sy = m.y + p.dt * (p.c_prec * ay + p.c_damp * by);
-    const float sz = m.z + p.dt * (p.c_prec * az + p.c_damp * bz);
-    const float s = g.Ms / sqrtf(sx * sx + sy * sy + sz * sz);  // renormalise to Ms (reading Q16)
-    const float ox = sx * s, oy = sy * s, oz = sz * s;
-    Mn[i] = ox;
-    Mn[N + i] = oy;
-    Mn[2 * N + i] = oz;
-    if (!(isfinite(ox) && isfinite(oy) && isfinite(oz)))
-      atomicMin(flag, ((unsigned long long)(p.step - 1) << 36) | (unsigned long long)i);
+#pragma unroll
+    for (int c = 0; c < CPI; ++c) {
+      if (!ok[c]) continue;
+      const size_t i = ic[c];
+      const int b = bc[c], x = xc[c];
+      const float3 mm = m[c];
+      // Eq. (2): H_eff = H_demag + H_exch + H_anis + H_ext
+      float hx = hs[(0 * B + b) * HP + x] + p.hext[0] + g.ck * mm.x;
+      float hy = hs[(1 * B + b) * HP + x] + p.hext[1];
+      float hz = hs[(2 * B + b) * HP + x] + p.hext[2];
+      // six-neighbour exchange (difference form: uniform M gives exactly 0)
+      float ex = 0.f, ey = 0.f, ez = 0.f;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        const float ck = k < 2 ? g.cx : (k < 4 ? g.cy : g.cz);
+        ex += ck * (q[c][k].x - mm.x);
+        ey += ck * (q[c][k].y - mm.y);
+        ez += ck * (q[c][k].z - mm.z);
+      }
+      hx += ex;
+      hy += ey;
+      hz += ez;
+      if (mode == 1) {
+        Hout[i] = hx;
+        Hout[N + i] = hy;
+        Hout[2 * N + i] = hz;
+        continue;
+      }
+      // Eq. (3): dM/dt = c_prec (M x H) + c_damp M x (M x H)
+      const float ax = mm.y * hz - mm.z * hy, ay = mm.z * hx - mm.x * hz, az = mm.x * hy - mm.y * hx;
+      const float bx = mm.y * az - mm.z * ay, by = mm.z * ax - mm.x * az, bz = mm.x * ay - mm.y * ax;
+      const float sx = mm.x + p.dt * (p.c_prec * ax + p.c_damp * bx);
+      const float sy = mm.y + p.dt * (p.c_prec * ay + p.c_damp * by);
+      const float sz = mm.z + p.dt * (p.c_prec * az + p.c_damp * bz);
+      const float sc = g.Ms / sqrtf(sx * sx + sy * sy + sz * sz);  // renormalise to Ms (reading Q16)
+      const float ox = sx * sc, oy = sy * sc, oz = sz * sc;
+      Mn[i] = ox;
+      Mn[N + i] = oy;
+      Mn[2 * N + i] = oz;
+      if (!(isfinite(ox) && isfinite(oy) && isfinite(oz)))
+        atomicMin(flag, ((unsigned long long)(p.step - 1) << 36) | (unsigned long long)i);
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
-// Tile choices and dispatch.
+// Tile choices and dispatch.  Every engine instance uses TPC = L/16 threads per
+// column, i.e. 16 complex values per thread per pass.
+// Complex values per thread per Stockham pass (EPT) and tile sizes, per kernel,
+// from the sweep in profiles/ (DESIGN.md §6).  TPC = L/EPT threads per column.
+#ifndef GRACE_EPT_X1
+#define GRACE_EPT_X1 16
+#endif
+#ifndef GRACE_EPT_X5
+#define GRACE_EPT_X5 32
+#endif
+#ifndef GRACE_EPT_Y
+#define GRACE_EPT_Y 16
+#endif
+#ifndef GRACE_EPT_Z
+#define GRACE_EPT_Z 32
+#endif
+#ifndef GRACE_Y_ELEMS
+#define GRACE_Y_ELEMS 16384  // complex values per K2/K4 tile
+#endif
+__host__ __device__ constexpr int tpc_of(int L, int ept) { return L >= ept ? L / ept : 1; }
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 template <int L>
-struct XCfg {  // K1 rows / K5 rows
-  static constexpr int B1 = (L == 0) ? 256 : (4096 / L > 0 ? 4096 / L : 1);
-  static constexpr int B5 = (L == 0) ? 64 : (2048 / L > 0 ? 2048 / L : 1);
-  static constexpr int NT = 256;
+struct XCfg {  // K1 rows / K5 rows (3 components per row)
+  static constexpr int TPC1 = tpc_of(L, GRACE_EPT_X1);
+  static constexpr int TPC5 = tpc_of(L, GRACE_EPT_X5);
+  static constexpr int B1 = (L == 0) ? 256 : cmax(1, 256 / TPC1);
+  static constexpr int NT1 = (L == 0) ? 256 : B1 * TPC1;
+  static constexpr int B5 = (L == 0) ? 64 : cmax(1, 128 / TPC5);
+  static constexpr int NT5 = (L == 0) ? 256 : 3 * B5 * TPC5;
 };
 template <int L>
 struct YCfg {  // K2/K4 columns
-  static constexpr int NCOL = (8192 / L > 32) ? 32 : (8192 / L < 4 ? 4 : 8192 / L);
-  static constexpr int E = NCOL * L;
-  static constexpr int NT = E / 32 > 512 ? 512 : (E / 32 < 128 ? 128 : E / 32);
+  static constexpr int NCOL = cmax(2, cmin(32, GRACE_Y_ELEMS / L));
+  static constexpr int NT = cmin(1024, cmax(32, NCOL * tpc_of(L, GRACE_EPT_Y)));
 };
 template <int L>
-struct ZCfg {  // K3 (3 components) and K2'
-  static constexpr int B = (8192 / (3 * L) > 32) ? 32 : (8192 / (3 * L) < 1 ? 1 : 8192 / (3 * L));
-  static constexpr int NT = 256;
-};
-template <int L>
-struct FCfg {  // K2' fused y: 3B*L <= 6144
-  static constexpr int B = (2048 / L > 32) ? 32 : (2048 / L < 1 ? 1 : 2048 / L);
-  static constexpr int NT = 256;
+struct ZCfg {  // K3 and K2' (3 components, B kx columns each)
+  static constexpr int B = cmax(1, cmin(32, 2048 / L));
+  static constexpr int NT = cmax(32, 3 * B * tpc_of(L, GRACE_EPT_Z));
 };
 
 template <class K>
 static cudaError_t prep(K kern, size_t smem) {
-  if (smem > 48 * 1024) return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e == cudaSuccess && smem > 48 * 1024)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return e;
 }
 
 #define GRACE_L_SWITCH(Lval, CASE) \
@@ -395,8 +511,8 @@ static cudaError_t prep(K kern, size_t smem) {
 template <int L>
 static cudaError_t k1_launch(const Geom& g, const float* M, float2* X1, const float2* tw, StepParams* bump,
                              cudaStream_t st) {
-  constexpr int B = XCfg<L>::B1, NT = XCfg<L>::NT;
-  const size_t smem = (L == 0) ? 0 : (size_t)B * L * sizeof(float2);
+  constexpr int B = XCfg<L>::B1, NT = XCfg<L>::NT1;
+  const size_t smem = (L == 0) ? 0 : (size_t)TileIdx<(L > 0 ? L : 1), B, false>::SMEM_ELEMS * sizeof(float2);
   auto kern = k1_fwd_x<L, B, NT>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
@@ -418,7 +534,7 @@ template <int L, bool INV>
 static cudaError_t ky_launch(const Geom& g, const float2* in, float2* out, const float2* tw, cudaStream_t st,
                              int in_rows, int out_rows, int n_in, int n_out) {
   constexpr int NCOL = YCfg<L>::NCOL, NT = YCfg<L>::NT;
-  const size_t smem = (size_t)NCOL * L * sizeof(float2);
+  const size_t smem = (size_t)TileIdx<L, NCOL, true>::SMEM_ELEMS * sizeof(float2);
   auto kern = k_y<L, NCOL, NT, INV>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
@@ -442,7 +558,8 @@ cudaError_t launch_k4(const Geom& g, const float2* X2, float2* X1, const float2*
 template <int L>
 static cudaError_t k3_launch(const Geom& g, float2* X2, const float* KS, const float2* tw, cudaStream_t st) {
   constexpr int B = ZCfg<L>::B, NT = ZCfg<L>::NT;
-  const size_t smem = (size_t)3 * B * L * sizeof(float2);
+  const size_t smem = (size_t)TileIdx<L, 3 * B, true>::SMEM_ELEMS * sizeof(float2) +
+                      (size_t)6 * (L / 2 + 1) * B * sizeof(float);
   auto kern = k3_z<L, B, NT>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
@@ -467,8 +584,8 @@ int kernel_count(const Geom& g) { return fused_y_path(g) ? 3 : 5; }
 
 template <int L>
 static cudaError_t k2f_launch(const Geom& g, float2* X1, const float* KS, const float2* tw, cudaStream_t st) {
-  constexpr int B = FCfg<L>::B, NT = FCfg<L>::NT;
-  const size_t smem = (size_t)3 * B * L * sizeof(float2);
+  constexpr int B = ZCfg<L>::B, NT = ZCfg<L>::NT;
+  const size_t smem = (size_t)TileIdx<L, 3 * B, true>::SMEM_ELEMS * sizeof(float2);
   auto kern = k2f_y_fused<L, B, NT>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
@@ -485,8 +602,9 @@ cudaError_t launch_k2f(const Geom& g, float2* X1, const float* KS, const float2*
 template <int L>
 static cudaError_t k5_launch(const Geom& g, int mode, const float2* X1, const float* M, float* Mn, float* Hout,
                              const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st) {
-  constexpr int B = XCfg<L>::B5, NT = XCfg<L>::NT;
-  const size_t smem = (L == 0) ? (size_t)3 * B * sizeof(float) : (size_t)3 * B * L * sizeof(float2);
+  constexpr int B = XCfg<L>::B5, NT = XCfg<L>::NT5;
+  const size_t smem = (L == 0) ? (size_t)3 * B * sizeof(float)
+                               : (size_t)TileIdx<(L > 0 ? L : 1), 3 * B, false>::SMEM_ELEMS * sizeof(float2);
   auto kern = k5_inv_x_llg<L, B, NT>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
