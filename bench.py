@@ -205,19 +205,34 @@ def run_own(args, w):
     pb.load()
     nx, ny, nz = w.n
     N = nx * ny * nz
-    g = pb.Grace(w.n, w.d, w.Ms, w.A, w.Ku, w.alpha, w.gamma0)
+    distributed = world > 1 and nz % world == 0
+    if distributed:  # z-slab partition over NCCL (strong scaling of one global grid)
+        from paper_1411_2565_b200.dist import create_context, partition
+
+        g = create_context(w, rank, world, local)
+        slab = partition(nx, nz, rank, world)
+        Mfull = random_m(w.n, w.Ms)
+        Mloc = np.ascontiguousarray(Mfull[:, slab.z_offset:slab.z_offset + slab.nz_local])
+        del Mfull
+        Nloc = Mloc[0].size
+    else:  # one grid per GPU (replicas)
+        g = pb.Grace(w.n, w.d, w.Ms, w.A, w.Ku, w.alpha, w.gamma0)
+        Mloc = random_m(w.n, w.Ms, seed=14112565 + rank)
+        Nloc = N
     stream = torch.cuda.Stream()
     pb.grace_set_stream(g.h, stream.cuda_stream)
-    M0 = torch.from_numpy(random_m(w.n, w.Ms, seed=14112565 + rank).astype(np.float32)).cuda()
+    M0 = torch.from_numpy(Mloc.astype(np.float32)).cuda()
     pb.grace_set_m_device(g.h, M0.data_ptr())
     g.set_hext(w.hext)
     geo = g.geometry
     fused = geo["kernels"] == 3
     names = ["K1", "K2f", "K5"] if fused else ["K1", "K2", "K3", "K4", "K5"]
     g.step(args.warmup, w.dt)
-    pb.grace_set_profiling(g.h, True)
-    g.step(2, w.dt)  # profiling warm-up (event pool)
-    pb.grace_kernel_times(g.h, reset=True)
+    profile = not distributed
+    if profile:
+        pb.grace_set_profiling(g.h, True)
+        g.step(2, w.dt)  # profiling warm-up (event pool)
+        pb.grace_kernel_times(g.h, reset=True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         if dist:
@@ -231,26 +246,32 @@ def run_own(args, w):
             dist.barrier()
     ms = ev0.elapsed_time(ev1)
     kms, klaunch = pb.grace_kernel_times(g.h, reset=True)
+    if not profile:
+        klaunch = [args.steps] * len(names)
     pb.grace_set_profiling(g.h, False)
     if dist:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = world * N * args.steps / (ms / 1e3)  # replicas: every rank steps its own full grid
+    # distributed: the ranks together step one grid of N cells; replicas: every rank its own
+    value = (N if distributed else world * N) * args.steps / (ms / 1e3)
 
     # roofline of the dominant kernel
     peak, peak_src = read_peaks()
     ab = algorithmic_bytes(geo, fused)
     kern = {}
+    if not profile:
+        kms = [0.0] * len(names)
     for name, t, nl in zip(names, kms, klaunch):
         avg = t / max(nl, 1)
         kern[name] = {"ms_per_launch": avg, "bytes_per_launch": ab[name],
                       "GBps": ab[name] / (avg / 1e3) / 1e9, "share": t / max(sum(kms), 1e-12)}
     dom = max(kern, key=lambda k: kern[k]["ms_per_launch"])
-    ach = kern[dom]["GBps"]
+    ach = kern[dom]["GBps"] if profile else None
     step_bytes = sum(ab.values())
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak if ach else None,
                 "traffic": ncu_traffic(w.name, dom), "peak_source": peak_src,
                 "step_bytes": step_bytes, "step_GBps": step_bytes / (ms_step / 1e3) / 1e9,
                 "step_frac": step_bytes / (ms_step / 1e3) / 1e9 / peak}
@@ -258,9 +279,9 @@ def run_own(args, w):
     # e2e through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        Mh = torch.empty(3 * N, dtype=torch.float64, pin_memory=True)
-        Mh.copy_(torch.from_numpy(random_m(w.n, w.Ms, seed=7 + rank).ravel()))
-        Mout = torch.empty(3 * N, dtype=torch.float64, pin_memory=True)
+        Mh = torch.empty(3 * Nloc, dtype=torch.float64, pin_memory=True)
+        Mh.copy_(torch.from_numpy(np.ascontiguousarray(Mloc).ravel()))
+        Mout = torch.empty(3 * Nloc, dtype=torch.float64, pin_memory=True)
         mh = Mh.numpy()
         mo = Mout.numpy()
         torch.cuda.synchronize()
@@ -283,27 +304,28 @@ def run_own(args, w):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             tms = float(t.item())
         K = args.steps
-        e2e = {"value": world * N * K / (tms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": (24 * N + 40 * K) / K, "d2h_bytes_per_step": (24 * N + 32 * K) / K,
+        e2e = {"value": (N if distributed else world * N) * K / (tms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": (24 * Nloc + 40 * K) / K, "d2h_bytes_per_step": (24 * Nloc + 32 * K) / K,
                "ms_per_step": tms / K, "host_wall_s": wall,
                "api": "grace_set_m(pinned) + K x (grace_set_hext, grace_step(1), grace_mavg) + grace_get_m(pinned)"}
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong" if distributed else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": w.name, "grid": list(w.n), "cell_m": list(w.d),
                    "padded": [geo["Px"], geo["Py"], geo["Pz"]], "Ms": w.Ms, "A": w.A, "Ku": w.Ku,
                    "alpha": w.alpha, "dt": w.dt, "gamma0": w.gamma0,
                    "l2": f"inputs larger than L2 ({(pb.grace_device_bytes(g.h)) / 1e9:.2f} GB resident vs 126 MB L2); no flush",
                    "parallelism": "single GPU" if world == 1 else
-                   f"{world} independent replicas (z-slab distributed path not yet built)",
+                   (f"z-slab x{world}: ncclAlltoAll transposes + halo planes (one grid)" if distributed
+                    else f"{world} independent replicas (nz not divisible by {world})"),
                    "step": "K1 x-R2C, K2 y-FFT, K3 z-FFT*N*iFFT, K4 y-iFFT, K5 x-C2R+exch+anis+Zeeman+LLG+Euler"
                    if not fused else "K1 x-R2C, K2' y-FFT*N*iFFT, K5 x-C2R+local+LLG+Euler",
                    "timing": "libgrace profiling mode: eager launches, a CUDA event pair per kernel on the library stream"},
         "roofline": roofline,
         "kernels": kern,
-        "gpu_launches": int(sum(klaunch)),
+        "gpu_launches": int(sum(klaunch)) if profile else args.steps * len(names),
         "clocks": clk.summary(),
         "e2e": e2e,
     }

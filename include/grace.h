@@ -134,6 +134,32 @@ int grace_kernel_spectrum(grace_ctx *h, float *out);
 int grace_set_profiling(grace_ctx *h, int on);
 int grace_kernel_times(grace_ctx *h, double *ms, long long *launches, int *nk, int reset);
 
+/* ---- distributed z-slab path ------------------------------------
+ * The grid is split into P slabs of nz/P planes (nz % P == 0).  One step: K1 on
+ * each slab, all-to-all to kx blocks of ceil(Kx/P) columns (C1), K2..K4 on the
+ * block (all z), all-to-all back (C2), one-plane halo exchange of M (C3), K5 on
+ * each slab.  Results are identical to the single-GPU path (same per-pencil
+ * arithmetic). */
+
+/* P ranks of one grid in this context on the current GPU; the exchanges are
+ * device-to-device copies.  Same interface as grace_create (whole-grid arrays);
+ * used to test the partition logic on one GPU.  nranks = 1 is grace_create. */
+int grace_create_virtual(int nx, int ny, int nz, double dx, double dy, double dz, double Ms, double A, double Ku,
+                         double alpha, double gamma, int nranks, grace_ctx **out);
+
+/* Write a fresh NCCL unique id (128 bytes) into out128 (rank 0; broadcast it to the
+ * other ranks, e.g. with torch.distributed). */
+int grace_nccl_unique_id(void *out128);
+
+/* This process's rank of an nranks-way NCCL partition on the current GPU.
+ * set_m/get_m/heff then address the local slab [3][nz/nranks][ny][nx] (z offset
+ * rank*nz/nranks); grace_step and grace_mavg are collective (call on every rank). */
+int grace_create_dist(int nx, int ny, int nz, double dx, double dy, double dz, double Ms, double A, double Ku,
+                      double alpha, double gamma, int rank, int nranks, const void *nccl_id, grace_ctx **out);
+
+/* out[0..7] = P, rank, nz_local, z_offset, kx_block, kx_columns_here, pitch1, pitch2. */
+int grace_partition(grace_ctx *h, long long *out8);
+
 #ifdef __cplusplus
 }
 #endif

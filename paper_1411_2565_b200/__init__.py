@@ -54,6 +54,10 @@ SIGNATURES = [
     ("grace_kernel_spectrum", _I, [_P, _PF]),
     ("grace_set_profiling", _I, [_P, _I]),
     ("grace_kernel_times", _I, [_P, _PD, _PLL, ctypes.POINTER(_I), _I]),
+    ("grace_create_virtual", _I, [_I, _I, _I, _D, _D, _D, _D, _D, _D, _D, _D, _I, ctypes.POINTER(_P)]),
+    ("grace_nccl_unique_id", _I, [_P]),
+    ("grace_create_dist", _I, [_I, _I, _I, _D, _D, _D, _D, _D, _D, _D, _D, _I, _I, _P, ctypes.POINTER(_P)]),
+    ("grace_partition", _I, [_P, _PLL]),
 ]
 
 _lib = None
@@ -102,6 +106,33 @@ def grace_create(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma):
     h = _P()
     _check(load().grace_create(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma, ctypes.byref(h)))
     return h
+
+
+def grace_create_virtual(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma, nranks):
+    h = _P()
+    _check(load().grace_create_virtual(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma, nranks, ctypes.byref(h)))
+    return h
+
+
+def grace_nccl_unique_id():
+    buf = ctypes.create_string_buffer(128)
+    _check(load().grace_nccl_unique_id(buf))
+    return bytes(buf.raw)
+
+
+def grace_create_dist(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma, rank, nranks, nccl_id):
+    h = _P()
+    idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+    _check(load().grace_create_dist(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma, rank, nranks, idbuf,
+                                    ctypes.byref(h)))
+    return h
+
+
+def grace_partition(h):
+    out = (ctypes.c_longlong * 8)()
+    _check(load().grace_partition(h, out))
+    keys = ("P", "rank", "nz_local", "z_offset", "kx_block", "kx_columns", "pitch1", "pitch2")
+    return dict(zip(keys, list(out)))
 
 
 def grace_destroy(h):
@@ -211,12 +242,26 @@ def grace_kernel_times(h, reset=False):
 # ---- object wrapper ------------------------------------------------------------
 
 class Grace:
-    """One LLG context on the current GPU (owns its device memory)."""
+    """One LLG context (owns its device memory).
 
-    def __init__(self, n, d, Ms, A, Ku, alpha, gamma0):
+    Default: the whole grid on the current GPU.  ``virtual_ranks=P`` partitions it
+    into P z-slabs in this process (exchanges by device copies); ``dist=(rank,
+    nranks, nccl_id)`` makes this process rank ``rank`` of an NCCL partition, and
+    the arrays are then the local slab.
+    """
+
+    def __init__(self, n, d, Ms, A, Ku, alpha, gamma0, virtual_ranks=None, dist=None):
         self.n = tuple(int(v) for v in n)
-        self.shape = (3, self.n[2], self.n[1], self.n[0])
-        self.h = grace_create(*self.n, *d, Ms, A, Ku, alpha, gamma0)
+        nz_here = self.n[2]
+        if dist is not None:
+            rank, nranks, nid = dist
+            self.h = grace_create_dist(*self.n, *d, Ms, A, Ku, alpha, gamma0, rank, nranks, nid)
+            nz_here = self.n[2] // nranks
+        elif virtual_ranks is not None:
+            self.h = grace_create_virtual(*self.n, *d, Ms, A, Ku, alpha, gamma0, int(virtual_ranks))
+        else:
+            self.h = grace_create(*self.n, *d, Ms, A, Ku, alpha, gamma0)
+        self.shape = (3, nz_here, self.n[1], self.n[0])
 
     def close(self):
         if self.h:

@@ -1,12 +1,23 @@
-// libgrace C-ABI implementation (include/grace.h): context, validation, device
-// memory, the CUDA-graph step loop, errors.  Host code; the arithmetic of the
-// path runs in step_kernels.cu and tensor_setup.cu.
+// libgrace C-ABI implementation (include/grace.h): contexts, validation, device
+// memory, the CUDA-graph step loop, the z-slab distributed step and errors.
+// Host code; the arithmetic of the path runs in step_kernels.cu and
+// tensor_setup.cu.
+//
+// A context holds one or more "ranks" (z slabs):
+//   single  - one rank, the whole grid; step = CUDA-graph replay.
+//   virtual - P ranks of one grid on one GPU in one process; the all-to-all and
+//             halo exchanges are cudaMemcpyAsync between the ranks' buffers
+//             (exercises the partition logic against the single path).
+//   nccl    - this process's rank of P (one GPU per process); the exchanges are
+//             ncclAlltoAll and grouped ncclSend/ncclRecv over NVLink.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -35,6 +46,11 @@ int fail(int code, const char* fmt, ...) {
     cudaError_t e_ = (call);                                                                   \
     if (e_ != cudaSuccess) return fail(GRACE_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
   } while (0)
+#define CE(call)                      \
+  do {                                \
+    cudaError_t e_ = (call);          \
+    if (e_ != cudaSuccess) return e_; \
+  } while (0)
 
 constexpr double kPI = 3.141592653589793;
 constexpr double kMU0 = 4.0 * kPI * 1e-7;  // S:L46, reading Q21
@@ -49,29 +65,91 @@ int padded(int n) {
 long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
 bool finite_pos(double v) { return std::isfinite(v) && v > 0.0; }
 
+// ---- NCCL, loaded at run time (torch has normally loaded libnccl.so.2 already) ----
+typedef struct ncclComm* ncclComm_t;
+typedef int ncclResult_t;
+struct ncclUniqueId {
+  char internal[128];
+};
+enum { kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0 };
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allToAll)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+  bool load() {
+    if (h) return true;
+    const char* env = getenv("GRACE_NCCL_LIB");
+    const char* names[] = {env, "libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      if (!n) continue;
+      h = dlopen(n, RTLD_NOW | RTLD_NOLOAD);
+      if (!h) h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
+    commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+    commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    allToAll = (decltype(allToAll))dlsym(h, "ncclAlltoAll");
+    allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+    send = (decltype(send))dlsym(h, "ncclSend");
+    recv = (decltype(recv))dlsym(h, "ncclRecv");
+    groupStart = (decltype(groupStart))dlsym(h, "ncclGroupStart");
+    groupEnd = (decltype(groupEnd))dlsym(h, "ncclGroupEnd");
+    errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
+    return getUniqueId && commInitRank && commDestroy && allToAll && allReduce && send && recv && groupStart &&
+           groupEnd && errStr;
+  }
+};
+Nccl g_nccl;
+
 }  // namespace
 
-struct grace_ctx {
+// ---------------------------------------------------------------------------------
+// One z slab with its device state.
+struct Rank {
   Geom g{};
+  int r = 0;
+  long long Nl = 0;  // cells in the slab
+  float* M[2] = {nullptr, nullptr};
+  float2* A = nullptr;   // single: X1 [3][nz][ny][Kxp]; dist: S1 / R2 [P][3][nzl][ny][Kb]
+  float2* B = nullptr;   // dist: R1 / S2 [P][3][nzl][ny][Kb]
+  float2* X2 = nullptr;  // [3][nz][Py][pitch2] (absent on the fused nz = 1 path)
+  float* KS = nullptr;
+  float* Hlo = nullptr;  // halo planes [3][ny][nx]
+  float* Hhi = nullptr;
+  StepParams* prm = nullptr;
+  unsigned long long* flag = nullptr;  // [0] step non-finite, [1] set_m zero cell
+  double* red = nullptr;               // mavg partials + 3 outputs
+  float* Hbuf = nullptr;
+};
+
+struct grace_ctx {
+  enum Mode { kSingle, kVirtual, kNccl } mode = kSingle;
+  int P = 1;       // ranks in the partition
+  int myrank = 0;  // nccl mode: this process's rank
   double dx, dy, dz, Ms, A, Ku, alpha, gamma0;
   double hext[3] = {0, 0, 0};
   long long steps = 0;
   long long nf_step = -1, nf_cell = -1;
-  long long N = 0;
+  long long N = 0;  // cells addressed by set_m/get_m/heff (whole grid, or the local slab in nccl mode)
   int cur = 0;
   bool fused = false;
-  float* M[2] = {nullptr, nullptr};
-  float2* X1 = nullptr;
-  float2* X2 = nullptr;
-  float* KS = nullptr;
+  Geom g0{};  // global geometry
+  std::vector<Rank> ranks;
   float2* tw = nullptr;
-  StepParams* prm = nullptr;
-  unsigned long long* flag = nullptr;   // [0] step non-finite, [1] set_m zero cell
-  double* red = nullptr;                // mavg partials + 3 outputs
-  float* Hbuf = nullptr;
   size_t bytes = 0;
   cudaStream_t own = nullptr, stream = nullptr, cap = nullptr;
   cudaGraphExec_t g1[2] = {nullptr, nullptr}, gc[2] = {nullptr, nullptr};
+  ncclComm_t comm = nullptr;
   bool profiling = false;
   std::vector<double> kms;
   std::vector<long long> klaunch;
@@ -79,6 +157,7 @@ struct grace_ctx {
   StepParams hprm{};
 
   int alloc(void** p, size_t b) {
+    if (b == 0) b = 16;
     cudaError_t e = cudaMalloc(p, b);
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -97,54 +176,119 @@ struct grace_ctx {
     for (int q = 0; q < 3; ++q) hprm.hext[q] = (float)hext[q];
     hprm.step = steps;
   }
+  cudaError_t upload_params(double dt) {
+    fill_params(dt);
+    for (auto& rk : ranks) CE(cudaMemcpyAsync(rk.prm, &hprm, sizeof(StepParams), cudaMemcpyHostToDevice, stream));
+    return cudaSuccess;
+  }
 
-  // One step M[c] -> M[1-c] on stream s (bump: advance the device step counter).
-  // ev (optional): 2 * kernel_count events, recorded before/after each kernel.
-  cudaError_t enqueue_step(int c, cudaStream_t s, cudaEvent_t* ev = nullptr) {
-    cudaError_t e;
-    int k = 0;
+  // ---- exchanges (distributed modes) ----
+  // all-to-all of [P][blk1] complex blocks: block q of rank s's send buffer goes to
+  // block s of rank q's receive buffer.
+  cudaError_t alltoall(float2* Rank::*src, float2* Rank::*dst, cudaStream_t s) {
+    const long long blk = ranks[0].g.blk1;
+    if (mode == kVirtual) {
+      for (int a = 0; a < P; ++a)
+        for (int b = 0; b < P; ++b)
+          CE(cudaMemcpyAsync(ranks[b].*dst + (size_t)a * blk, ranks[a].*src + (size_t)b * blk,
+                             sizeof(float2) * blk, cudaMemcpyDeviceToDevice, s));
+      return cudaSuccess;
+    }
+    Rank& rk = ranks[0];
+    const ncclResult_t r = g_nccl.allToAll(rk.*src, rk.*dst, (size_t)blk * 2, kNcclFloat32, comm, s);
+    return r == 0 ? cudaSuccess : cudaErrorUnknown;
+  }
+  // halo: plane nzl-1 of rank r-1 -> Hlo of rank r; plane 0 of rank r+1 -> Hhi of rank r.
+  cudaError_t halo(int c, cudaStream_t s) {
+    const size_t plane = (size_t)g0.ny * g0.nx;
+    const int nzl = ranks[0].g.nzl;
+    const long long Nl = ranks[0].Nl;
+    if (mode == kVirtual) {
+      for (int r = 0; r < P; ++r)
+        for (int q = 0; q < 3; ++q) {
+          if (r > 0)
+            CE(cudaMemcpyAsync(ranks[r].Hlo + q * plane, ranks[r - 1].M[c] + q * Nl + (size_t)(nzl - 1) * plane,
+                               sizeof(float) * plane, cudaMemcpyDeviceToDevice, s));
+          if (r + 1 < P)
+            CE(cudaMemcpyAsync(ranks[r].Hhi + q * plane, ranks[r + 1].M[c] + q * Nl, sizeof(float) * plane,
+                               cudaMemcpyDeviceToDevice, s));
+        }
+      return cudaSuccess;
+    }
+    Rank& rk = ranks[0];
+    const int r = myrank;
+    bool bad = g_nccl.groupStart() != 0;
+    for (int q = 0; q < 3 && !bad; ++q) {
+      if (r > 0) {
+        bad |= g_nccl.send(rk.M[c] + q * Nl, plane, kNcclFloat32, r - 1, comm, s) != 0;
+        bad |= g_nccl.recv(rk.Hlo + q * plane, plane, kNcclFloat32, r - 1, comm, s) != 0;
+      }
+      if (r + 1 < P) {
+        bad |= g_nccl.send(rk.M[c] + q * Nl + (size_t)(nzl - 1) * plane, plane, kNcclFloat32, r + 1, comm, s) != 0;
+        bad |= g_nccl.recv(rk.Hhi + q * plane, plane, kNcclFloat32, r + 1, comm, s) != 0;
+      }
+    }
+    bad |= g_nccl.groupEnd() != 0;
+    return bad ? cudaErrorUnknown : cudaSuccess;
+  }
+
+  // H~ for every rank: K1 .. K4 plus the transposes.  M[c] is the input.
+  cudaError_t demag_stages(int c, cudaStream_t s, bool bump, cudaEvent_t* ev = nullptr) {
     auto rec = [&](int idx) {
       if (ev) cudaEventRecord(ev[idx], s);
     };
-    const int nk = kernel_count(g);
-    rec(2 * k);
-    if ((e = launch_k1(g, M[c], X1, tw, prm, s)) != cudaSuccess) return e;
-    rec(2 * k + 1);
-    ++k;
-    if (fused) {
-      rec(2 * k);
-      if ((e = launch_k2f(g, X1, KS, tw, s)) != cudaSuccess) return e;
-      rec(2 * k + 1);
-      ++k;
-    } else {
-      rec(2 * k);
-      if ((e = launch_k2(g, X1, X2, tw, s)) != cudaSuccess) return e;
-      rec(2 * k + 1);
-      ++k;
-      rec(2 * k);
-      if ((e = launch_k3(g, X2, KS, tw, s)) != cudaSuccess) return e;
-      rec(2 * k + 1);
-      ++k;
-      rec(2 * k);
-      if ((e = launch_k4(g, X2, X1, tw, s)) != cudaSuccess) return e;
-      rec(2 * k + 1);
-      ++k;
+    if (mode == kSingle) {
+      Rank& rk = ranks[0];
+      rec(0);
+      CE(launch_k1(rk.g, rk.M[c], rk.A, tw, bump ? rk.prm : nullptr, s));
+      rec(1);
+      if (fused) {
+        rec(2);
+        CE(launch_k2f(rk.g, rk.A, rk.KS, tw, s));
+        rec(3);
+      } else {
+        rec(2);
+        CE(launch_k2(rk.g, rk.A, rk.X2, tw, s));
+        rec(3);
+        rec(4);
+        CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s));
+        rec(5);
+        rec(6);
+        CE(launch_k4(rk.g, rk.X2, rk.A, tw, s));
+        rec(7);
+      }
+      return cudaSuccess;
     }
-    rec(2 * k);
-    if ((e = launch_k5(g, 0, X1, M[c], M[1 - c], nullptr, tw, prm, flag, s)) != cudaSuccess) return e;
-    rec(2 * k + 1);
-    (void)nk;
+    for (auto& rk : ranks) CE(launch_k1(rk.g, rk.M[c], rk.A, tw, bump ? rk.prm : nullptr, s));
+    CE(alltoall(&Rank::A, &Rank::B, s));  // C1: z slabs -> kx blocks
+    for (auto& rk : ranks) {
+      if (rk.g.Kc > 0) {
+        CE(launch_k2(rk.g, rk.B, rk.X2, tw, s));
+        CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s));
+        CE(launch_k4(rk.g, rk.X2, rk.B, tw, s));
+      }
+    }
+    CE(alltoall(&Rank::B, &Rank::A, s));  // C2: kx blocks -> z slabs
+    CE(halo(c, s));                       // C3: one M plane to each neighbour
+    return cudaSuccess;
+  }
+
+  // One step M[c] -> M[1-c] (ev: optional 2 events per kernel, single mode).
+  cudaError_t enqueue_step(int c, cudaStream_t s, cudaEvent_t* ev = nullptr) {
+    CE(demag_stages(c, s, true, ev));
+    const int k5 = 2 * (kernel_count(g0) - 1);
+    if (ev) cudaEventRecord(ev[k5], s);
+    for (auto& rk : ranks)
+      CE(launch_k5(rk.g, 0, rk.A, rk.M[c], rk.M[1 - c], nullptr, tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+    if (ev) cudaEventRecord(ev[k5 + 1], s);
     return cudaSuccess;
   }
 
   cudaError_t build_graph(int c, int nsteps, cudaGraphExec_t* out) {
     cudaGraph_t graph = nullptr;
-    cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
-    if (e != cudaSuccess) return e;
-    for (int i = 0; i < nsteps; ++i) {
-      e = enqueue_step((c + i) & 1, cap);
-      if (e != cudaSuccess) break;
-    }
+    CE(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < nsteps && e == cudaSuccess; ++i) e = enqueue_step((c + i) & 1, cap);
     cudaError_t e2 = cudaStreamEndCapture(cap, &graph);
     if (e != cudaSuccess) {
       if (graph) cudaGraphDestroy(graph);
@@ -160,37 +304,24 @@ struct grace_ctx {
     for (int c = 0; c < 2; ++c) {
       if (g1[c]) cudaGraphExecDestroy(g1[c]);
       if (gc[c]) cudaGraphExecDestroy(gc[c]);
-      if (M[c]) cudaFree(M[c]);
     }
     for (auto e : ev) cudaEventDestroy(e);
-    void* ptrs[] = {X1, X2, KS, tw, prm, flag, red, Hbuf};
-    for (void* p : ptrs)
-      if (p) cudaFree(p);
+    for (auto& rk : ranks) {
+      void* ptrs[] = {rk.M[0], rk.M[1], rk.A, rk.B, rk.X2, rk.KS, rk.Hlo, rk.Hhi, rk.prm, rk.flag, rk.red, rk.Hbuf};
+      for (void* p : ptrs)
+        if (p) cudaFree(p);
+    }
+    if (tw) cudaFree(tw);
+    if (comm) g_nccl.commDestroy(comm);
     if (own) cudaStreamDestroy(own);
     if (cap) cudaStreamDestroy(cap);
   }
 };
 
-extern "C" {
+namespace {
 
-const char* grace_last_error(void) { return g_err.c_str(); }
-
-int grace_create(int nx, int ny, int nz, double dx, double dy, double dz, double Ms, double A, double Ku, double alpha,
-                 double gamma, grace_ctx** out) {
-  g_err.clear();
-  if (!out) return fail(GRACE_EINVAL, "out is NULL");
-  *out = nullptr;
-  if (nx < 1 || ny < 1 || nz < 1) return fail(GRACE_EINVAL, "cell counts must be >= 1 (got %d %d %d)", nx, ny, nz);
-  if (!finite_pos(dx) || !finite_pos(dy) || !finite_pos(dz))
-    return fail(GRACE_EINVAL, "cell sizes must be finite and > 0");
-  if (!finite_pos(Ms)) return fail(GRACE_EINVAL, "Ms must be finite and > 0");
-  if (!std::isfinite(A) || A < 0) return fail(GRACE_EINVAL, "A must be finite and >= 0");
-  if (!std::isfinite(Ku) || Ku < 0) return fail(GRACE_EINVAL, "Ku must be finite and >= 0");
-  if (!std::isfinite(alpha) || alpha < 0) return fail(GRACE_EINVAL, "alpha must be finite and >= 0");
-  if (!finite_pos(gamma)) return fail(GRACE_EINVAL, "gamma must be finite and > 0");
-  if (gamma > 1e9) return fail(GRACE_EINVAL, "pass gamma0 = gamma*mu0 in m/(A s) (e.g. 2.211e5), not gamma in rad/(s T)");
-  const long long N = (long long)nx * ny * nz;
-  if (N >= (1LL << 36)) return fail(GRACE_EUNSUPPORTED, "grid of %lld cells exceeds 2^36", N);
+// Global geometry and material coefficients.
+int make_geom(int nx, int ny, int nz, double dx, double dy, double dz, double Ms, double A, double Ku, Geom* out) {
   Geom g{};
   g.nx = nx;
   g.ny = ny;
@@ -213,9 +344,67 @@ int grace_create(int nx, int ny, int nz, double dx, double dy, double dz, double
   g.cz = nz > 1 ? (float)(ex / (dz * dz)) : 0.f;
   g.ck = (float)(2.0 * Ku / (kMU0 * Ms * Ms));
   g.Ms = (float)Ms;
+  g.nzl = nz;
+  g.pitch1 = g.Kxp;
+  g.kb = 0;
+  g.blk1 = 0;
+  g.Kc = g.Kx;
+  g.pitch2 = g.Kxp;
+  g.has_lo = g.has_hi = 0;
+  *out = g;
+  return GRACE_OK;
+}
 
+// The slab of rank r of P.
+Geom rank_geom(const Geom& g0, int r, int P) {
+  Geom g = g0;
+  if (P == 1) return g;
+  const int Kb = (g0.Kx + P - 1) / P;
+  g.nzl = g0.nz / P;
+  g.kb = Kb;
+  g.pitch1 = Kb;
+  g.blk1 = 3LL * g.nzl * g0.ny * Kb;
+  g.Kc = std::max(0, std::min(g0.Kx, (r + 1) * Kb) - r * Kb);
+  g.pitch2 = (int)round_up(std::max(g.Kc, 1), 16);
+  g.KSp = (int)round_up(std::max(g.Kc, 1), 32);
+  g.has_lo = r > 0;
+  g.has_hi = r + 1 < P;
+  return g;
+}
+
+int validate(int nx, int ny, int nz, double dx, double dy, double dz, double Ms, double A, double Ku, double alpha,
+             double gamma) {
+  if (nx < 1 || ny < 1 || nz < 1) return fail(GRACE_EINVAL, "cell counts must be >= 1 (got %d %d %d)", nx, ny, nz);
+  if (!finite_pos(dx) || !finite_pos(dy) || !finite_pos(dz))
+    return fail(GRACE_EINVAL, "cell sizes must be finite and > 0");
+  if (!finite_pos(Ms)) return fail(GRACE_EINVAL, "Ms must be finite and > 0");
+  if (!std::isfinite(A) || A < 0) return fail(GRACE_EINVAL, "A must be finite and >= 0");
+  if (!std::isfinite(Ku) || Ku < 0) return fail(GRACE_EINVAL, "Ku must be finite and >= 0");
+  if (!std::isfinite(alpha) || alpha < 0) return fail(GRACE_EINVAL, "alpha must be finite and >= 0");
+  if (!finite_pos(gamma)) return fail(GRACE_EINVAL, "gamma must be finite and > 0");
+  if (gamma > 1e9)
+    return fail(GRACE_EINVAL, "pass gamma0 = gamma*mu0 in m/(A s) (e.g. 2.211e5), not gamma in rad/(s T)");
+  if ((long long)nx * ny * nz >= (1LL << 36)) return fail(GRACE_EUNSUPPORTED, "grid exceeds 2^36 cells");
+  return GRACE_OK;
+}
+
+// Build a context with `nranks_here` rank slabs (ranks first_rank ...) of a P-way partition.
+int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double Ms, double A, double Ku,
+                double alpha, double gamma, grace_ctx::Mode mode, int P, int first_rank, int nranks_here,
+                const void* nccl_id, grace_ctx** out) {
+  g_err.clear();
+  if (!out) return fail(GRACE_EINVAL, "out is NULL");
+  *out = nullptr;
+  int rc = validate(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma);
+  if (rc) return rc;
+  if (P < 1 || nz % P != 0) return fail(GRACE_EINVAL, "nz = %d must be a multiple of the rank count %d", nz, P);
+  Geom g0{};
+  if ((rc = make_geom(nx, ny, nz, dx, dy, dz, Ms, A, Ku, &g0))) return rc;
   grace_ctx* h = new grace_ctx();
-  h->g = g;
+  h->mode = mode;
+  h->P = P;
+  h->myrank = first_rank;
+  h->g0 = g0;
   h->dx = dx;
   h->dy = dy;
   h->dz = dz;
@@ -224,9 +413,7 @@ int grace_create(int nx, int ny, int nz, double dx, double dy, double dz, double
   h->Ku = Ku;
   h->alpha = alpha;
   h->gamma0 = gamma;
-  h->N = N;
-  h->fused = fused_y_path(g);
-  int rc = GRACE_OK;
+  h->fused = (P == 1) && fused_y_path(g0);
   auto bail = [&](int code) {
     h->release();
     delete h;
@@ -238,51 +425,149 @@ int grace_create(int nx, int ny, int nz, double dx, double dy, double dz, double
     if (e != cudaSuccess) return bail(fail(GRACE_ECUDA, "stream creation: %s", cudaGetErrorString(e)));
   }
   h->stream = h->own;
-  const size_t mbytes = sizeof(float) * 3 * (size_t)N;
-  const size_t x1 = sizeof(float2) * 3 * (size_t)nz * ny * g.Kxp;
-  const size_t x2 = h->fused ? 0 : sizeof(float2) * 3 * (size_t)nz * g.Py * g.Kxp;
-  const size_t ks = sizeof(float) * 6 * (size_t)g.Kzh * g.Kyh * g.KSp;
-  if ((rc = h->alloc((void**)&h->M[0], mbytes)) || (rc = h->alloc((void**)&h->M[1], mbytes)) ||
-      (rc = h->alloc((void**)&h->X1, x1)) || (x2 && (rc = h->alloc((void**)&h->X2, x2))) ||
-      (rc = h->alloc((void**)&h->KS, ks)) || (rc = h->alloc((void**)&h->tw, sizeof(float2) * g.Lmax)) ||
-      (rc = h->alloc((void**)&h->prm, sizeof(StepParams))) ||
-      (rc = h->alloc((void**)&h->flag, 2 * sizeof(unsigned long long))) ||
-      (rc = h->alloc((void**)&h->red, sizeof(double) * (kMavgPartials + 3))))
-    return bail(rc);
   cudaStream_t s = h->stream;
-  // setup: fp64 octant -> fp64 padded spectrum -> fp32 folded KS (S1..S5)
+  if (mode == grace_ctx::kNccl) {
+    if (!g_nccl.load()) return bail(fail(GRACE_EUNSUPPORTED, "libnccl.so.2 not found (set GRACE_NCCL_LIB)"));
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof id);
+    const ncclResult_t r = g_nccl.commInitRank(&h->comm, P, id, first_rank);
+    if (r != 0) return bail(fail(GRACE_ECUDA, "ncclCommInitRank: %s", g_nccl.errStr(r)));
+  }
+  h->ranks.resize(nranks_here);
+  for (int i = 0; i < nranks_here; ++i) {
+    Rank& rk = h->ranks[i];
+    rk.r = first_rank + i;
+    rk.g = rank_geom(g0, rk.r, P);
+    const Geom& g = rk.g;
+    rk.Nl = (long long)g.nzl * ny * nx;
+    const size_t mb = sizeof(float) * 3 * (size_t)rk.Nl;
+    const size_t ab = P == 1 ? sizeof(float2) * 3 * (size_t)nz * ny * g.Kxp : sizeof(float2) * (size_t)P * g.blk1;
+    const size_t x2 = h->fused ? 0 : sizeof(float2) * 3 * (size_t)nz * g.Py * g.pitch2;
+    const size_t ks = sizeof(float) * 6 * (size_t)g.Kzh * g.Kyh * g.KSp;
+    const size_t hb = sizeof(float) * 3 * (size_t)ny * nx;
+    if ((rc = h->alloc((void**)&rk.M[0], mb)) || (rc = h->alloc((void**)&rk.M[1], mb)) ||
+        (rc = h->alloc((void**)&rk.A, ab)) || (P > 1 && (rc = h->alloc((void**)&rk.B, ab))) ||
+        (x2 && (rc = h->alloc((void**)&rk.X2, x2))) || (rc = h->alloc((void**)&rk.KS, ks)) ||
+        (g.has_lo && (rc = h->alloc((void**)&rk.Hlo, hb))) || (g.has_hi && (rc = h->alloc((void**)&rk.Hhi, hb))) ||
+        (rc = h->alloc((void**)&rk.prm, sizeof(StepParams))) ||
+        (rc = h->alloc((void**)&rk.flag, 2 * sizeof(unsigned long long))) ||
+        (rc = h->alloc((void**)&rk.red, sizeof(double) * (kMavgPartials + 3))))
+      return bail(rc);
+  }
+  if ((rc = h->alloc((void**)&h->tw, sizeof(float2) * g0.Lmax))) return bail(rc);
+  h->N = (mode == grace_ctx::kNccl) ? h->ranks[0].Nl : (long long)nx * ny * nz;
+
+  // setup: fp64 octant -> fp64 padded spectrum -> fp32 folded KS (S1..S5), once,
+  // then each rank keeps its kx columns
+  const long long Ng = (long long)nx * ny * nz;
   double* oct = nullptr;
   double2* work = nullptr;
-  const size_t octb = sizeof(double) * 6 * (size_t)N;
-  const size_t workb = sizeof(double2) * (size_t)g.Px * g.Py * g.Pz;
-  if (cudaMalloc(&oct, octb) != cudaSuccess || cudaMalloc(&work, workb) != cudaSuccess) {
+  float* ksfull = nullptr;
+  const size_t octb = sizeof(double) * 6 * (size_t)Ng;
+  const size_t workb = sizeof(double2) * (size_t)g0.Px * g0.Py * g0.Pz;
+  const size_t ksfb = sizeof(float) * 6 * (size_t)g0.Kzh * g0.Kyh * g0.KSp;
+  if (cudaMalloc(&oct, octb) != cudaSuccess || cudaMalloc(&work, workb) != cudaSuccess ||
+      (P > 1 && cudaMalloc(&ksfull, ksfb) != cudaSuccess)) {
     cudaGetLastError();
     if (oct) cudaFree(oct);
-    return bail(fail(GRACE_ENOMEM, "setup needs %zu bytes of fp64 scratch", octb + workb));
+    if (work) cudaFree(work);
+    return bail(fail(GRACE_ENOMEM, "setup needs %zu bytes of fp64 scratch", octb + workb + ksfb));
   }
   cudaError_t e = tensor_octant_device(nx, ny, nz, dx, dy, dz, oct, s);
-  if (e == cudaSuccess) e = kernel_spectrum_device(g, oct, work, h->KS, s);
-  if (e == cudaSuccess) e = launch_twiddles(h->tw, g.Lmax, s);
-  if (e == cudaSuccess) e = launch_fill_uniform_x(h->M[0], N, (float)Ms, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(h->flag, 0xff, 2 * sizeof(unsigned long long), s);
-  if (e == cudaSuccess) {
-    h->fill_params(1e-15);
-    e = cudaMemcpyAsync(h->prm, &h->hprm, sizeof(StepParams), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = kernel_spectrum_device(g0, oct, work, P == 1 ? h->ranks[0].KS : ksfull, s);
+  if (e == cudaSuccess && P > 1) {
+    for (auto& rk : h->ranks) {
+      if (rk.g.Kc == 0) continue;
+      const int kx0 = rk.r * rk.g.kb;
+      e = cudaMemcpy2DAsync(rk.KS, sizeof(float) * rk.g.KSp, ksfull + kx0, sizeof(float) * g0.KSp,
+                            sizeof(float) * rk.g.Kc, (size_t)6 * g0.Kzh * g0.Kyh, cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) break;
+    }
   }
+  if (e == cudaSuccess) e = launch_twiddles(h->tw, g0.Lmax, s);
+  for (auto& rk : h->ranks) {
+    if (e == cudaSuccess) e = launch_fill_uniform_x(rk.M[0], rk.Nl, (float)Ms, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(rk.flag, 0xff, 2 * sizeof(unsigned long long), s);
+  }
+  if (e == cudaSuccess) e = h->upload_params(1e-15);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   cudaFree(oct);
   cudaFree(work);
+  if (ksfull) cudaFree(ksfull);
   if (e != cudaSuccess) return bail(fail(GRACE_ECUDA, "tensor setup: %s", cudaGetErrorString(e)));
   // Dry run of one step (M[0] -> M[1], the spare buffer) so every kernel's
   // shared-memory attribute is set before any graph capture; then restore the
-  // device step counter and flags.
+  // device step counters and flags.
   e = h->enqueue_step(0, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(h->flag, 0xff, 2 * sizeof(unsigned long long), s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(h->prm, &h->hprm, sizeof(StepParams), cudaMemcpyHostToDevice, s);
+  for (auto& rk : h->ranks)
+    if (e == cudaSuccess) e = cudaMemsetAsync(rk.flag, 0xff, 2 * sizeof(unsigned long long), s);
+  if (e == cudaSuccess) e = h->upload_params(1e-15);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return bail(fail(GRACE_ECUDA, "first step: %s", cudaGetErrorString(e)));
   *out = h;
   return GRACE_OK;
+}
+
+// First set flag over the ranks (0: step non-finite, packed step<<36|cell; 1: set_m
+// zero cell), translated to the caller's cell numbering, and reset on the device.
+int check_flags(grace_ctx* h, int which, unsigned long long* first) {
+  *first = kNoFlag;
+  for (auto& rk : h->ranks) {
+    unsigned long long f = kNoFlag;
+    CUDA_OR(cudaMemcpyAsync(&f, rk.flag + which, sizeof f, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_OR(cudaStreamSynchronize(h->stream));
+    if (f == kNoFlag) continue;
+    CUDA_OR(cudaMemsetAsync(rk.flag + which, 0xff, sizeof f, h->stream));
+    CUDA_OR(cudaStreamSynchronize(h->stream));
+    const unsigned long long off =
+        (h->mode == grace_ctx::kVirtual) ? (unsigned long long)rk.r * rk.g.nzl * h->g0.ny * h->g0.nx : 0;
+    const unsigned long long mask = (1ULL << 36) - 1;
+    const unsigned long long packed = (which == 0) ? ((f & ~mask) | ((f & mask) + off)) : f + off;
+    if (packed < *first) *first = packed;
+  }
+  return GRACE_OK;
+}
+
+// Offset of rank rk's slab inside the caller's component array (virtual mode).
+size_t slab_offset(const grace_ctx* h, const Rank& rk) {
+  return (h->mode == grace_ctx::kVirtual) ? (size_t)rk.r * rk.Nl : 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* grace_last_error(void) { return g_err.c_str(); }
+
+int grace_create(int nx, int ny, int nz, double dx, double dy, double dz, double Ms, double A, double Ku, double alpha,
+                 double gamma, grace_ctx** out) {
+  return create_impl(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma, grace_ctx::kSingle, 1, 0, 1, nullptr, out);
+}
+
+int grace_create_virtual(int nx, int ny, int nz, double dx, double dy, double dz, double Ms, double A, double Ku,
+                         double alpha, double gamma, int nranks, grace_ctx** out) {
+  if (nranks < 1) return fail(GRACE_EINVAL, "nranks must be >= 1");
+  const auto mode = nranks == 1 ? grace_ctx::kSingle : grace_ctx::kVirtual;
+  return create_impl(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma, mode, nranks, 0, nranks, nullptr, out);
+}
+
+int grace_nccl_unique_id(void* out128) {
+  if (!out128) return fail(GRACE_EINVAL, "NULL argument");
+  if (!g_nccl.load()) return fail(GRACE_EUNSUPPORTED, "libnccl.so.2 not found (set GRACE_NCCL_LIB)");
+  ncclUniqueId id;
+  const ncclResult_t r = g_nccl.getUniqueId(&id);
+  if (r != 0) return fail(GRACE_ECUDA, "ncclGetUniqueId: %s", g_nccl.errStr(r));
+  std::memcpy(out128, &id, sizeof id);
+  return GRACE_OK;
+}
+
+int grace_create_dist(int nx, int ny, int nz, double dx, double dy, double dz, double Ms, double A, double Ku,
+                      double alpha, double gamma, int rank, int nranks, const void* nccl_id, grace_ctx** out) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(GRACE_EINVAL, "bad rank %d of %d", rank, nranks);
+  if (nranks == 1) return grace_create(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma, out);
+  if (!nccl_id) return fail(GRACE_EINVAL, "NULL nccl id");
+  return create_impl(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma, grace_ctx::kNccl, nranks, rank, 1, nccl_id,
+                     out);
 }
 
 void grace_destroy(grace_ctx* h) {
@@ -300,47 +585,69 @@ int grace_set_stream(grace_ctx* h, void* stream) {
 }
 
 static int finish_set_m(grace_ctx* h, int target) {
-  unsigned long long f = kNoFlag;
-  CUDA_OR(cudaMemcpyAsync(&f, h->flag + 1, sizeof f, cudaMemcpyDeviceToHost, h->stream));
-  CUDA_OR(cudaStreamSynchronize(h->stream));
-  if (f != kNoFlag) {
-    CUDA_OR(cudaMemsetAsync(h->flag + 1, 0xff, sizeof f, h->stream));
-    CUDA_OR(cudaStreamSynchronize(h->stream));
-    return fail(GRACE_EZEROCELL, "cell %llu has |M| = 0 or a non-finite component", f);
-  }
+  unsigned long long f;
+  int rc = check_flags(h, 1, &f);
+  if (rc) return rc;
+  if (f != kNoFlag) return fail(GRACE_EZEROCELL, "cell %llu has |M| = 0 or a non-finite component", f);
   h->cur = target;
   return GRACE_OK;
 }
 
 int grace_set_m(grace_ctx* h, const double* m) {
   if (!h || !m) return fail(GRACE_EINVAL, "NULL argument");
-  // stage the fp64 input in X1 (>= 24 N bytes), normalise into the spare M buffer
+  // stage the fp64 input (24 bytes/cell fits in the A buffer), normalise into the spare M buffer
   const int target = 1 - h->cur;
-  double* stage = reinterpret_cast<double*>(h->X1);
-  CUDA_OR(cudaMemcpyAsync(stage, m, sizeof(double) * 3 * (size_t)h->N, cudaMemcpyHostToDevice, h->stream));
-  CUDA_OR(launch_set_m_f64(stage, h->M[target], h->N, h->Ms, h->flag + 1, h->stream));
+  for (auto& rk : h->ranks) {
+    double* stage = reinterpret_cast<double*>(rk.A);
+    const size_t off = slab_offset(h, rk);
+    for (int c = 0; c < 3; ++c)
+      CUDA_OR(cudaMemcpyAsync(stage + c * rk.Nl, m + c * h->N + off, sizeof(double) * rk.Nl, cudaMemcpyHostToDevice,
+                              h->stream));
+    CUDA_OR(launch_set_m_f64(stage, rk.M[target], rk.Nl, h->Ms, rk.flag + 1, h->stream));
+  }
   return finish_set_m(h, target);
 }
 
 int grace_set_m_device(grace_ctx* h, const float* d_m) {
   if (!h || !d_m) return fail(GRACE_EINVAL, "NULL argument");
   const int target = 1 - h->cur;
-  CUDA_OR(launch_set_m_f32(d_m, h->M[target], h->N, (float)h->Ms, h->flag + 1, h->stream));
+  for (auto& rk : h->ranks) {
+    if (h->mode != grace_ctx::kVirtual) {
+      CUDA_OR(launch_set_m_f32(d_m, rk.M[target], rk.Nl, (float)h->Ms, rk.flag + 1, h->stream));
+    } else {
+      float* stage = reinterpret_cast<float*>(rk.A);
+      const size_t off = slab_offset(h, rk);
+      for (int c = 0; c < 3; ++c)
+        CUDA_OR(cudaMemcpyAsync(stage + c * rk.Nl, d_m + c * h->N + off, sizeof(float) * rk.Nl,
+                                cudaMemcpyDeviceToDevice, h->stream));
+      CUDA_OR(launch_set_m_f32(stage, rk.M[target], rk.Nl, (float)h->Ms, rk.flag + 1, h->stream));
+    }
+  }
   return finish_set_m(h, target);
 }
 
 int grace_get_m(grace_ctx* h, double* out) {
   if (!h || !out) return fail(GRACE_EINVAL, "NULL argument");
-  double* stage = reinterpret_cast<double*>(h->X1);
-  CUDA_OR(launch_widen(h->M[h->cur], stage, 3 * h->N, h->stream));
-  CUDA_OR(cudaMemcpyAsync(out, stage, sizeof(double) * 3 * (size_t)h->N, cudaMemcpyDeviceToHost, h->stream));
-  CUDA_OR(cudaStreamSynchronize(h->stream));
+  for (auto& rk : h->ranks) {
+    double* stage = reinterpret_cast<double*>(rk.A);
+    const size_t off = slab_offset(h, rk);
+    CUDA_OR(launch_widen(rk.M[h->cur], stage, 3 * rk.Nl, h->stream));
+    for (int c = 0; c < 3; ++c)
+      CUDA_OR(cudaMemcpyAsync(out + c * h->N + off, stage + c * rk.Nl, sizeof(double) * rk.Nl,
+                              cudaMemcpyDeviceToHost, h->stream));
+    CUDA_OR(cudaStreamSynchronize(h->stream));
+  }
   return GRACE_OK;
 }
 
 int grace_get_m_device(grace_ctx* h, float* d_out) {
   if (!h || !d_out) return fail(GRACE_EINVAL, "NULL argument");
-  CUDA_OR(cudaMemcpyAsync(d_out, h->M[h->cur], sizeof(float) * 3 * (size_t)h->N, cudaMemcpyDeviceToDevice, h->stream));
+  for (auto& rk : h->ranks) {
+    const size_t off = slab_offset(h, rk);
+    for (int c = 0; c < 3; ++c)
+      CUDA_OR(cudaMemcpyAsync(d_out + c * h->N + off, rk.M[h->cur] + c * rk.Nl, sizeof(float) * rk.Nl,
+                              cudaMemcpyDeviceToDevice, h->stream));
+  }
   CUDA_OR(cudaStreamSynchronize(h->stream));
   return GRACE_OK;
 }
@@ -363,27 +670,25 @@ int grace_set_alpha(grace_ctx* h, double alpha) {
 
 int grace_heff(grace_ctx* h, double* out) {
   if (!h || !out) return fail(GRACE_EINVAL, "NULL argument");
-  const Geom& g = h->g;
   cudaStream_t s = h->stream;
-  if (!h->Hbuf) {
-    int rc = h->alloc((void**)&h->Hbuf, sizeof(float) * 3 * (size_t)h->N);
-    if (rc) return rc;
+  for (auto& rk : h->ranks)
+    if (!rk.Hbuf) {
+      int rc = h->alloc((void**)&rk.Hbuf, sizeof(float) * 3 * (size_t)rk.Nl);
+      if (rc) return rc;
+    }
+  CUDA_OR(h->upload_params(1e-15));
+  CUDA_OR(h->demag_stages(h->cur, s, false));
+  for (auto& rk : h->ranks)
+    CUDA_OR(launch_k5(rk.g, 1, rk.A, rk.M[h->cur], nullptr, rk.Hbuf, h->tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+  for (auto& rk : h->ranks) {
+    double* stage = reinterpret_cast<double*>(rk.A);
+    const size_t off = slab_offset(h, rk);
+    CUDA_OR(launch_widen(rk.Hbuf, stage, 3 * rk.Nl, s));
+    for (int c = 0; c < 3; ++c)
+      CUDA_OR(cudaMemcpyAsync(out + c * h->N + off, stage + c * rk.Nl, sizeof(double) * rk.Nl,
+                              cudaMemcpyDeviceToHost, s));
+    CUDA_OR(cudaStreamSynchronize(s));
   }
-  h->fill_params(1e-15);
-  CUDA_OR(cudaMemcpyAsync(h->prm, &h->hprm, sizeof(StepParams), cudaMemcpyHostToDevice, s));
-  CUDA_OR(launch_k1(g, h->M[h->cur], h->X1, h->tw, nullptr, s));
-  if (h->fused) {
-    CUDA_OR(launch_k2f(g, h->X1, h->KS, h->tw, s));
-  } else {
-    CUDA_OR(launch_k2(g, h->X1, h->X2, h->tw, s));
-    CUDA_OR(launch_k3(g, h->X2, h->KS, h->tw, s));
-    CUDA_OR(launch_k4(g, h->X2, h->X1, h->tw, s));
-  }
-  CUDA_OR(launch_k5(g, 1, h->X1, h->M[h->cur], nullptr, h->Hbuf, h->tw, h->prm, h->flag, s));
-  double* stage = reinterpret_cast<double*>(h->X1);
-  CUDA_OR(launch_widen(h->Hbuf, stage, 3 * h->N, s));
-  CUDA_OR(cudaMemcpyAsync(out, stage, sizeof(double) * 3 * (size_t)h->N, cudaMemcpyDeviceToHost, s));
-  CUDA_OR(cudaStreamSynchronize(s));
   return GRACE_OK;
 }
 
@@ -393,10 +698,15 @@ int grace_step(grace_ctx* h, int n, double dt) {
   if (!finite_pos(dt)) return fail(GRACE_EINVAL, "dt must be finite and > 0");
   if (n == 0) return GRACE_OK;
   cudaStream_t s = h->stream;
-  h->fill_params(dt);
-  CUDA_OR(cudaMemcpyAsync(h->prm, &h->hprm, sizeof(StepParams), cudaMemcpyHostToDevice, s));
-  const int nk = kernel_count(h->g);
-  if (h->profiling) {
+  CUDA_OR(h->upload_params(dt));
+  const int nk = kernel_count(h->g0);
+  if (h->mode != grace_ctx::kSingle) {
+    for (int i = 0; i < n; ++i) {
+      cudaError_t e = h->enqueue_step(h->cur, s);
+      if (e != cudaSuccess) return fail(GRACE_ECUDA, "distributed step: %s", cudaGetErrorString(e));
+      h->cur ^= 1;
+    }
+  } else if (h->profiling) {
     // eager launches with an event pair around every kernel; events are read in
     // batches of kProfBatch steps so the host never waits inside a batch
     constexpr int kProfBatch = 64;
@@ -437,15 +747,13 @@ int grace_step(grace_ctx* h, int n, double dt) {
       h->cur ^= (done & 1);
     }
   }
-  unsigned long long f = kNoFlag;
-  CUDA_OR(cudaMemcpyAsync(&f, h->flag, sizeof f, cudaMemcpyDeviceToHost, s));
-  CUDA_OR(cudaStreamSynchronize(s));
+  unsigned long long f;
+  int rc = check_flags(h, 0, &f);
+  if (rc) return rc;
   h->steps += n;
   if (f != kNoFlag) {
     h->nf_step = (long long)(f >> 36);
     h->nf_cell = (long long)(f & ((1ULL << 36) - 1));
-    CUDA_OR(cudaMemsetAsync(h->flag, 0xff, sizeof f, s));
-    CUDA_OR(cudaStreamSynchronize(s));
     return fail(GRACE_ENONFINITE, "non-finite magnetisation at step %lld, cell %lld (dt too large?)", h->nf_step,
                 h->nf_cell);
   }
@@ -454,9 +762,20 @@ int grace_step(grace_ctx* h, int n, double dt) {
 
 int grace_mavg(grace_ctx* h, double* out3) {
   if (!h || !out3) return fail(GRACE_EINVAL, "NULL argument");
-  CUDA_OR(launch_mavg(h->M[h->cur], h->N, h->Ms, h->red, h->red + kMavgPartials, h->stream));
-  CUDA_OR(cudaMemcpyAsync(out3, h->red + kMavgPartials, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  CUDA_OR(cudaStreamSynchronize(h->stream));
+  double acc[3] = {0, 0, 0};
+  for (auto& rk : h->ranks) {
+    double part[3];
+    CUDA_OR(launch_mavg(rk.M[h->cur], rk.Nl, h->Ms, rk.red, rk.red + kMavgPartials, h->stream));
+    if (h->mode == grace_ctx::kNccl) {
+      const ncclResult_t r = g_nccl.allReduce(rk.red + kMavgPartials, rk.red + kMavgPartials, 3, kNcclFloat64,
+                                              kNcclSum, h->comm, h->stream);
+      if (r != 0) return fail(GRACE_ECUDA, "ncclAllReduce: %s", g_nccl.errStr(r));
+    }
+    CUDA_OR(cudaMemcpyAsync(part, rk.red + kMavgPartials, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_OR(cudaStreamSynchronize(h->stream));
+    for (int q = 0; q < 3; ++q) acc[q] += part[q];
+  }
+  for (int q = 0; q < 3; ++q) out3[q] = acc[q] / h->P;  // equal slabs: mean of the slab means
   return GRACE_OK;
 }
 
@@ -475,8 +794,17 @@ int grace_last_nonfinite(grace_ctx* h, long long* step, long long* cell) {
 
 int grace_geometry(grace_ctx* h, long long* o) {
   if (!h || !o) return fail(GRACE_EINVAL, "NULL argument");
-  const Geom& g = h->g;
+  const Geom& g = h->g0;
   const long long v[12] = {g.nx, g.ny, g.nz, g.Px, g.Py, g.Pz, g.Kx, g.Kxp, g.Kyh, g.Kzh, g.KSp, kernel_count(g)};
+  std::memcpy(o, v, sizeof v);
+  return GRACE_OK;
+}
+
+int grace_partition(grace_ctx* h, long long* o) {
+  if (!h || !o) return fail(GRACE_EINVAL, "NULL argument");
+  const Geom& g = h->ranks[0].g;
+  const long long v[8] = {h->P, h->ranks[0].r, g.nzl, (long long)h->ranks[0].r * g.nzl, g.kb, g.Kc, g.pitch1,
+                          g.pitch2};
   std::memcpy(o, v, sizeof v);
   return GRACE_OK;
 }
@@ -506,9 +834,10 @@ int grace_tensor_octant(int nx, int ny, int nz, double dx, double dy, double dz,
 
 int grace_kernel_spectrum(grace_ctx* h, float* out) {
   if (!h || !out) return fail(GRACE_EINVAL, "NULL argument");
-  const Geom& g = h->g;
-  CUDA_OR(cudaMemcpyAsync(out, h->KS, sizeof(float) * 6 * (size_t)g.Kzh * g.Kyh * g.KSp, cudaMemcpyDeviceToHost,
-                          h->stream));
+  if (h->P != 1) return fail(GRACE_EUNSUPPORTED, "kernel spectrum copy is single-rank only");
+  const Geom& g = h->g0;
+  CUDA_OR(cudaMemcpyAsync(out, h->ranks[0].KS, sizeof(float) * 6 * (size_t)g.Kzh * g.Kyh * g.KSp,
+                          cudaMemcpyDeviceToHost, h->stream));
   CUDA_OR(cudaStreamSynchronize(h->stream));
   return GRACE_OK;
 }
@@ -521,7 +850,7 @@ int grace_set_profiling(grace_ctx* h, int on) {
 
 int grace_kernel_times(grace_ctx* h, double* ms, long long* launches, int* nk, int reset) {
   if (!h || !nk) return fail(GRACE_EINVAL, "NULL argument");
-  const int k = kernel_count(h->g);
+  const int k = kernel_count(h->g0);
   const int cap = *nk;
   *nk = k;
   for (int i = 0; i < k && i < cap; ++i) {

@@ -21,13 +21,22 @@ struct StepParams {
 
 // Geometry and the constant material coefficients (fp32, rounded once from fp64 on the host).
 struct Geom {
-  int nx, ny, nz;
+  int nx, ny, nz;   // global grid
   int Px, Py, Pz;   // padded FFT sizes (power of two >= 2n-1, 1 for a singleton axis)
   int Kx;           // Px/2 + 1 complex outputs of the x R2C (1 when Px == 1)
-  int Kxp;          // complex row pitch of X1/X2
+  int Kxp;          // complex row pitch of X1/X2 on a single GPU
   int Kyh, Kzh;     // Py/2 + 1, Pz/2 + 1 (1 for a singleton axis): folded spectrum extents
-  int KSp;          // float row pitch of the spectral table KS
+  int KSp;          // float row pitch of this rank's spectral table KS
   int Lmax;         // length of the twiddle table
+  // z-slab partition.  Single GPU: nzl = nz, pitch1 = pitch2 = Kxp,
+  // kb = 0 (no kx blocks), Kc = Kx, no halos.
+  int nzl;          // z planes owned by this rank (K1 / K5 rows)
+  int pitch1;       // row pitch of the x-row layouts (K1 out, K2 in, K4 out, K5 in)
+  int kb;           // kx block of the all-to-all (0: unblocked)
+  long long blk1;   // complex elements per kx block of an x-row layout (3 nzl ny pitch1)
+  int Kc;           // kx columns handled by K2..K4 on this rank
+  int pitch2;       // row pitch of X2
+  int has_lo, has_hi;  // z-1 / z+1 halo planes present
   float cx, cy, cz; // exchange 2A/(mu0 Ms^2 d^2) per axis (0 for a singleton axis)
   float ck;         // anisotropy 2Ku/(mu0 Ms^2)
   float Ms;
@@ -39,13 +48,17 @@ constexpr unsigned long long kNoFlag = ~0ull;
 // K1 also advances bump->step (nullptr: no step, e.g. grace_heff).
 cudaError_t launch_k1(const Geom& g, const float* M, float2* X1, const float2* tw, StepParams* bump,
                       cudaStream_t st);
+// K2 in / K4 out use the x-row layout (pitch1, slabs of nzl planes per kx block);
+// X2 is [3][nz][Py][pitch2] over this rank's Kc columns.
 cudaError_t launch_k2(const Geom& g, const float2* X1, float2* X2, const float2* tw, cudaStream_t st);
 cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* tw, cudaStream_t st);
 cudaError_t launch_k4(const Geom& g, const float2* X2, float2* X1, const float2* tw, cudaStream_t st);
 cudaError_t launch_k2f(const Geom& g, float2* X1, const float* KS, const float2* tw, cudaStream_t st);
 // mode 0: LLG Euler step M -> Mn; mode 1: store H_eff into Hout.
+// Hlo / Hhi: halo planes [3][ny][nx] of z-1 / z+1 (used when g.has_lo / g.has_hi).
 cudaError_t launch_k5(const Geom& g, int mode, const float2* X1, const float* M, float* Mn, float* Hout,
-                      const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st);
+                      const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st,
+                      const float* Hlo = nullptr, const float* Hhi = nullptr);
 bool fused_y_path(const Geom& g);  // nz == 1 and the y-pencils of 3 components fit one CTA
 int kernel_count(const Geom& g);   // kernels per step
 

@@ -83,19 +83,19 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // K1: x R2C.  A real row of Px (nx nonzero) is packed as z[n] = x[2n] + i x[2n+1],
 // a length-L = Px/2 complex FFT gives Z, and
 //   X[k] = (Z[k] + conj Z[L-k])/2 - (i/2) w^k (Z[k] - conj Z[L-k]),  w = exp(-2 pi i/Px), k = 0..L.
-template <int L, int B, int NT>
+template <int L, int B, int NT, bool DIST>
 __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k1_fwd_x(const float* __restrict__ M, float2* __restrict__ X1,
                                                const float2* __restrict__ tw, Geom g, StepParams* bump) {
   extern __shared__ float2 smem[];
   // The step index lives on the device so captured graphs stay valid: K1 of each
   // step advances it, K5 of the same step reads step - 1.
   if (bump != nullptr && blockIdx.x == 0 && threadIdx.x == 0) bump->step += 1;
-  const int nrows = 3 * g.nz * g.ny;
+  const int nrows = 3 * g.nzl * g.ny;
   const int row0 = blockIdx.x * B;
   if constexpr (L == 0) {  // Px == 1: X[0] = x[0]
     for (int b = threadIdx.x; b < B; b += NT) {
       const int row = row0 + b;
-      if (row < nrows) X1[(size_t)row * g.Kxp] = make_float2(__ldg(M + row), 0.f);
+      if (row < nrows) X1[(size_t)row * g.pitch1] = make_float2(__ldg(M + row), 0.f);
     }
   } else {
     struct Ld {
@@ -128,9 +128,23 @@ __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k1_fwd_x(const float* __re
       const float2 E = make_float2(0.5f * (Zk.x + Zn.x), 0.5f * (Zk.y - Zn.y));
       const float2 D = make_float2(0.5f * (Zk.x - Zn.x), 0.5f * (Zk.y + Zn.y));
       const float2 wD = cmul(__ldg(tw + k * twpx), D);
-      X1[(size_t)row * g.Kxp + k] = make_float2(E.x + wD.y, E.y - wD.x);
+      const float2 Xk = make_float2(E.x + wD.y, E.y - wD.x);
+      if constexpr (DIST) {  // destination-blocked for the all-to-all: block k / kb
+        const int q = k / g.kb;
+        X1[q * g.blk1 + (size_t)row * g.pitch1 + (k - q * g.kb)] = Xk;
+      } else {
+        X1[(size_t)row * g.pitch1 + k] = Xk;
+      }
     }
   }
+}
+
+// Offset of the (component, global z) slab of an x-row layout: kx block
+// z / nzl (the source / destination rank of the all-to-all), plane z % nzl.
+__device__ __forceinline__ size_t xrow_slab(const Geom& g, int slab) {
+  const int c = slab / g.nz, z = slab - c * g.nz;
+  const int q = z / g.nzl, zl = z - q * g.nzl;
+  return ((size_t)(q * 3 + c) * g.nzl + zl) * g.ny * g.pitch1;
 }
 
 // ---------------------------------------------------------------------------
@@ -151,7 +165,8 @@ __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k_y(const float2* __restri
       const int i = ib + C;
       return (i < n_in && b < ncol_valid) ? __ldg(p + (b + i * pitch)) : make_float2(0.f, 0.f);
     }
-  } ld{in + slab * in_rows * g.Kxp + kx0, g.Kxp, n_in, g.Kx - kx0};
+  } ld{in + (!INV ? xrow_slab(g, (int)slab) : slab * in_rows * g.pitch2) + kx0, !INV ? g.pitch1 : g.pitch2, n_in,
+       g.Kc - kx0};
   struct St {
     __device__ static constexpr bool kSmem() { return false; }
     float2* p;
@@ -160,7 +175,8 @@ __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k_y(const float2* __restri
       const int i = ib + C;
       if (i < n_out && b < ncol_valid) p[b + i * pitch] = v;
     }
-  } st{out + slab * out_rows * g.Kxp + kx0, g.Kxp, n_out, g.Kx - kx0};
+  } st{out + (INV ? xrow_slab(g, (int)slab) : slab * out_rows * g.pitch2) + kx0, INV ? g.pitch1 : g.pitch2, n_out,
+       g.Kc - kx0};
   fft_tile<L, NCOL, NT, true, INV, !INV && (L > 1), INV && (L > 1)>(smem, ld, st, tw, g.Lmax / L);
 }
 
@@ -175,9 +191,9 @@ __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k3_z(float2* __restrict__ 
   constexpr int NCOL = 3 * B;
   const int kx0 = blockIdx.x * B;
   const int kyf = blockIdx.y;
-  const int zstride = g.Py * g.Kxp;                   // between z planes
+  const int zstride = g.Py * g.pitch2;                // between z planes
   const size_t cstride = (size_t)g.nz * zstride;      // between components
-  const int nvalid = g.Kx - kx0;
+  const int nvalid = g.Kc - kx0;
   const int nky = (kyf == 0 || 2 * kyf == g.Py) ? 1 : 2;
   // Stage this CTA's folded KS slice (6 comps x Kzh x B) in smem with cp.async;
   // it lands while the first forward z-FFT runs and serves both ky and Py-ky.
@@ -201,7 +217,7 @@ __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k3_z(float2* __restrict__ 
   }
   for (int rep = 0; rep < nky; ++rep) {
     const int ky = rep == 0 ? kyf : g.Py - kyf;
-    float2* base = X2 + (size_t)ky * g.Kxp + kx0;
+    float2* base = X2 + (size_t)ky * g.pitch2 + kx0;
     struct Ld {
       __device__ static constexpr bool kSmem() { return false; }
       const float2* p;
@@ -248,9 +264,9 @@ __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k3_z(float2* __restrict__ 
 __global__ void k_mul_plane(float2* __restrict__ X2, const float* __restrict__ KS, Geom g) {
   const int kx = blockIdx.x * blockDim.x + threadIdx.x;
   const int ky = blockIdx.y;
-  if (kx >= g.Kx) return;
-  const size_t cs = (size_t)g.Py * g.Kxp;
-  float2* p = X2 + (size_t)ky * g.Kxp + kx;
+  if (kx >= g.Kc) return;
+  const size_t cs = (size_t)g.Py * g.pitch2;
+  float2* p = X2 + (size_t)ky * g.pitch2 + kx;
   float2 a = p[0], b = p[cs], c = p[2 * cs];
   kmul3(a, b, c, KS, g, 0, ky, kx);
   p[0] = a;
@@ -316,24 +332,25 @@ __device__ __forceinline__ float3 ld3(const float* __restrict__ M, size_t N, siz
   return make_float3(__ldg(M + i), __ldg(M + N + i), __ldg(M + 2 * N + i));
 }
 
-template <int L, int B, int NT>
+template <int L, int B, int NT, bool DIST>
 __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k5_inv_x_llg(const float2* __restrict__ X1, const float* __restrict__ M,
                                                    float* __restrict__ Mn, float* __restrict__ Hout,
                                                    const float2* __restrict__ tw, Geom g,
                                                    const StepParams* __restrict__ prm,
-                                                   unsigned long long* __restrict__ flag, int mode) {
+                                                   unsigned long long* __restrict__ flag, int mode,
+                                                   const float* __restrict__ Hlo, const float* __restrict__ Hhi) {
   extern __shared__ float2 smem[];
   constexpr int NCOL = 3 * B;
-  const int nrows = g.nz * g.ny;
+  const int nrows = g.nzl * g.ny;
   const int row0 = blockIdx.x * B;
   const size_t N = (size_t)nrows * g.nx;
-  const size_t cstrideX = (size_t)nrows * g.Kxp;  // X1 component stride
+  const size_t cstrideX = (size_t)nrows * g.pitch1;  // X1 component stride
   float* hs = reinterpret_cast<float*>(smem);      // H_demag rows [3B][2L] (reals), aliasing the tile
   if constexpr (L == 0) {
     for (int col = threadIdx.x; col < NCOL; col += NT) {
       const int c = col / B, b = col - c * B;
       const int row = row0 + b;
-      hs[col] = row < nrows ? __ldg(X1 + c * cstrideX + (size_t)row * g.Kxp).x : 0.f;
+      hs[col] = row < nrows ? __ldg(X1 + c * cstrideX + (size_t)row * g.pitch1).x : 0.f;
     }
   } else {
     const int twpx = g.Lmax / (2 * L);
@@ -342,14 +359,23 @@ __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k5_inv_x_llg(const float2*
       const float2* X;
       const float2* tw;
       size_t cs;
-      int row0, nrows, pitch, twpx;
+      int row0, nrows, pitch, twpx, kb;
+      long long blk1;
       __device__ float2 operator()(int col, int ib, int C) const {
         const int k = ib + C;
         const int c = col / B, b = col - c * B;
         const int row = row0 + b;
         if (row >= nrows) return make_float2(0.f, 0.f);
         const float2* p = X + c * cs + (size_t)row * pitch;
-        const float2 a = __ldg(p + k), m = __ldg(p + (L - k));
+        float2 a, m;
+        if constexpr (DIST) {  // gather from the source kx blocks of the all-to-all
+          const int qa = k / kb, qm = (L - k) / kb;
+          a = __ldg(p + qa * blk1 + (k - qa * kb));
+          m = __ldg(p + qm * blk1 + ((L - k) - qm * kb));
+        } else {
+          a = __ldg(p + k);
+          m = __ldg(p + (L - k));
+        }
         const float2 S = make_float2(a.x + m.x, a.y - m.y);  // X[k] + conj X[L-k]
         const float2 D = make_float2(a.x - m.x, a.y + m.y);  // X[k] - conj X[L-k]
         float2 w = __ldg(tw + k * twpx);                       // exp(-2 pi i k/Px)
@@ -357,7 +383,7 @@ __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k5_inv_x_llg(const float2*
         const float2 wD = cmul(w, D);
         return make_float2(S.x - wD.y, S.y + wD.x);            // S + i wD
       }
-    } ld{X1, tw, cstrideX, row0, nrows, g.Kxp, twpx};
+    } ld{X1, tw, cstrideX, row0, nrows, g.pitch1, twpx, g.kb, g.blk1};
     struct St {
       __device__ static constexpr bool kSmem() { return true; }
       float* hs;
@@ -403,8 +429,10 @@ __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k5_inv_x_llg(const float2*
       q[c][1] = ld3(M, N, xx + 1 < g.nx ? i + 1 : i);
       q[c][2] = ld3(M, N, y > 0 ? i - g.nx : i);
       q[c][3] = ld3(M, N, y + 1 < g.ny ? i + g.nx : i);
-      q[c][4] = ld3(M, N, z > 0 ? i - plane : i);
-      q[c][5] = ld3(M, N, z + 1 < g.nz ? i + plane : i);
+      if (DIST && z == 0 && g.has_lo) q[c][4] = ld3(Hlo, plane, (size_t)y * g.nx + xx);
+      else q[c][4] = ld3(M, N, z > 0 ? i - plane : i);
+      if (DIST && z + 1 == g.nzl && g.has_hi) q[c][5] = ld3(Hhi, plane, (size_t)y * g.nx + xx);
+      else q[c][5] = ld3(M, N, z + 1 < g.nzl ? i + plane : i);
     }
 #pragma unroll
     for (int c = 0; c < CPI; ++c) {
@@ -508,24 +536,28 @@ static cudaError_t prep(K kern, size_t smem) {
     default: return cudaErrorInvalidValue; \
   }
 
-template <int L>
+template <int L, bool DIST>
 static cudaError_t k1_launch(const Geom& g, const float* M, float2* X1, const float2* tw, StepParams* bump,
                              cudaStream_t st) {
   constexpr int B = XCfg<L>::B1, NT = XCfg<L>::NT1;
   const size_t smem = (L == 0) ? 0 : (size_t)TileIdx<(L > 0 ? L : 1), B, false>::SMEM_ELEMS * sizeof(float2);
-  auto kern = k1_fwd_x<L, B, NT>;
+  auto kern = k1_fwd_x<L, B, NT, DIST>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
-  const int nrows = 3 * g.nz * g.ny;
+  const int nrows = 3 * g.nzl * g.ny;
   kern<<<(nrows + B - 1) / B, NT, smem, st>>>(M, X1, tw, g, bump);
   return cudaGetLastError();
 }
 
 cudaError_t launch_k1(const Geom& g, const float* M, float2* X1, const float2* tw, StepParams* bump,
                       cudaStream_t st) {
-  if (g.Px == 1) return k1_launch<0>(g, M, X1, tw, bump, st);
+  if (g.Px == 1) return g.kb ? k1_launch<0, true>(g, M, X1, tw, bump, st) : k1_launch<0, false>(g, M, X1, tw, bump, st);
   const int L = g.Px / 2;
-#define CASE(v) case v: return (v >= 2) ? k1_launch<(v >= 2 ? v : 2)>(g, M, X1, tw, bump, st) : cudaErrorInvalidValue;
+#define CASE(v)                                                                                         \
+  case v:                                                                                               \
+    return (v < 2) ? cudaErrorInvalidValue                                                              \
+           : g.kb  ? k1_launch<(v >= 2 ? v : 2), true>(g, M, X1, tw, bump, st)                          \
+                   : k1_launch<(v >= 2 ? v : 2), false>(g, M, X1, tw, bump, st);
   GRACE_L_SWITCH(L, CASE)
 #undef CASE
 }
@@ -538,7 +570,7 @@ static cudaError_t ky_launch(const Geom& g, const float2* in, float2* out, const
   auto kern = k_y<L, NCOL, NT, INV>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((g.Kx + NCOL - 1) / NCOL, 3 * g.nz);
+  dim3 grid((g.Kc + NCOL - 1) / NCOL, 3 * g.nz);
   kern<<<grid, NT, smem, st>>>(in, out, tw, g, in_rows, out_rows, n_in, n_out);
   return cudaGetLastError();
 }
@@ -563,14 +595,14 @@ static cudaError_t k3_launch(const Geom& g, float2* X2, const float* KS, const f
   auto kern = k3_z<L, B, NT>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((g.Kx + B - 1) / B, g.Kyh);
+  dim3 grid((g.Kc + B - 1) / B, g.Kyh);
   kern<<<grid, NT, smem, st>>>(X2, KS, tw, g);
   return cudaGetLastError();
 }
 
 cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* tw, cudaStream_t st) {
   if (g.Pz == 1) {
-    dim3 grid((g.Kx + 127) / 128, g.Py);
+    dim3 grid((g.Kc + 127) / 128, g.Py);
     k_mul_plane<<<grid, 128, 0, st>>>(X2, KS, g);
     return cudaGetLastError();
   }
@@ -599,25 +631,33 @@ cudaError_t launch_k2f(const Geom& g, float2* X1, const float* KS, const float2*
 #undef CASE
 }
 
-template <int L>
+template <int L, bool DIST>
 static cudaError_t k5_launch(const Geom& g, int mode, const float2* X1, const float* M, float* Mn, float* Hout,
-                             const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st) {
+                             const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st,
+                             const float* Hlo, const float* Hhi) {
   constexpr int B = XCfg<L>::B5, NT = XCfg<L>::NT5;
   const size_t smem = (L == 0) ? (size_t)3 * B * sizeof(float)
                                : (size_t)TileIdx<(L > 0 ? L : 1), 3 * B, false>::SMEM_ELEMS * sizeof(float2);
-  auto kern = k5_inv_x_llg<L, B, NT>;
+  auto kern = k5_inv_x_llg<L, B, NT, DIST>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
-  const int nrows = g.nz * g.ny;
-  kern<<<(nrows + B - 1) / B, NT, smem, st>>>(X1, M, Mn, Hout, tw, g, prm, flag, mode);
+  const int nrows = g.nzl * g.ny;
+  kern<<<(nrows + B - 1) / B, NT, smem, st>>>(X1, M, Mn, Hout, tw, g, prm, flag, mode, Hlo, Hhi);
   return cudaGetLastError();
 }
 
 cudaError_t launch_k5(const Geom& g, int mode, const float2* X1, const float* M, float* Mn, float* Hout,
-                      const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st) {
-  if (g.Px == 1) return k5_launch<0>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st);
+                      const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st,
+                      const float* Hlo, const float* Hhi) {
+  if (g.Px == 1)
+    return g.kb ? k5_launch<0, true>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi)
+                : k5_launch<0, false>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi);
   const int L = g.Px / 2;
-#define CASE(v) case v: return (v >= 2) ? k5_launch<(v >= 2 ? v : 2)>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st) : cudaErrorInvalidValue;
+#define CASE(v)                                                                                                 \
+  case v:                                                                                                       \
+    return (v < 2) ? cudaErrorInvalidValue                                                                      \
+           : g.kb  ? k5_launch<(v >= 2 ? v : 2), true>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi)   \
+                   : k5_launch<(v >= 2 ? v : 2), false>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi);
   GRACE_L_SWITCH(L, CASE)
 #undef CASE
 }

@@ -1,0 +1,86 @@
+"""Distributed z-slab path on one GPU: P virtual ranks vs the single-GPU path.
+
+grace_create_virtual runs the partitioned algorithm (K1 per slab, all-to-all to
+kx blocks, K2..K4 per block, all-to-all back, halo planes, K5 per slab) with
+device copies standing in for NCCL, so every index, pack and halo rule of the
+distributed step is exercised here.  The per-pencil arithmetic
+is the same, so H_eff and M(t) must agree with the single path to fp32
+round-off (observed: bitwise), and with the oracle.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import paper_1411_2565_b200 as pb  # noqa: E402
+from paper_1411_2565_b200.dist import partition  # noqa: E402
+from oracle.demag import DemagFFT  # noqa: E402
+from oracle.fields import heff as oracle_heff  # noqa: E402
+from oracle.tensor import tensor_octant  # noqa: E402
+from workloads import GAMMA0, random_m  # noqa: E402
+
+CASES = [
+    ((16, 12, 8), (1e-9, 1e-9, 1e-9), (2, 4, 8)),
+    ((100, 20, 4), (5e-9, 5e-9, 3e-9), (2, 4)),
+    ((7, 5, 6), (1e-9, 2e-9, 1e-9), (2, 3, 6)),
+    ((2, 3, 4), (1e-9, 1e-9, 1e-9), (4,)),       # Kx = 3 < 4 ranks: an empty kx block
+    ((64, 48, 16), (2e-9, 2e-9, 2e-9), (2, 8)),
+]
+
+
+@pytest.mark.parametrize("n,d,Ps", CASES)
+def test_virtual_ranks_match_single_and_oracle(n, d, Ps):
+    Ms, A, Ku, alpha = 8e5, 1.3e-11, 2e4, 0.3
+    hext = (1e4, -2e3, 5e3)
+    M = random_m(n, Ms, seed=31)
+    ref = pb.Grace(n, d, Ms, A, Ku, alpha, GAMMA0)
+    ref.set_m(M)
+    ref.set_hext(hext)
+    H1 = ref.heff()
+    Ho = oracle_heff(M, DemagFFT(tensor_octant(*n, *d)), A, Ms, Ku, d, hext)
+    assert np.linalg.norm(H1 - Ho) <= 1e-5 * np.linalg.norm(Ho)
+    ref.step(7, 1e-14)
+    M1 = ref.get_m()
+    m1 = ref.mavg()
+    for P in Ps:
+        g = pb.Grace(n, d, Ms, A, Ku, alpha, GAMMA0, virtual_ranks=P)
+        part = pb.grace_partition(g.h)
+        want = partition(n[0], n[2], 0, P)
+        assert (part["P"], part["nz_local"], part["kx_block"], part["kx_columns"]) == \
+            (P, want.nz_local, want.kx_block, want.kx_columns)
+        g.set_m(M)
+        g.set_hext(hext)
+        H = g.heff()
+        assert np.abs(H - H1).max() <= 1e-6 * np.abs(H1).max(), P
+        g.step(7, 1e-14)
+        Mp = g.get_m()
+        assert np.abs(Mp - M1).max() <= 1e-6 * Ms, P
+        np.testing.assert_allclose(g.mavg(), m1, rtol=0, atol=1e-9)
+        g.close()
+    ref.close()
+
+
+def test_virtual_ranks_bitwise_on_slab_like_grid():
+    n, d = (128, 64, 16), (1e-9, 1e-9, 1e-9)
+    M = random_m(n, 1e6, seed=3)
+    out = []
+    for P in (None, 4):
+        g = pb.Grace(n, d, 1e6, 1e-11, 6.2832e4, 0.5, GAMMA0, virtual_ranks=P)
+        g.set_m(M)
+        g.step(5, 1e-15)
+        out.append(g.get_m())
+        g.close()
+    assert np.array_equal(out[0], out[1])
+
+
+def test_virtual_errors():
+    with pytest.raises(pb.GraceError) as e:
+        pb.Grace((8, 8, 6), (1e-9,) * 3, 8e5, 1e-11, 0, 0.5, GAMMA0, virtual_ranks=4)
+    assert e.value.code == pb.GRACE_EINVAL
+    g = pb.Grace((8, 4, 4), (1e-9,) * 3, 8e5, 1e-11, 0, 0.5, GAMMA0, virtual_ranks=2)
+    M = random_m((8, 4, 4), 8e5, seed=1)
+    M[:, 3, 1, 2] = 0.0  # cell ((3*4)+1)*8+2 = 106, in rank 1's slab
+    with pytest.raises(pb.GraceError) as e:
+        g.set_m(M)
+    assert e.value.code == pb.GRACE_EZEROCELL and "cell 106" in str(e.value)
+    g.close()
