@@ -160,6 +160,17 @@ __device__ __forceinline__ void dft_halfout(float2* a) {
   }
 }
 
+// Radix plan of an L-point transform; REV runs the same radices in reverse
+// order (an inverse that starts with the forward's last radix keeps every
+// thread's elements in place across a fused forward-last / inverse-first pass).
+template <int L, bool REV>
+struct Plan {
+  static constexpr int NP = fft_npass(L);
+  __host__ __device__ static constexpr int bits(int p) { return fft_pass_bits(L, REV ? NP - 1 - p : p); }
+  __host__ __device__ static constexpr int R(int p) { return 1 << bits(p); }
+  __host__ __device__ static constexpr int NS(int p) { return p == 0 ? 1 : NS(p - 1) * R(p - 1); }
+};
+
 // Shared-memory tile addressing.  A tile holds NCOL columns of ROWS rows; row
 // stride RS and column stride CS depend on the mode:
 //   COLMODE: element (b, row) at row*NCOL + b   (RS = NCOL, CS = 1)
@@ -168,36 +179,43 @@ __device__ __forceinline__ void dft_halfout(float2* a) {
 // one row per R0 rows ("PAD" layout, row(i) = i + i/R0) when that stride would
 // hit one bank; every other interface, and the caller-visible layout used by
 // SmemLd/SmemSt, is linear, so offsets of the compile-time butterfly pattern
-// fold into immediates.
-template <int L, int NCOL, bool COLMODE>
+// fold into immediates.  V components are V consecutive tiles of ELEMS each.
+template <int L, int NCOL, bool COLMODE, int R0 = fft_rmax(L)>
 struct TileIdx {
-  static constexpr int R0 = fft_rmax(L);
+  static constexpr int R0v = R0;
   static constexpr int SH = ilog2(R0);
   static constexpr bool PAD = (L >= 16) && (COLMODE ? NCOL < 16 : true);
-  static constexpr int ROWS = L + (PAD ? L / R0 : 0);
-  static constexpr int SMEM_ELEMS = NCOL * ROWS;
   static constexpr int RS = COLMODE ? NCOL : 1;
+  // rows reserved per column: enough for the padding of either radix order
+  // (the smallest radix of the plan pads the most)
+  static constexpr int RMIN = L <= 1 ? 1 : 1 << fft_pass_bits(L, fft_npass(L) - 1);
+  static constexpr int ROWS = L + (PAD ? L / RMIN : 0);
+  static constexpr int ELEMS = NCOL * ROWS;
+  static constexpr int SMEM_ELEMS = ELEMS;
   static constexpr int CS = COLMODE ? 1 : ROWS;
-  __device__ __forceinline__ static int at(int b, int i) { return b * CS + i * RS; }     // linear
+  __device__ __forceinline__ static int at(int b, int i) { return b * CS + i * RS; }  // linear
   __device__ __forceinline__ static int padrow(int i) { return PAD ? i + (i >> SH) : i; }
 };
 
-// Caller-visible smem accessors (linear layout).  Interface of all accessors:
-// element index i = ib + C, ib per thread, C a compile-time constant after unrolling.
+// Caller-visible smem accessors (linear layout, component v in tile v).
+// Interface of all accessors: element i = ib + C of component v of column b,
+// ib per thread, C a compile-time constant after unrolling.
 template <int L, int NCOL, bool COLMODE>
 struct SmemLd {
   __device__ static constexpr bool kSmem() { return true; }
   float2* s;
-  __device__ __forceinline__ float2 operator()(int b, int ib, int C) const {
-    return s[TileIdx<L, NCOL, COLMODE>::at(b, ib) + C * TileIdx<L, NCOL, COLMODE>::RS];
+  __device__ __forceinline__ float2 operator()(int b, int v, int ib, int C) const {
+    using T = TileIdx<L, NCOL, COLMODE>;
+    return s[v * T::ELEMS + T::at(b, ib) + C * T::RS];
   }
 };
 template <int L, int NCOL, bool COLMODE>
 struct SmemSt {
   __device__ static constexpr bool kSmem() { return true; }
   float2* s;
-  __device__ __forceinline__ void operator()(int b, int ib, int C, float2 v) const {
-    s[TileIdx<L, NCOL, COLMODE>::at(b, ib) + C * TileIdx<L, NCOL, COLMODE>::RS] = v;
+  __device__ __forceinline__ void operator()(int b, int v, int ib, int C, float2 x) const {
+    using T = TileIdx<L, NCOL, COLMODE>;
+    s[v * T::ELEMS + T::at(b, ib) + C * T::RS] = x;
   }
 };
 
@@ -219,6 +237,235 @@ struct ThreadMap {
 
 enum { kExt = 0, kLin = 1, kPad = 2 };  // where a pass reads from / writes to
 
+// One Stockham pass P of an L-point transform (plan REV) over V components per
+// thread.  The pieces (load / compute / store) are exposed so kernels can fuse
+// work between passes (K3: forward last pass -> k-space multiply -> inverse
+// first pass, all in registers).
+template <int L, int P, bool REV, int NCOL, int NT, bool COLMODE, int V>
+struct Pass {
+  using PL = Plan<L, REV>;
+  using TM = ThreadMap<L, NCOL, NT, COLMODE>;
+  using T = TileIdx<L, NCOL, COLMODE, PL::R(0)>;
+  static constexpr int R = PL::R(P);
+  static constexpr int NS = PL::NS(P);
+  static constexpr int JR = L / R;
+  static constexpr int TPC = NT / NCOL;
+  static_assert(JR % TPC == 0 || TPC % JR == 0, "pow2 mapping");
+  static constexpr int UPT = JR >= TPC ? JR / TPC : 1;
+  static constexpr bool SPLIT = ((UPT == 1) || (TPC % T::R0v == 0)) && (JR % T::R0v == 0);
+
+  float2 v[UPT][V][R];
+
+  __device__ __forceinline__ static bool active(const TM& tm) { return (JR >= TPC) || tm.jb < JR; }
+  // input element of unit (q, r): i = jb + q TPC + r JR
+  __device__ __forceinline__ static constexpr int Cin(int q, int r) { return q * TPC + r * JR; }
+  // j mod Ns of unit q
+  __device__ __forceinline__ static int jm(const TM& tm, int q) {
+    if constexpr (NS <= TPC) return tm.jb % NS;
+    else return tm.jb + TPC * (q % (NS / TPC));
+  }
+  // output element of unit (q, r): d = sb + C2
+  __device__ __forceinline__ static int sb(const TM& tm) {
+    if constexpr (NS <= TPC) return (tm.jb / NS) * NS * R + tm.jb % NS;
+    else return tm.jb;
+  }
+  __device__ __forceinline__ static constexpr int C2(int q, int r) {
+    if constexpr (NS <= TPC) return q * TPC * R + r * NS;
+    else return TPC * (q % (NS / TPC)) + (q / (NS / TPC)) * NS * R + r * NS;
+  }
+
+  template <int RIN, class LD>
+  __device__ __forceinline__ void load_ext(const TM& tm, const LD& ld) {
+#pragma unroll
+    for (int q = 0; q < UPT; ++q)
+#pragma unroll
+      for (int w = 0; w < V; ++w)
+#pragma unroll
+        for (int r = 0; r < RIN; ++r) v[q][w][r] = ld(tm.b, w, tm.jb, Cin(q, r));
+  }
+  template <int RIN, bool PADDED>
+  __device__ __forceinline__ void load_smem(const TM& tm, const float2* s) {
+    const int lin0 = T::at(tm.b, tm.jb);
+    const int pad0 = T::at(tm.b, T::padrow(tm.jb));
+#pragma unroll
+    for (int q = 0; q < UPT; ++q)
+#pragma unroll
+      for (int w = 0; w < V; ++w)
+#pragma unroll
+        for (int r = 0; r < RIN; ++r) {
+          const int C = Cin(q, r);
+          if constexpr (!PADDED || !T::PAD) v[q][w][r] = s[w * T::ELEMS + lin0 + C * T::RS];
+          else if constexpr (SPLIT) v[q][w][r] = s[w * T::ELEMS + pad0 + (C + (C >> T::SH)) * T::RS];
+          else v[q][w][r] = s[w * T::ELEMS + T::at(tm.b, T::padrow(tm.jb + C))];
+        }
+  }
+  template <bool INV, bool HIN, bool HOUT>
+  __device__ __forceinline__ void compute(const TM& tm, const float2* __restrict__ tw, int twstride) {
+    constexpr int RIN = HIN ? R / 2 : R;
+#pragma unroll
+    for (int q = 0; q < UPT; ++q) {
+      if constexpr (NS > 1) {
+        const int k1 = jm(tm, q) * ((L / (NS * R)) * twstride);
+#pragma unroll
+        for (int r = 1; r < RIN; ++r) {
+          const float2 t = __ldg(tw + k1 * r);
+#pragma unroll
+          for (int w = 0; w < V; ++w) v[q][w][r] = INV ? cmulc(v[q][w][r], t) : cmul(v[q][w][r], t);
+        }
+      }
+#pragma unroll
+      for (int w = 0; w < V; ++w) {
+        if constexpr (HIN) dft_halfzero<R, INV>(v[q][w]);
+        else if constexpr (HOUT) dft_halfout<R, INV>(v[q][w]);
+        else dft_inplace<R, INV>(v[q][w]);
+      }
+    }
+  }
+  template <int ROUT, class ST>
+  __device__ __forceinline__ void store_ext(const TM& tm, const ST& st) {
+    const int b0 = sb(tm);
+#pragma unroll
+    for (int q = 0; q < UPT; ++q)
+#pragma unroll
+      for (int w = 0; w < V; ++w)
+#pragma unroll
+        for (int r = 0; r < ROUT; ++r) st(tm.b, w, b0, C2(q, r), v[q][w][r]);
+  }
+  template <int ROUT, bool PADDED>
+  __device__ __forceinline__ void store_smem(const TM& tm, float2* s) {
+    static_assert(!PADDED || NS == 1, "only pass 0 writes the padded interface");
+    const int lin1 = T::at(tm.b, sb(tm));
+    const int pad1 = T::at(tm.b, tm.jb * (R + 1));
+#pragma unroll
+    for (int q = 0; q < UPT; ++q)
+#pragma unroll
+      for (int w = 0; w < V; ++w)
+#pragma unroll
+        for (int r = 0; r < ROUT; ++r) {
+          if constexpr (!PADDED || !T::PAD) s[w * T::ELEMS + lin1 + C2(q, r) * T::RS] = v[q][w][r];
+          else s[w * T::ELEMS + pad1 + ((q * TPC) * (R + 1) + r) * T::RS] = v[q][w][r];  // d = (jb+qTPC)R + r
+        }
+  }
+};
+
+// Run pass P with sources/destinations SRC/DST (kExt functor, kLin / kPad smem).
+template <int L, int P, bool REV, int NCOL, int NT, bool COLMODE, int V, bool INV, bool HIN, bool HOUT, int SRC,
+          int DST, class LD, class ST>
+__device__ __forceinline__ void fft_pass(const ThreadMap<L, NCOL, NT, COLMODE>& tm, const LD& ld, const ST& st,
+                                         float2* s, const float2* __restrict__ tw, int twstride) {
+  using PS = Pass<L, P, REV, NCOL, NT, COLMODE, V>;
+  constexpr int RIN = HIN ? PS::R / 2 : PS::R;
+  constexpr int ROUT = HOUT ? PS::R / 2 : PS::R;
+  PS ps;
+  const bool act = PS::active(tm);
+  if (act) {
+    if constexpr (SRC == kExt) ps.template load_ext<RIN>(tm, ld);
+    else ps.template load_smem<RIN, SRC == kPad>(tm, s);
+  }
+  constexpr bool SRC_SMEM = (SRC != kExt) || LD::kSmem();
+  constexpr bool DST_SMEM = (DST != kExt) || ST::kSmem();
+  if constexpr (SRC_SMEM && DST_SMEM) __syncthreads();  // in-place hazard
+  if (act) {
+    ps.template compute<INV, HIN, HOUT>(tm, tw, twstride);
+    if constexpr (DST == kExt) ps.template store_ext<ROUT>(tm, st);
+    else ps.template store_smem<ROUT, DST == kPad>(tm, s);
+  }
+}
+
+template <int L, int P, bool REV, int NCOL, int NT, bool COLMODE, int V, bool INV, bool HIN, bool HOUT, int SRC0,
+          int DSTN, class LD, class ST>
+__device__ __forceinline__ void fft_passes(const ThreadMap<L, NCOL, NT, COLMODE>& tm, float2* s, const LD& ld,
+                                           const ST& st, const float2* __restrict__ tw, int twstride) {
+  constexpr int NP = fft_npass(L);
+  constexpr bool first = (P == 0), last = (P == NP - 1);
+  constexpr int IFACE0 = TileIdx<L, NCOL, COLMODE, Plan<L, REV>::R(0)>::PAD ? kPad : kLin;
+  if constexpr (first && last) {
+    fft_pass<L, P, REV, NCOL, NT, COLMODE, V, INV, HIN, HOUT, SRC0, DSTN>(tm, ld, st, s, tw, twstride);
+  } else if constexpr (first) {
+    fft_pass<L, P, REV, NCOL, NT, COLMODE, V, INV, HIN, false, SRC0, IFACE0>(tm, ld, st, s, tw, twstride);
+    __syncthreads();
+    fft_passes<L, P + 1, REV, NCOL, NT, COLMODE, V, INV, HIN, HOUT, SRC0, DSTN>(tm, s, ld, st, tw, twstride);
+  } else {
+    constexpr int SRCP = (P == 1) ? IFACE0 : kLin;
+    if constexpr (last) {
+      fft_pass<L, P, REV, NCOL, NT, COLMODE, V, INV, false, HOUT, SRCP, DSTN>(tm, ld, st, s, tw, twstride);
+    } else {
+      fft_pass<L, P, REV, NCOL, NT, COLMODE, V, INV, false, false, SRCP, kLin>(tm, ld, st, s, tw, twstride);
+      __syncthreads();
+      fft_passes<L, P + 1, REV, NCOL, NT, COLMODE, V, INV, HIN, HOUT, SRC0, DSTN>(tm, s, ld, st, tw, twstride);
+    }
+  }
+}
+
+// Passes 0 .. NP-2 of a transform (the first from `ld`, writing the smem tile),
+// then the last pass is loaded and computed into `ps` and left in registers:
+// output element i = PS::sb(tm) + PS::C2(q, r) of component w is ps.v[q][w][r].
+template <int L, int NCOL, int NT, bool COLMODE, int V, bool INV, bool HIN, bool HOUT, bool REV, class LD,
+          class PS>
+__device__ __forceinline__ void fft_to_regs(const ThreadMap<L, NCOL, NT, COLMODE>& tm, float2* s, const LD& ld,
+                                            const float2* __restrict__ tw, int twstride, PS& ps) {
+  constexpr int NP = fft_npass(L);
+  constexpr int IFACE0 = TileIdx<L, NCOL, COLMODE, Plan<L, REV>::R(0)>::PAD ? kPad : kLin;
+  if constexpr (NP == 1) {
+    if (PS::active(tm)) {
+      ps.template load_ext<HIN ? PS::R / 2 : PS::R>(tm, ld);
+      ps.template compute<INV, HIN, HOUT>(tm, tw, twstride);
+    }
+  } else {
+    struct None {
+      __device__ static constexpr bool kSmem() { return true; }
+      __device__ void operator()(int, int, int, int, float2) const {}
+    } none;
+    if constexpr (NP == 2) {
+      fft_pass<L, 0, REV, NCOL, NT, COLMODE, V, INV, HIN, false, kExt, IFACE0>(tm, ld, none, s, tw, twstride);
+    } else {
+      fft_pass<L, 0, REV, NCOL, NT, COLMODE, V, INV, HIN, false, kExt, IFACE0>(tm, ld, none, s, tw, twstride);
+      __syncthreads();
+      fft_pass<L, 1, REV, NCOL, NT, COLMODE, V, INV, false, false, IFACE0, kLin>(tm, ld, none, s, tw, twstride);
+      static_assert(NP <= 3, "plans have at most 3 passes (L <= 4096)");
+    }
+    __syncthreads();
+    if (PS::active(tm)) {
+      ps.template load_smem<PS::R, NP == 2 && IFACE0 == kPad>(tm, s);
+      ps.template compute<INV, false, HOUT>(tm, tw, twstride);
+    }
+  }
+}
+
+// The counterpart: `ps` holds pass 0's inputs in registers (element
+// i = jb + PS::Cin(q, r)); compute it, then the remaining passes, the last one
+// writing through `st`.  The caller must __syncthreads() before if the smem
+// tile is still being read.
+template <int L, int NCOL, int NT, bool COLMODE, int V, bool INV, bool HOUT, bool REV, class ST, class PS>
+__device__ __forceinline__ void fft_from_regs(const ThreadMap<L, NCOL, NT, COLMODE>& tm, float2* s, const ST& st,
+                                              const float2* __restrict__ tw, int twstride, PS& ps) {
+  constexpr int NP = fft_npass(L);
+  constexpr int IFACE0 = TileIdx<L, NCOL, COLMODE, Plan<L, REV>::R(0)>::PAD ? kPad : kLin;
+  struct None {
+    __device__ static constexpr bool kSmem() { return true; }
+    __device__ float2 operator()(int, int, int, int) const { return make_float2(0.f, 0.f); }
+  } none;
+  if constexpr (NP == 1) {
+    if (PS::active(tm)) {
+      ps.template compute<INV, false, HOUT>(tm, tw, twstride);
+      ps.template store_ext<HOUT ? PS::R / 2 : PS::R>(tm, st);
+    }
+  } else {
+    if (PS::active(tm)) {
+      ps.template compute<INV, false, false>(tm, tw, twstride);
+      ps.template store_smem<PS::R, IFACE0 == kPad>(tm, s);
+    }
+    __syncthreads();
+    if constexpr (NP == 2) {
+      fft_pass<L, 1, REV, NCOL, NT, COLMODE, V, INV, false, HOUT, IFACE0, kExt>(tm, none, st, s, tw, twstride);
+    } else {
+      fft_pass<L, 1, REV, NCOL, NT, COLMODE, V, INV, false, false, IFACE0, kLin>(tm, none, st, s, tw, twstride);
+      __syncthreads();
+      fft_pass<L, 2, REV, NCOL, NT, COLMODE, V, INV, false, HOUT, kLin, kExt>(tm, none, st, s, tw, twstride);
+    }
+  }
+}
+
 template <class T>
 struct IsTileLd : std::false_type {};
 template <int L, int N, bool C>
@@ -228,130 +475,25 @@ struct IsTileSt : std::false_type {};
 template <int L, int N, bool C>
 struct IsTileSt<SmemSt<L, N, C>> : std::true_type {};
 
-// One Stockham pass P of an L-point transform.  SRC/DST: kExt = caller functor,
-// kLin = linear smem tile, kPad = padded smem tile (the pass 0 -> 1 interface).
-template <int L, int P, int NCOL, int NT, bool COLMODE, bool INV, bool HIN, bool HOUT, int SRC, int DST, class LD,
-          class ST>
-__device__ __forceinline__ void fft_pass(const ThreadMap<L, NCOL, NT, COLMODE>& tm, const LD& ld, const ST& st,
-                                         float2* s, const float2* __restrict__ tw, int twstride) {
-  using T = TileIdx<L, NCOL, COLMODE>;
-  constexpr int R = 1 << fft_pass_bits(L, P);
-  constexpr int NS = fft_ns(L, P);
-  constexpr int JR = L / R;
-  constexpr int TPC = NT / NCOL;
-  static_assert(JR % TPC == 0 || TPC % JR == 0, "pow2 mapping");
-  constexpr int UPT = JR >= TPC ? JR / TPC : 1;
-  const bool active = (JR >= TPC) || tm.jb < JR;
-  constexpr int RIN = HIN ? R / 2 : R;    // inputs loaded
-  constexpr int ROUT = HOUT ? R / 2 : R;  // outputs stored
-  static_assert(DST != kPad || NS == 1, "only pass 0 writes the padded interface");
-  // loads: i = jb + C, C = q TPC + r JR
-  constexpr bool SPLIT = ((UPT == 1) || (TPC % T::R0 == 0)) && (JR % T::R0 == 0);
-  float2 v[UPT][R];
-  if (active) {
-    const int lin0 = T::at(tm.b, tm.jb);
-    const int pad0 = T::at(tm.b, T::padrow(tm.jb));
-#pragma unroll
-    for (int q = 0; q < UPT; ++q) {
-#pragma unroll
-      for (int r = 0; r < RIN; ++r) {
-        const int C = q * TPC + r * JR;
-        if constexpr (SRC == kExt) {
-          v[q][r] = ld(tm.b, tm.jb, C);
-        } else if constexpr (SRC == kLin) {
-          v[q][r] = s[lin0 + C * T::RS];
-        } else if constexpr (SPLIT) {
-          v[q][r] = s[pad0 + (C + (C >> T::SH)) * T::RS];
-        } else {
-          v[q][r] = s[T::at(tm.b, T::padrow(tm.jb + C))];
-        }
-      }
-    }
-  }
-  constexpr bool SRC_SMEM = (SRC != kExt) || LD::kSmem();
-  constexpr bool DST_SMEM = (DST != kExt) || ST::kSmem();
-  if constexpr (SRC_SMEM && DST_SMEM) __syncthreads();  // in-place hazard
-  if (active) {
-    int sb;  // per-thread part of the output row d = sb + C2
-    if constexpr (NS <= TPC) sb = (tm.jb / NS) * NS * R + tm.jb % NS;
-    else sb = tm.jb;
-    const int lin1 = T::at(tm.b, sb);
-    const int pad1 = T::at(tm.b, tm.jb * (R + 1));
-#pragma unroll
-    for (int q = 0; q < UPT; ++q) {
-      int jm;  // j mod Ns, j = jb + q TPC
-      if constexpr (NS <= TPC) jm = tm.jb % NS;
-      else jm = tm.jb + TPC * (q % (NS / TPC));
-      if constexpr (NS > 1) {
-        const int k1 = jm * ((L / (NS * R)) * twstride);
-#pragma unroll
-        for (int r = 1; r < RIN; ++r) {
-          const float2 w = __ldg(tw + k1 * r);
-          v[q][r] = INV ? cmulc(v[q][r], w) : cmul(v[q][r], w);
-        }
-      }
-      if constexpr (HIN) dft_halfzero<R, INV>(v[q]);
-      else if constexpr (HOUT) dft_halfout<R, INV>(v[q]);
-      else dft_inplace<R, INV>(v[q]);
-#pragma unroll
-      for (int r = 0; r < ROUT; ++r) {
-        int C2;
-        if constexpr (NS <= TPC) C2 = q * TPC * R + r * NS;
-        else C2 = TPC * (q % (NS / TPC)) + (q / (NS / TPC)) * NS * R + r * NS;
-        if constexpr (DST == kExt) {
-          st(tm.b, sb, C2, v[q][r]);
-        } else if constexpr (DST == kLin) {
-          s[lin1 + C2 * T::RS] = v[q][r];
-        } else {
-          // pass 0 (NS = 1): d = (jb + q TPC) R + r, padded row = (jb + q TPC)(R+1) + r
-          s[pad1 + ((q * TPC) * (R + 1) + r) * T::RS] = v[q][r];
-        }
-      }
-    }
-  }
-}
-
-template <int L, int P, int NCOL, int NT, bool COLMODE, bool INV, bool HIN, bool HOUT, int SRC0, int DSTN, class LD,
-          class ST>
-__device__ __forceinline__ void fft_passes(const ThreadMap<L, NCOL, NT, COLMODE>& tm, float2* s, const LD& ld,
-                                           const ST& st, const float2* __restrict__ tw, int twstride) {
-  constexpr int NP = fft_npass(L);
-  constexpr bool first = (P == 0), last = (P == NP - 1);
-  constexpr int IFACE0 = TileIdx<L, NCOL, COLMODE>::PAD ? kPad : kLin;
-  if constexpr (first && last) {
-    fft_pass<L, P, NCOL, NT, COLMODE, INV, HIN, HOUT, SRC0, DSTN>(tm, ld, st, s, tw, twstride);
-  } else if constexpr (first) {
-    fft_pass<L, P, NCOL, NT, COLMODE, INV, HIN, false, SRC0, IFACE0>(tm, ld, st, s, tw, twstride);
-    __syncthreads();
-    fft_passes<L, P + 1, NCOL, NT, COLMODE, INV, HIN, HOUT, SRC0, DSTN>(tm, s, ld, st, tw, twstride);
-  } else {
-    constexpr int SRCP = (P == 1) ? IFACE0 : kLin;
-    if constexpr (last) {
-      fft_pass<L, P, NCOL, NT, COLMODE, INV, false, HOUT, SRCP, DSTN>(tm, ld, st, s, tw, twstride);
-    } else {
-      fft_pass<L, P, NCOL, NT, COLMODE, INV, false, false, SRCP, kLin>(tm, ld, st, s, tw, twstride);
-      __syncthreads();
-      fft_passes<L, P + 1, NCOL, NT, COLMODE, INV, HIN, HOUT, SRC0, DSTN>(tm, s, ld, st, tw, twstride);
-    }
-  }
-}
-
-// Transform NCOL columns of length L.  ld(b, ib, C) supplies input element
-// i = ib + C of column b (HIN: only i < L/2 is requested, the rest is zero);
-// st(b, ib, C, v) receives output i = ib + C (HOUT: only i < L/2 is produced).
-// SmemLd/SmemSt as ld/st address the tile s itself (linear layout).  s holds
-// TileIdx::SMEM_ELEMS float2; the caller must __syncthreads() before reusing s.
-// twstride = Lmax / L.  L == 1 is the identity.
-template <int L, int NCOL, int NT, bool COLMODE, bool INV, bool HIN = false, bool HOUT = false, class LD, class ST>
+// Transform V components of NCOL columns of length L.  ld(b, v, ib, C) supplies
+// input element i = ib + C of component v of column b (HIN: only i < L/2 is
+// requested, the rest is zero); st(b, v, ib, C, x) receives output i = ib + C
+// (HOUT: only i < L/2 is produced).  SmemLd/SmemSt as ld/st address the tile s
+// itself (linear layout).  s holds V * TileIdx::ELEMS float2; the caller must
+// __syncthreads() before reusing s.  twstride = Lmax / L.  L == 1 is the identity.
+template <int L, int NCOL, int NT, bool COLMODE, bool INV, bool HIN = false, bool HOUT = false, int V = 1,
+          bool REV = false, class LD, class ST>
 __device__ __forceinline__ void fft_tile(float2* s, const LD& ld, const ST& st, const float2* __restrict__ tw,
                                          int twstride) {
   if constexpr (L == 1) {
-    for (int b = threadIdx.x; b < NCOL; b += NT) st(b, 0, 0, ld(b, 0, 0));
+    for (int b = threadIdx.x; b < NCOL; b += NT)
+#pragma unroll
+      for (int w = 0; w < V; ++w) st(b, w, 0, 0, ld(b, w, 0, 0));
   } else {
     const ThreadMap<L, NCOL, NT, COLMODE> tm;
     constexpr int SRC0 = IsTileLd<LD>::value ? kLin : kExt;
     constexpr int DSTN = IsTileSt<ST>::value ? kLin : kExt;
-    fft_passes<L, 0, NCOL, NT, COLMODE, INV, HIN, HOUT, SRC0, DSTN>(tm, s, ld, st, tw, twstride);
+    fft_passes<L, 0, REV, NCOL, NT, COLMODE, V, INV, HIN, HOUT, SRC0, DSTN>(tm, s, ld, st, tw, twstride);
   }
 }
 

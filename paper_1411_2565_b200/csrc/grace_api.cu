@@ -130,6 +130,8 @@ struct Rank {
   unsigned long long* flag = nullptr;  // [0] step non-finite, [1] set_m zero cell
   double* red = nullptr;               // mavg partials + 3 outputs
   float* Hbuf = nullptr;
+  bool tma = false;                    // TMA descriptors of the K2 / K4 inputs built
+  TmapBlob k2map{}, k4map{};
 };
 
 struct grace_ctx {
@@ -248,13 +250,13 @@ struct grace_ctx {
         rec(3);
       } else {
         rec(2);
-        CE(launch_k2(rk.g, rk.A, rk.X2, tw, s));
+        CE(launch_k2(rk.g, rk.A, rk.X2, tw, s, rk.tma ? &rk.k2map : nullptr));
         rec(3);
         rec(4);
         CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s));
         rec(5);
         rec(6);
-        CE(launch_k4(rk.g, rk.X2, rk.A, tw, s));
+        CE(launch_k4(rk.g, rk.X2, rk.A, tw, s, rk.tma ? &rk.k4map : nullptr));
         rec(7);
       }
       return cudaSuccess;
@@ -263,9 +265,9 @@ struct grace_ctx {
     CE(alltoall(&Rank::A, &Rank::B, s));  // C1: z slabs -> kx blocks
     for (auto& rk : ranks) {
       if (rk.g.Kc > 0) {
-        CE(launch_k2(rk.g, rk.B, rk.X2, tw, s));
+        CE(launch_k2(rk.g, rk.B, rk.X2, tw, s, rk.tma ? &rk.k2map : nullptr));
         CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s));
-        CE(launch_k4(rk.g, rk.X2, rk.B, tw, s));
+        CE(launch_k4(rk.g, rk.X2, rk.B, tw, s, rk.tma ? &rk.k4map : nullptr));
       }
     }
     CE(alltoall(&Rank::B, &Rank::A, s));  // C2: kx blocks -> z slabs
@@ -351,6 +353,10 @@ int make_geom(int nx, int ny, int nz, double dx, double dy, double dz, double Ms
   g.Kc = g.Kx;
   g.pitch2 = g.Kxp;
   g.has_lo = g.has_hi = 0;
+  int dev = 0, nsm = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaGetLastError();
+  g.nsm = nsm > 0 ? nsm : 148;
   *out = g;
   return GRACE_OK;
 }
@@ -359,7 +365,7 @@ int make_geom(int nx, int ny, int nz, double dx, double dy, double dz, double Ms
 Geom rank_geom(const Geom& g0, int r, int P) {
   Geom g = g0;
   if (P == 1) return g;
-  const int Kb = (g0.Kx + P - 1) / P;
+  const int Kb = (int)round_up((g0.Kx + P - 1) / P, 2);  // even: 16-byte TMA row strides
   g.nzl = g0.nz / P;
   g.kb = Kb;
   g.pitch1 = Kb;
@@ -455,6 +461,11 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
       return bail(rc);
   }
   if ((rc = h->alloc((void**)&h->tw, sizeof(float2) * g0.Lmax))) return bail(rc);
+  // TMA descriptors for the y-pencil kernels (K2 reads the x-row layout, K4 reads X2)
+  if (!h->fused && !getenv("GRACE_NO_TMA"))
+    for (auto& rk : h->ranks)
+      rk.tma = make_ky_tmaps(rk.g, P == 1 ? rk.A : rk.B, rk.X2, &rk.k2map, &rk.k4map) == cudaSuccess;
+  cudaGetLastError();
   h->N = (mode == grace_ctx::kNccl) ? h->ranks[0].Nl : (long long)nx * ny * nz;
 
   // setup: fp64 octant -> fp64 padded spectrum -> fp32 folded KS (S1..S5), once,

@@ -37,6 +37,7 @@ struct Geom {
   int Kc;           // kx columns handled by K2..K4 on this rank
   int pitch2;       // row pitch of X2
   int has_lo, has_hi;  // z-1 / z+1 halo planes present
+  int nsm;             // SMs of the device (persistent grids)
   float cx, cy, cz; // exchange 2A/(mu0 Ms^2 d^2) per axis (0 for a singleton axis)
   float ck;         // anisotropy 2Ku/(mu0 Ms^2)
   float Ms;
@@ -50,9 +51,17 @@ cudaError_t launch_k1(const Geom& g, const float* M, float2* X1, const float2* t
                       cudaStream_t st);
 // K2 in / K4 out use the x-row layout (pitch1, slabs of nzl planes per kx block);
 // X2 is [3][nz][Py][pitch2] over this rank's Kc columns.
-cudaError_t launch_k2(const Geom& g, const float2* X1, float2* X2, const float2* tw, cudaStream_t st);
+// 128-byte CUtensorMap storage (TMA descriptor built on the host, passed by value).
+struct alignas(64) TmapBlob {
+  unsigned char b[128];
+};
+// Tensor maps of the K2 input (x-row layout) and the K4 input (X2) for TMA loads.
+cudaError_t make_ky_tmaps(const Geom& g, const float2* k2_in, const float2* x2, TmapBlob* k2map, TmapBlob* k4map);
+cudaError_t launch_k2(const Geom& g, const float2* X1, float2* X2, const float2* tw, cudaStream_t st,
+                      const TmapBlob* tmap = nullptr);
 cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* tw, cudaStream_t st);
-cudaError_t launch_k4(const Geom& g, const float2* X2, float2* X1, const float2* tw, cudaStream_t st);
+cudaError_t launch_k4(const Geom& g, const float2* X2, float2* X1, const float2* tw, cudaStream_t st,
+                      const TmapBlob* tmap = nullptr);
 cudaError_t launch_k2f(const Geom& g, float2* X1, const float* KS, const float2* tw, cudaStream_t st);
 // mode 0: LLG Euler step M -> Mn; mode 1: store H_eff into Hout.
 // Hlo / Hhi: halo planes [3][ny][nx] of z-1 / z+1 (used when g.has_lo / g.has_hi).

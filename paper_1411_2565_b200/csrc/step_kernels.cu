@@ -10,9 +10,13 @@
 // nz == 1 (thin films, SP4): K2' fuses y-FFT, multiply and inverse y in one
 // CTA (the z axis is unpadded), so the step is K1, K2', K5.
 // The 1/(Px Py Pz) normalisation and the minus sign of H = -N*M live in KS.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cudaTypedefs.h>
+
 #include <cstdint>
+#include <cstring>
 
 #include "fft_engine.cuh"
 #include "internal.h"
@@ -21,51 +25,6 @@ namespace grace {
 
 // Occupancy target per block size: at most ~64 registers per thread.
 #define GRACE_MINB(NT) ((NT) <= 256 ? 4 : ((NT) <= 512 ? 2 : 1))
-
-// ---------------------------------------------------------------------------
-// k-space tensor-vector multiply at (kz, ky, kx) from the folded real table.
-// KS[c][kz'][ky'][kx], kz' = min(kz, Pz-kz), ky' = min(ky, Py-ky); a folded
-// axis flips the sign of the components odd in it (xy, yz odd in y; xz, yz in z).
-__device__ __forceinline__ void kmul3(float2& a, float2& b, float2& c, const float* __restrict__ KS, const Geom& g,
-                                      int kz, int ky, int kx) {
-  const bool fy = ky > (g.Py >> 1), fz = kz > (g.Pz >> 1);
-  const int kyf = fy ? g.Py - ky : ky;
-  const int kzf = fz ? g.Pz - kz : kz;
-  const size_t cs = (size_t)g.Kzh * g.Kyh * g.KSp;
-  const float* p = KS + ((size_t)kzf * g.Kyh + kyf) * g.KSp + kx;
-  const float nxx = __ldg(p), nyy = __ldg(p + 3 * cs), nzz = __ldg(p + 5 * cs);
-  float nxy = __ldg(p + cs);
-  if (fy) nxy = -nxy;
-  float nxz = 0.f, nyz = 0.f;
-  if (g.Pz > 1) {
-    nxz = __ldg(p + 2 * cs);
-    nyz = __ldg(p + 4 * cs);
-    if (fz) nxz = -nxz;
-    if (fy != fz) nyz = -nyz;
-  }
-  const float2 mx = a, my = b, mz = c;
-  a = make_float2(nxx * mx.x + nxy * my.x + nxz * mz.x, nxx * mx.y + nxy * my.y + nxz * mz.y);
-  b = make_float2(nxy * mx.x + nyy * my.x + nyz * mz.x, nxy * mx.y + nyy * my.y + nyz * mz.y);
-  c = make_float2(nxz * mx.x + nyz * my.x + nzz * mz.x, nxz * mx.y + nyz * my.y + nzz * mz.y);
-}
-
-// The same multiply with this CTA's KS slice staged in shared memory:
-// kss[c][kz'][b] for the CTA's ky' and kx tile (c = 0..5).
-__device__ __forceinline__ void kmul3_s(float2& a, float2& b, float2& c, const float* kss, int Kzh, int B,
-                                        const Geom& g, int kz, int ky, int bcol) {
-  const bool fy = ky > (g.Py >> 1), fz = kz > (g.Pz >> 1);
-  const int kzf = fz ? g.Pz - kz : kz;
-  const int cs = Kzh * B;
-  const float* p = kss + kzf * B + bcol;
-  const float nxx = p[0], nyy = p[3 * cs], nzz = p[5 * cs];
-  const float nxy = fy ? -p[cs] : p[cs];
-  const float nxz = fz ? -p[2 * cs] : p[2 * cs];
-  const float nyz = (fy != fz) ? -p[4 * cs] : p[4 * cs];
-  const float2 mx = a, my = b, mz = c;
-  a = make_float2(nxx * mx.x + nxy * my.x + nxz * mz.x, nxx * mx.y + nxy * my.y + nxz * mz.y);
-  b = make_float2(nxy * mx.x + nyy * my.x + nyz * mz.x, nxy * mx.y + nyy * my.y + nyz * mz.y);
-  c = make_float2(nxz * mx.x + nyz * my.x + nzz * mz.x, nxz * mx.y + nyz * my.y + nzz * mz.y);
-}
 
 __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -79,61 +38,105 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+// ---- TMA + mbarrier (sm_90+ async proxy) ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], "
+      "[%2];\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // K1: x R2C.  A real row of Px (nx nonzero) is packed as z[n] = x[2n] + i x[2n+1],
 // a length-L = Px/2 complex FFT gives Z, and
 //   X[k] = (Z[k] + conj Z[L-k])/2 - (i/2) w^k (Z[k] - conj Z[L-k]),  w = exp(-2 pi i/Px), k = 0..L.
-template <int L, int B, int NT, bool DIST>
-__global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k1_fwd_x(const float* __restrict__ M, float2* __restrict__ X1,
-                                               const float2* __restrict__ tw, Geom g, StepParams* bump) {
+// The three components of a spatial row are transformed by the same thread
+// (V = 3: shared twiddles and indexing).
+template <int L, int B, int NT, int MINB, bool DIST>
+__global__ void __launch_bounds__(NT, MINB) k1_fwd_x(const float* __restrict__ M, float2* __restrict__ X1,
+                                                     const float2* __restrict__ tw, Geom g, StepParams* bump) {
   extern __shared__ float2 smem[];
   // The step index lives on the device so captured graphs stay valid: K1 of each
   // step advances it, K5 of the same step reads step - 1.
   if (bump != nullptr && blockIdx.x == 0 && threadIdx.x == 0) bump->step += 1;
-  const int nrows = 3 * g.nzl * g.ny;
+  const int nrows = g.nzl * g.ny;  // spatial rows of this slab
   const int row0 = blockIdx.x * B;
+  const size_t N = (size_t)nrows * g.nx;
+  auto out = [&](int c, int row, int k) -> size_t {
+    if constexpr (DIST) {  // destination-blocked for the all-to-all: block k / kb
+      const int q = k / g.kb;
+      return q * g.blk1 + ((size_t)c * nrows + row) * g.pitch1 + (k - q * g.kb);
+    } else {
+      return ((size_t)c * nrows + row) * g.pitch1 + k;
+    }
+  };
   if constexpr (L == 0) {  // Px == 1: X[0] = x[0]
-    for (int b = threadIdx.x; b < B; b += NT) {
-      const int row = row0 + b;
-      if (row < nrows) X1[(size_t)row * g.pitch1] = make_float2(__ldg(M + row), 0.f);
+    for (int t = threadIdx.x; t < 3 * B; t += NT) {
+      const int c = t / B, row = row0 + (t - c * B);
+      if (row < nrows) X1[out(c, row, 0)] = make_float2(__ldg(M + c * N + row), 0.f);
     }
   } else {
     struct Ld {
       __device__ static constexpr bool kSmem() { return false; }
       const float* M;
+      size_t N;
       int row0, nrows, nx;
-      __device__ float2 operator()(int b, int ib, int C) const {
+      __device__ float2 operator()(int b, int c, int ib, int C) const {
         const int i = ib + C;
         float2 v = make_float2(0.f, 0.f);
         const int row = row0 + b;
         if (row < nrows) {
-          const float* p = M + (size_t)row * nx;
+          const float* p = M + c * N + (size_t)row * nx;
           const int x0 = 2 * i;
-          if (x0 < nx) v.x = __ldg(p + x0);
-          if (x0 + 1 < nx) v.y = __ldg(p + x0 + 1);
+          if ((nx & 1) == 0) {
+            if (x0 < nx) v = __ldg(reinterpret_cast<const float2*>(p + x0));
+          } else {
+            if (x0 < nx) v.x = __ldg(p + x0);
+            if (x0 + 1 < nx) v.y = __ldg(p + x0 + 1);
+          }
         }
         return v;
       }
-    } ld{M, row0, nrows, g.nx};
-    const int twstride = g.Lmax / L;
-    fft_tile<L, B, NT, false, false, true>(smem, ld, SmemSt<L, B, false>{smem}, tw, twstride);
+    } ld{M, N, row0, nrows, g.nx};
+    fft_tile<L, B, NT, false, false, true, false, 3>(smem, ld, SmemSt<L, B, false>{smem}, tw, g.Lmax / L);
     __syncthreads();
+    using T = TileIdx<L, B, false>;
     const int twpx = g.Lmax / (2 * L);
     for (int u = threadIdx.x; u < B * (L + 1); u += NT) {
       const int b = u / (L + 1), k = u - b * (L + 1);
       const int row = row0 + b;
       if (row >= nrows) continue;
-      const float2 Zk = smem[TileIdx<L, B, false>::at(b, k & (L - 1))];
-      const float2 Zn = smem[TileIdx<L, B, false>::at(b, (L - k) & (L - 1))];
-      const float2 E = make_float2(0.5f * (Zk.x + Zn.x), 0.5f * (Zk.y - Zn.y));
-      const float2 D = make_float2(0.5f * (Zk.x - Zn.x), 0.5f * (Zk.y + Zn.y));
-      const float2 wD = cmul(__ldg(tw + k * twpx), D);
-      const float2 Xk = make_float2(E.x + wD.y, E.y - wD.x);
-      if constexpr (DIST) {  // destination-blocked for the all-to-all: block k / kb
-        const int q = k / g.kb;
-        X1[q * g.blk1 + (size_t)row * g.pitch1 + (k - q * g.kb)] = Xk;
-      } else {
-        X1[(size_t)row * g.pitch1 + k] = Xk;
+      const float2 w = __ldg(tw + k * twpx);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float2 Zk = smem[c * T::ELEMS + T::at(b, k & (L - 1))];
+        const float2 Zn = smem[c * T::ELEMS + T::at(b, (L - k) & (L - 1))];
+        const float2 E = make_float2(0.5f * (Zk.x + Zn.x), 0.5f * (Zk.y - Zn.y));
+        const float2 D = make_float2(0.5f * (Zk.x - Zn.x), 0.5f * (Zk.y + Zn.y));
+        const float2 wD = cmul(w, D);
+        X1[out(c, row, k)] = make_float2(E.x + wD.y, E.y - wD.x);
       }
     }
   }
@@ -150,10 +153,10 @@ __device__ __forceinline__ size_t xrow_slab(const Geom& g, int slab) {
 // ---------------------------------------------------------------------------
 // K2 / K4: y pencils.  Columns (kx) are contiguous; a CTA owns NCOL columns of one
 // (component, z) slab.  Forward: ny of L inputs nonzero.  Inverse: keep y < ny.
-template <int L, int NCOL, int NT, bool INV>
-__global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k_y(const float2* __restrict__ in, float2* __restrict__ out,
-                                          const float2* __restrict__ tw, Geom g, int in_rows, int out_rows,
-                                          int n_in, int n_out) {
+template <int L, int NCOL, int NT, int MINB, bool INV>
+__global__ void __launch_bounds__(NT, MINB) k_y(const float2* __restrict__ in, float2* __restrict__ out,
+                                                const float2* __restrict__ tw, Geom g, int in_rows, int out_rows,
+                                                int n_in, int n_out) {
   extern __shared__ float2 smem[];
   const int kx0 = blockIdx.x * NCOL;
   const size_t slab = blockIdx.y;
@@ -161,7 +164,7 @@ __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k_y(const float2* __restri
     __device__ static constexpr bool kSmem() { return false; }
     const float2* p;
     int pitch, n_in, ncol_valid;
-    __device__ float2 operator()(int b, int ib, int C) const {
+    __device__ float2 operator()(int b, int, int ib, int C) const {
       const int i = ib + C;
       return (i < n_in && b < ncol_valid) ? __ldg(p + (b + i * pitch)) : make_float2(0.f, 0.f);
     }
@@ -171,7 +174,7 @@ __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k_y(const float2* __restri
     __device__ static constexpr bool kSmem() { return false; }
     float2* p;
     int pitch, n_out, ncol_valid;
-    __device__ void operator()(int b, int ib, int C, float2 v) const {
+    __device__ void operator()(int b, int, int ib, int C, float2 v) const {
       const int i = ib + C;
       if (i < n_out && b < ncol_valid) p[b + i * pitch] = v;
     }
@@ -180,41 +183,213 @@ __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k_y(const float2* __restri
   fft_tile<L, NCOL, NT, true, INV, !INV && (L > 1), INV && (L > 1)>(smem, ld, st, tw, g.Lmax / L);
 }
 
+// Persistent, TMA-fed variant of K2/K4 (L >= 64): each CTA loops over tiles;
+// while the FFT of tile t runs in place in one smem buffer, the tensor-map load
+// of the CTA's next tile lands in the other (mbarrier completion), so HBM reads
+// overlap the radix passes.  Box = {NCOL columns, <= 256 rows}; rows beyond ny
+// (forward) and columns beyond Kc are zero-filled by the TMA unit.
+template <int L, int NCOL>
+struct YTma {
+  using T = TileIdx<L, NCOL, true>;
+  static constexpr int TB = ((T::ELEMS * 8 + 1023) / 1024) * 1024;  // bytes per tile buffer
+  static constexpr size_t SMEM = 2 * (size_t)TB + 64;
+  static constexpr int NT = NCOL * (L / 16);
+  __host__ __device__ static constexpr int rows_in(bool inv) { return inv ? L : L / 2; }
+  __host__ __device__ static constexpr int br(bool inv) { return rows_in(inv) < 256 ? rows_in(inv) : 256; }
+};
+
+template <int L, int NCOL, bool INV>
+__global__ void __launch_bounds__(YTma<L, NCOL>::NT, 1)
+    k_y_tma(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, const float2* __restrict__ tw, Geom g,
+            int n_out) {
+  using Y = YTma<L, NCOL>;
+  constexpr int NT = Y::NT;
+  constexpr int ROWS = Y::rows_in(INV);
+  constexpr int BR = Y::br(INV);
+  constexpr int NBOX = ROWS / BR;
+  constexpr unsigned TX = NCOL * ROWS * 8;
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  float2* buf[2] = {reinterpret_cast<float2*>(smraw), reinterpret_cast<float2*>(smraw + Y::TB)};
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 2 * Y::TB);
+  const int ntx = (g.Kc + NCOL - 1) / NCOL;
+  const int ntiles = ntx * 3 * g.nz;
+  auto issue = [&](int t, float2* dst, uint64_t* b) {
+    const int slab = t / ntx, xt = t - slab * ntx;
+    const int c = slab / g.nz, z = slab - c * g.nz;
+    int c2 = z, c4 = 0;
+    if (!INV) {  // x-row layout [q][c][zl][y][kx]
+      c4 = z / g.nzl;
+      c2 = z - c4 * g.nzl;
+    }
+    mbar_expect_tx(b, TX);
+#pragma unroll
+    for (int nb = 0; nb < NBOX; ++nb) tma_load_5d(dst + nb * BR * NCOL, &tin, b, xt * NCOL, nb * BR, c2, c, c4);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  int t = blockIdx.x;
+  if (threadIdx.x == 0 && t < ntiles) issue(t, buf[0], bar);
+  struct St {
+    __device__ static constexpr bool kSmem() { return false; }
+    float2* p;
+    int pitch, n_out, ncol_valid;
+    __device__ void operator()(int b, int, int ib, int C, float2 v) const {
+      const int i = ib + C;
+      if (i < n_out && b < ncol_valid) p[b + i * pitch] = v;
+    }
+  };
+  for (int k = 0; t < ntiles; ++k, t += gridDim.x) {
+    float2* cur = buf[k & 1];
+    if (threadIdx.x == 0 && t + (int)gridDim.x < ntiles) {
+      fence_proxy_async();
+      issue(t + gridDim.x, buf[(k + 1) & 1], bar + ((k + 1) & 1));
+    }
+    mbar_wait(bar + (k & 1), (k >> 1) & 1);
+    const int slab = t / ntx, xt = t - slab * ntx;
+    const int kx0 = xt * NCOL;
+    const St st{out + (INV ? xrow_slab(g, slab) : (size_t)slab * g.Py * g.pitch2) + kx0, INV ? g.pitch1 : g.pitch2,
+                n_out, g.Kc - kx0};
+    fft_tile<L, NCOL, NT, true, INV, !INV, INV>(cur, SmemLd<L, NCOL, true>{cur}, st, tw, g.Lmax / L);
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------------------
-// K3: z pencils of the three components for one ky' (and its mirror Py - ky'):
-// forward z-FFT (nz of L nonzero), H~ = KS . M~, inverse z-FFT, keep z < nz.
-// Processing ky and Py-ky in one CTA reads each folded KS slice once.
-template <int L, int B, int NT>
-__global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k3_z(float2* __restrict__ X2, const float* __restrict__ KS,
-                                           const float2* __restrict__ tw, Geom g) {
-  extern __shared__ float2 smem[];
-  constexpr int NCOL = 3 * B;
-  const int kx0 = blockIdx.x * B;
-  const int kyf = blockIdx.y;
-  const int zstride = g.Py * g.pitch2;                // between z planes
-  const size_t cstride = (size_t)g.nz * zstride;      // between components
-  const int nvalid = g.Kc - kx0;
-  const int nky = (kyf == 0 || 2 * kyf == g.Py) ? 1 : 2;
-  // Stage this CTA's folded KS slice (6 comps x Kzh x B) in smem with cp.async;
-  // it lands while the first forward z-FFT runs and serves both ky and Py-ky.
-  constexpr int KZH = L / 2 + 1;
-  float* kss = reinterpret_cast<float*>(smem + TileIdx<L, NCOL, true>::SMEM_ELEMS);
-  {
-    const size_t csK = (size_t)g.Kzh * g.Kyh * g.KSp;
-    if constexpr (B % 4 == 0) {
-      for (int t = threadIdx.x; t < 6 * KZH * (B / 4); t += NT) {
-        const int ch = t % (B / 4), r = t / (B / 4);
-        const int comp = r / KZH, kz = r - comp * KZH;
-        cp_async16(kss + r * B + 4 * ch, KS + comp * csK + ((size_t)kz * g.Kyh + kyf) * g.KSp + kx0 + 4 * ch);
-      }
-    } else {
-      for (int t = threadIdx.x; t < 6 * KZH * B; t += NT) {
-        const int bb = t % B, r = t / B;
-        const int comp = r / KZH, kz = r - comp * KZH;
-        cp_async4(kss + r * B + bb, KS + comp * csK + ((size_t)kz * g.Kyh + kyf) * g.KSp + kx0 + bb);
-      }
+// k-space multiply with the CTA's folded KS slice staged in smem:
+// kss[c][kf][b], c = 0..5 (xx xy xz yy yz zz), kf the folded index of the
+// staged axis.  fy / fz: the k index was folded along y / z, which flips the
+// sign of the components odd in that axis (xy, yz odd in y; xz, yz odd in z).
+__device__ __forceinline__ void kmul_s(float2& a, float2& b, float2& c, const float* kss, int KH, int B, int kf,
+                                       int bcol, bool fy, bool fz) {
+  const int cs = KH * B;
+  const float* p = kss + kf * B + bcol;
+  const float nxx = p[0], nyy = p[3 * cs], nzz = p[5 * cs];
+  const float nxy = fy ? -p[cs] : p[cs];
+  const float nxz = fz ? -p[2 * cs] : p[2 * cs];
+  const float nyz = (fy != fz) ? -p[4 * cs] : p[4 * cs];
+  const float2 mx = a, my = b, mz = c;
+  a = make_float2(nxx * mx.x + nxy * my.x + nxz * mz.x, nxx * mx.y + nxy * my.y + nxz * mz.y);
+  b = make_float2(nxy * mx.x + nyy * my.x + nyz * mz.x, nxy * mx.y + nyy * my.y + nyz * mz.y);
+  c = make_float2(nxz * mx.x + nyz * my.x + nzz * mz.x, nxz * mx.y + nyz * my.y + nzz * mz.y);
+}
+
+// Stage KS[c][k1][k2][kx0 .. kx0+B) for c = 0..5 into kss[c][k][b] with cp.async,
+// where the staged axis k runs over KH entries at stride kstride (floats) from `base`.
+template <int B, int NT>
+__device__ __forceinline__ void stage_ks(float* kss, const float* __restrict__ base, size_t cstride, size_t kstride,
+                                         int KH) {
+  if constexpr (B % 4 == 0) {
+    for (int t = threadIdx.x; t < 6 * KH * (B / 4); t += NT) {
+      const int ch = t % (B / 4), r = t / (B / 4);
+      const int comp = r / KH, k = r - comp * KH;
+      cp_async16(kss + r * B + 4 * ch, base + comp * cstride + k * kstride + 4 * ch);
+    }
+  } else {
+    for (int t = threadIdx.x; t < 6 * KH * B; t += NT) {
+      const int bb = t % B, r = t / B;
+      const int comp = r / KH, k = r - comp * KH;
+      cp_async4(kss + r * B + bb, base + comp * cstride + k * kstride + bb);
     }
   }
+}
+
+// FFT along one pencil axis of the three components, H~ = KS . M~, inverse FFT.
+// The forward input has n nonzero of L (HIN), the inverse keeps n outputs (HOUT).
+// FUSE (L <= 64): the forward last pass, the multiply and the inverse first pass
+// (reversed radix plan) run in registers without a shared-memory round trip.
+template <int L>
+struct ZPlan {
+  static constexpr bool FUSE = L >= 2 && L <= 64;
+  static constexpr int RLAST = L <= 1 ? 1 : 1 << fft_pass_bits(L, fft_npass(L) - 1);
+  static constexpr int B = L <= 1 ? 32 : (2048 / L > 32 ? 32 : (2048 / L < 1 ? 1 : 2048 / L));
+  static constexpr int TPC = L <= 1 ? 1 : (FUSE ? L / RLAST : (L / 8 > 0 ? L / 8 : 1));
+  static constexpr int NT = B * TPC < 32 ? 32 : B * TPC;
+};
+
+template <int L, int B, int NT, class LD, class ST>
+__device__ __forceinline__ void pencil_conv(float2* smem, const LD& ld, const ST& st, const float* kss, int KH,
+                                            const float2* __restrict__ tw, int twstride, int P_other, int k_other,
+                                            bool fold_is_y, bool wait_ks) {
+  // k along the pencil axis (length L = P_axis); the other folded axis index is
+  // fixed for the CTA.  fold_is_y: the pencil axis is y (K2'), else z (K3).
+  auto flags = [&](int k, bool& fy, bool& fz, int& kf) {
+    const bool fa = k > (L >> 1);
+    kf = fa ? L - k : k;
+    const bool fo = k_other > (P_other >> 1);
+    if (fold_is_y) {
+      fy = fa;
+      fz = false;
+    } else {
+      fy = fo;
+      fz = fa;
+    }
+  };
+  const ThreadMap<L, B, NT, true> tm;
+  if constexpr (ZPlan<L>::FUSE) {
+    using PF = Pass<L, fft_npass(L) - 1, false, B, NT, true, 3>;
+    using PI = Pass<L, 0, true, B, NT, true, 3>;
+    static_assert(PF::R == PI::R && PF::UPT == 1 && PI::UPT == 1, "fused plan");
+    PF pf;
+    fft_to_regs<L, B, NT, true, 3, false, true, false, false>(tm, smem, ld, tw, twstride, pf);
+    if (wait_ks) cp_async_wait_all();
+    __syncthreads();
+    PI pi;
+#pragma unroll
+    for (int r = 0; r < PF::R; ++r) {
+      const int k = PF::sb(tm) + PF::C2(0, r);
+      bool fy, fz;
+      int kf;
+      flags(k, fy, fz, kf);
+      float2 a = pf.v[0][0][r], b = pf.v[0][1][r], c = pf.v[0][2][r];
+      kmul_s(a, b, c, kss, KH, B, kf, tm.b, fy, fz);
+      pi.v[0][0][r] = a;
+      pi.v[0][1][r] = b;
+      pi.v[0][2][r] = c;
+    }
+    fft_from_regs<L, B, NT, true, 3, true, true, true>(tm, smem, st, tw, twstride, pi);
+  } else {
+    using T = TileIdx<L, B, true>;
+    fft_tile<L, B, NT, true, false, (L > 1), false, 3>(smem, ld, SmemSt<L, B, true>{smem}, tw, twstride);
+    if (wait_ks) cp_async_wait_all();
+    __syncthreads();
+    for (int u = threadIdx.x; u < L * B; u += NT) {
+      const int k = u / B, b = u - k * B;
+      bool fy, fz;
+      int kf;
+      flags(k, fy, fz, kf);
+      float2* s0 = smem + T::at(b, k);
+      float2 a = s0[0], bb = s0[T::ELEMS], c = s0[2 * T::ELEMS];
+      kmul_s(a, bb, c, kss, KH, B, kf, b, fy, fz);
+      s0[0] = a;
+      s0[T::ELEMS] = bb;
+      s0[2 * T::ELEMS] = c;
+    }
+    __syncthreads();
+    fft_tile<L, B, NT, true, true, false, (L > 1), 3>(smem, SmemLd<L, B, true>{smem}, st, tw, twstride);
+  }
+}
+
+// K3: z pencils of the three components for one ky' (and its mirror Py - ky'):
+// forward z-FFT (nz of L nonzero), H~ = KS . M~, inverse z-FFT, keep z < nz.
+// Processing ky and Py-ky in one CTA reads each folded KS slice once; the slice
+// is staged by cp.async while the first forward FFT runs.
+template <int L, int B, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k3_z(float2* __restrict__ X2, const float* __restrict__ KS,
+                                                 const float2* __restrict__ tw, Geom g) {
+  extern __shared__ float2 smem[];
+  constexpr int KZH = L / 2 + 1;
+  const int kx0 = blockIdx.x * B;
+  const int kyf = blockIdx.y;
+  const int zstride = g.Py * g.pitch2;            // between z planes
+  const size_t cstride = (size_t)g.nz * zstride;  // between components
+  const int nvalid = g.Kc - kx0;
+  const int nky = (kyf == 0 || 2 * kyf == g.Py) ? 1 : 2;
+  float* kss = reinterpret_cast<float*>(smem + 3 * TileIdx<L, B, true>::ELEMS);
+  stage_ks<B, NT>(kss, KS + (size_t)kyf * g.KSp + kx0, (size_t)g.Kzh * g.Kyh * g.KSp, (size_t)g.Kyh * g.KSp, KZH);
   for (int rep = 0; rep < nky; ++rep) {
     const int ky = rep == 0 ? kyf : g.Py - kyf;
     float2* base = X2 + (size_t)ky * g.pitch2 + kx0;
@@ -224,9 +399,8 @@ __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k3_z(float2* __restrict__ 
       int zs;
       size_t cs;
       int nz, nvalid;
-      __device__ float2 operator()(int col, int ib, int C) const {
+      __device__ float2 operator()(int b, int c, int ib, int C) const {
         const int i = ib + C;
-        const int c = col / B, b = col - c * B;
         return (i < nz && b < nvalid) ? __ldg(p + c * cs + (b + i * zs)) : make_float2(0.f, 0.f);
       }
     } ld{base, zstride, cstride, g.nz, nvalid};
@@ -236,31 +410,31 @@ __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k3_z(float2* __restrict__ 
       int zs;
       size_t cs;
       int nz, nvalid;
-      __device__ void operator()(int col, int ib, int C, float2 v) const {
+      __device__ void operator()(int b, int c, int ib, int C, float2 v) const {
         const int i = ib + C;
-        const int c = col / B, b = col - c * B;
         if (i < nz && b < nvalid) p[c * cs + (b + i * zs)] = v;
       }
     } st{base, zstride, cstride, g.nz, nvalid};
     if (rep) __syncthreads();
-    fft_tile<L, NCOL, NT, true, false, (L > 1)>(smem, ld, SmemSt<L, NCOL, true>{smem}, tw, g.Lmax / L);
-    if (rep == 0) cp_async_wait_all();
-    __syncthreads();
-    for (int u = threadIdx.x; u < L * B; u += NT) {
-      const int kz = u / B, b = u - kz * B;
-      float2* s = smem + TileIdx<L, NCOL, true>::at(b, kz);
-      float2 a = s[0], bb = s[B], c = s[2 * B];
-      kmul3_s(a, bb, c, kss, KZH, B, g, kz, ky, b);
-      s[0] = a;
-      s[B] = bb;
-      s[2 * B] = c;
-    }
-    __syncthreads();
-    fft_tile<L, NCOL, NT, true, true, false, (L > 1)>(smem, SmemLd<L, NCOL, true>{smem}, st, tw, g.Lmax / L);
+    pencil_conv<L, B, NT>(smem, ld, st, kss, KZH, tw, g.Lmax / L, g.Py, ky, false, rep == 0);
   }
 }
 
-// Pz == 1 without the fused y path: H~ = KS . M~ on X2 [3][1][Py][Kxp].
+// Pz == 1 without the fused y path: H~ = KS . M~ on X2 [3][1][Py][pitch2].
+__device__ __forceinline__ void kmul3(float2& a, float2& b, float2& c, const float* __restrict__ KS, const Geom& g,
+                                      int ky, int kx) {
+  const bool fy = ky > (g.Py >> 1);
+  const int kyf = fy ? g.Py - ky : ky;
+  const size_t cs = (size_t)g.Kzh * g.Kyh * g.KSp;
+  const float* p = KS + (size_t)kyf * g.KSp + kx;
+  const float nxx = __ldg(p), nyy = __ldg(p + 3 * cs), nzz = __ldg(p + 5 * cs);
+  const float nxy = fy ? -__ldg(p + cs) : __ldg(p + cs);
+  const float2 mx = a, my = b, mz = c;
+  a = make_float2(nxx * mx.x + nxy * my.x, nxx * mx.y + nxy * my.y);
+  b = make_float2(nxy * mx.x + nyy * my.x, nxy * mx.y + nyy * my.y);
+  c = make_float2(nzz * mz.x, nzz * mz.y);
+}
+
 __global__ void k_mul_plane(float2* __restrict__ X2, const float* __restrict__ KS, Geom g) {
   const int kx = blockIdx.x * blockDim.x + threadIdx.x;
   const int ky = blockIdx.y;
@@ -268,7 +442,7 @@ __global__ void k_mul_plane(float2* __restrict__ X2, const float* __restrict__ K
   const size_t cs = (size_t)g.Py * g.pitch2;
   float2* p = X2 + (size_t)ky * g.pitch2 + kx;
   float2 a = p[0], b = p[cs], c = p[2 * cs];
-  kmul3(a, b, c, KS, g, 0, ky, kx);
+  kmul3(a, b, c, KS, g, ky, kx);
   p[0] = a;
   p[cs] = b;
   p[2 * cs] = c;
@@ -276,51 +450,38 @@ __global__ void k_mul_plane(float2* __restrict__ X2, const float* __restrict__ K
 
 // ---------------------------------------------------------------------------
 // K2': nz == 1.  y-FFT (ny of L nonzero), multiply, inverse y (keep y < ny), in place on X1.
-template <int L, int B, int NT>
-__global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k2f_y_fused(float2* __restrict__ X1, const float* __restrict__ KS,
-                                                  const float2* __restrict__ tw, Geom g) {
+template <int L, int B, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k2f_y_fused(float2* __restrict__ X1, const float* __restrict__ KS,
+                                                        const float2* __restrict__ tw, Geom g) {
   extern __shared__ float2 smem[];
-  constexpr int NCOL = 3 * B;
+  constexpr int KYH = L / 2 + 1;
   const int kx0 = blockIdx.x * B;
   const int nvalid = g.Kx - kx0;
-  const size_t cstride = (size_t)g.ny * g.Kxp;
+  const size_t cstride = (size_t)g.ny * g.pitch1;
   float2* base = X1 + kx0;
+  float* kss = reinterpret_cast<float*>(smem + 3 * TileIdx<L, B, true>::ELEMS);
+  stage_ks<B, NT>(kss, KS + kx0, (size_t)g.Kzh * g.Kyh * g.KSp, (size_t)g.KSp, KYH);
   struct Ld {
     __device__ static constexpr bool kSmem() { return false; }
     const float2* p;
     size_t cs;
     int pitch, ny, nvalid;
-    __device__ float2 operator()(int col, int ib, int C) const {
+    __device__ float2 operator()(int b, int c, int ib, int C) const {
       const int i = ib + C;
-      const int c = col / B, b = col - c * B;
       return (i < ny && b < nvalid) ? __ldg(p + c * cs + (b + i * pitch)) : make_float2(0.f, 0.f);
     }
-  } ld{base, cstride, g.Kxp, g.ny, nvalid};
+  } ld{base, cstride, g.pitch1, g.ny, nvalid};
   struct St {
     __device__ static constexpr bool kSmem() { return false; }
     float2* p;
     size_t cs;
     int pitch, ny, nvalid;
-    __device__ void operator()(int col, int ib, int C, float2 v) const {
+    __device__ void operator()(int b, int c, int ib, int C, float2 v) const {
       const int i = ib + C;
-      const int c = col / B, b = col - c * B;
       if (i < ny && b < nvalid) p[c * cs + (b + i * pitch)] = v;
     }
-  } st{base, cstride, g.Kxp, g.ny, nvalid};
-  fft_tile<L, NCOL, NT, true, false, (L > 1)>(smem, ld, SmemSt<L, NCOL, true>{smem}, tw, g.Lmax / L);
-  __syncthreads();
-  for (int u = threadIdx.x; u < L * B; u += NT) {
-    const int ky = u / B, b = u - ky * B;
-    if (b >= nvalid) continue;
-    float2* s = smem + TileIdx<L, NCOL, true>::at(b, ky);
-    float2 a = s[0], bb = s[B], c = s[2 * B];
-    kmul3(a, bb, c, KS, g, 0, ky, kx0 + b);
-    s[0] = a;
-    s[B] = bb;
-    s[2 * B] = c;
-  }
-  __syncthreads();
-  fft_tile<L, NCOL, NT, true, true, false, (L > 1)>(smem, SmemLd<L, NCOL, true>{smem}, st, tw, g.Lmax / L);
+  } st{base, cstride, g.pitch1, g.ny, nvalid};
+  pencil_conv<L, B, NT>(smem, ld, st, kss, KYH, tw, g.Lmax / L, 1, 0, true, true);
 }
 
 // ---------------------------------------------------------------------------
@@ -328,29 +489,133 @@ __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k2f_y_fused(float2* __rest
 // C2R of length Px = 2L from the half spectrum X[0..L]:
 //   Z[k] = (X[k] + conj X[L-k]) + i w^-k (X[k] - conj X[L-k]),  k < L,
 //   z = IFFT_L(Z) (unnormalised; 1/P is in KS),  x[2n] = Re z[n], x[2n+1] = Im z[n].
-__device__ __forceinline__ float3 ld3(const float* __restrict__ M, size_t N, size_t i) {
-  return make_float3(__ldg(M + i), __ldg(M + N + i), __ldg(M + 2 * N + i));
+// The last inverse pass leaves H_demag of cells x = 2n, 2n+1 (all three
+// components) in the registers of one thread, which applies Eq. (2), Eq. (3)
+// and the Euler update to that cell pair directly.
+struct CellCtx {
+  const float* M;
+  float* Mn;
+  float* Hout;
+  const float* Hlo;
+  const float* Hhi;
+  unsigned long long* flag;
+  size_t N, plane;
+  int mode;
+};
+
+__device__ __forceinline__ float2 ld2(const float* p, bool pair_ok) {
+  // (p[0], p[1]); p[1] only if pair_ok.  8-byte aligned when pair_ok and nx even.
+  return pair_ok ? make_float2(__ldg(p), __ldg(p + 1)) : make_float2(__ldg(p), 0.f);
 }
 
-template <int L, int B, int NT, bool DIST>
-__global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k5_inv_x_llg(const float2* __restrict__ X1, const float* __restrict__ M,
-                                                   float* __restrict__ Mn, float* __restrict__ Hout,
-                                                   const float2* __restrict__ tw, Geom g,
-                                                   const StepParams* __restrict__ prm,
-                                                   unsigned long long* __restrict__ flag, int mode,
-                                                   const float* __restrict__ Hlo, const float* __restrict__ Hhi) {
+// Update cells (x0, zl, y) and (x0+1, zl, y) (the second only if hasB) with
+// H_demag hA / hB.  Missing neighbours (Neumann) use the centre value.
+template <bool DIST>
+__device__ __forceinline__ void cell_pair(const CellCtx& cc, const Geom& g, const StepParams& p, int row, int x0,
+                                          bool hasB, const float hA[3], const float hB[3]) {
+  const int zl = row / g.ny, y = row - zl * g.ny;
+  const size_t i = (size_t)row * g.nx + x0;
+  const size_t iy0 = y > 0 ? i - g.nx : i, iy1 = y + 1 < g.ny ? i + g.nx : i;
+  const float* zlo;  // pointers to the z-1 / z+1 cell of x0 (component 0), and component strides
+  const float* zhi;
+  size_t czlo = cc.N, czhi = cc.N;
+  if (zl > 0) zlo = cc.M + (i - cc.plane);
+  else if (DIST && g.has_lo) { zlo = cc.Hlo + (size_t)y * g.nx + x0; czlo = cc.plane; }
+  else zlo = cc.M + i;
+  if (zl + 1 < g.nzl) zhi = cc.M + (i + cc.plane);
+  else if (DIST && g.has_hi) { zhi = cc.Hhi + (size_t)y * g.nx + x0; czhi = cc.plane; }
+  else zhi = cc.M + i;
+  const bool xm = x0 > 0, xp = x0 + 2 < g.nx;
+  float m[3][2], nx0[3], nx1[3], ny0[3][2], ny1[3][2], nz0[3][2], nz1[3][2];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const float* mc = cc.M + c * cc.N;
+    const float2 mm = ld2(mc + i, hasB);
+    m[c][0] = mm.x;
+    m[c][1] = mm.y;
+    nx0[c] = xm ? __ldg(mc + i - 1) : mm.x;
+    nx1[c] = xp ? __ldg(mc + i + 2) : (hasB ? mm.y : mm.x);
+    const float2 a = ld2(mc + iy0, hasB), b = ld2(mc + iy1, hasB);
+    const float2 d = ld2(zlo + c * czlo, hasB), e = ld2(zhi + c * czhi, hasB);
+    ny0[c][0] = a.x; ny0[c][1] = a.y;
+    ny1[c][0] = b.x; ny1[c][1] = b.y;
+    nz0[c][0] = d.x; nz0[c][1] = d.y;
+    nz1[c][0] = e.x; nz1[c][1] = e.y;
+  }
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    if (s == 1 && !hasB) break;
+    const float* hd = s ? hB : hA;
+    const float mx = m[0][s], my = m[1][s], mz = m[2][s];
+    // Eq. (2): H_eff = H_demag + H_exch + H_anis + H_ext
+    float hx = hd[0] + p.hext[0] + g.ck * mx;
+    float hy = hd[1] + p.hext[1];
+    float hz = hd[2] + p.hext[2];
+    // six-neighbour exchange (difference form: uniform M gives exactly 0; reading Q11)
+    float e3[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float mc = m[c][s];
+      const float xl = s ? m[c][0] : nx0[c];                 // x-1
+      const float xr = s ? nx1[c] : (hasB ? m[c][1] : nx1[c]);  // x+1
+      float e = 0.f;
+      e += g.cx * (xl - mc);
+      e += g.cx * (xr - mc);
+      e += g.cy * (ny0[c][s] - mc);
+      e += g.cy * (ny1[c][s] - mc);
+      e += g.cz * (nz0[c][s] - mc);
+      e += g.cz * (nz1[c][s] - mc);
+      e3[c] = e;
+    }
+    hx += e3[0];
+    hy += e3[1];
+    hz += e3[2];
+    const size_t ic = i + s;
+    if (cc.mode == 1) {
+      cc.Hout[ic] = hx;
+      cc.Hout[cc.N + ic] = hy;
+      cc.Hout[2 * cc.N + ic] = hz;
+      continue;
+    }
+    // Eq. (3): dM/dt = c_prec (M x H) + c_damp M x (M x H); Euler; renormalise (Q16)
+    const float ax = my * hz - mz * hy, ay = mz * hx - mx * hz, az = mx * hy - my * hx;
+    const float bx = my * az - mz * ay, by = mz * ax - mx * az, bz = mx * ay - my * ax;
+    const float sx = mx + p.dt * (p.c_prec * ax + p.c_damp * bx);
+    const float sy = my + p.dt * (p.c_prec * ay + p.c_damp * by);
+    const float sz = mz + p.dt * (p.c_prec * az + p.c_damp * bz);
+    const float sc = g.Ms / sqrtf(sx * sx + sy * sy + sz * sz);
+    const float ox = sx * sc, oy = sy * sc, oz = sz * sc;
+    cc.Mn[ic] = ox;
+    cc.Mn[cc.N + ic] = oy;
+    cc.Mn[2 * cc.N + ic] = oz;
+    if (!(isfinite(ox) && isfinite(oy) && isfinite(oz)))
+      atomicMin(cc.flag, ((unsigned long long)(p.step - 1) << 36) | (unsigned long long)ic);
+  }
+}
+
+template <int L, int B, int NT, int MINB, bool DIST>
+__global__ void __launch_bounds__(NT, MINB) k5_inv_x_llg(const float2* __restrict__ X1, const float* __restrict__ M,
+                                                         float* __restrict__ Mn, float* __restrict__ Hout,
+                                                         const float2* __restrict__ tw, Geom g,
+                                                         const StepParams* __restrict__ prm,
+                                                         unsigned long long* __restrict__ flag, int mode,
+                                                         const float* __restrict__ Hlo,
+                                                         const float* __restrict__ Hhi) {
   extern __shared__ float2 smem[];
-  constexpr int NCOL = 3 * B;
   const int nrows = g.nzl * g.ny;
   const int row0 = blockIdx.x * B;
   const size_t N = (size_t)nrows * g.nx;
   const size_t cstrideX = (size_t)nrows * g.pitch1;  // X1 component stride
-  float* hs = reinterpret_cast<float*>(smem);      // H_demag rows [3B][2L] (reals), aliasing the tile
-  if constexpr (L == 0) {
-    for (int col = threadIdx.x; col < NCOL; col += NT) {
-      const int c = col / B, b = col - c * B;
+  const StepParams p = *prm;
+  const CellCtx cc{M, Mn, Hout, Hlo, Hhi, flag, N, (size_t)g.nx * g.ny, mode};
+  if constexpr (L == 0) {  // nx == 1: H_demag = Re X[0]
+    for (int b = threadIdx.x; b < B; b += NT) {
       const int row = row0 + b;
-      hs[col] = row < nrows ? __ldg(X1 + c * cstrideX + (size_t)row * g.pitch1).x : 0.f;
+      if (row >= nrows) continue;
+      float h[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) h[c] = __ldg(X1 + c * cstrideX + (size_t)row * g.pitch1).x;
+      cell_pair<DIST>(cc, g, p, row, 0, false, h, h);
     }
   } else {
     const int twpx = g.Lmax / (2 * L);
@@ -361,140 +626,65 @@ __global__ void __launch_bounds__(NT, GRACE_MINB(NT)) k5_inv_x_llg(const float2*
       size_t cs;
       int row0, nrows, pitch, twpx, kb;
       long long blk1;
-      __device__ float2 operator()(int col, int ib, int C) const {
+      __device__ float2 operator()(int b, int c, int ib, int C) const {
         const int k = ib + C;
-        const int c = col / B, b = col - c * B;
         const int row = row0 + b;
         if (row >= nrows) return make_float2(0.f, 0.f);
-        const float2* p = X + c * cs + (size_t)row * pitch;
+        const float2* q = X + c * cs + (size_t)row * pitch;
         float2 a, m;
         if constexpr (DIST) {  // gather from the source kx blocks of the all-to-all
           const int qa = k / kb, qm = (L - k) / kb;
-          a = __ldg(p + qa * blk1 + (k - qa * kb));
-          m = __ldg(p + qm * blk1 + ((L - k) - qm * kb));
+          a = __ldg(q + qa * blk1 + (k - qa * kb));
+          m = __ldg(q + qm * blk1 + ((L - k) - qm * kb));
         } else {
-          a = __ldg(p + k);
-          m = __ldg(p + (L - k));
+          a = __ldg(q + k);
+          m = __ldg(q + (L - k));
         }
         const float2 S = make_float2(a.x + m.x, a.y - m.y);  // X[k] + conj X[L-k]
         const float2 D = make_float2(a.x - m.x, a.y + m.y);  // X[k] - conj X[L-k]
-        float2 w = __ldg(tw + k * twpx);                       // exp(-2 pi i k/Px)
-        w.y = -w.y;                                            // w^-k
-        const float2 wD = cmul(w, D);
-        return make_float2(S.x - wD.y, S.y + wD.x);            // S + i wD
+        const float2 w = __ldg(tw + k * twpx);                 // exp(-2 pi i k/Px)
+        const float2 wD = cmulc(D, w);                         // w^-k D
+        return make_float2(S.x - wD.y, S.y + wD.x);            // S + i w^-k D
       }
     } ld{X1, tw, cstrideX, row0, nrows, g.pitch1, twpx, g.kb, g.blk1};
-    struct St {
-      __device__ static constexpr bool kSmem() { return true; }
-      float* hs;
-      int nx;
-      __device__ void operator()(int col, int ib, int C, float2 v) const {
-        const int n = ib + C;
-        float* p = hs + col * (2 * L) + 2 * n;
-        if (2 * n + 1 < nx) *reinterpret_cast<float2*>(p) = v;
-        else if (2 * n < nx) p[0] = v.x;
-      }
-    } st{hs, g.nx};
-    fft_tile<L, NCOL, NT, false, true, false, true>(smem, ld, st, tw, g.Lmax / L);
-  }
-  __syncthreads();
-  constexpr int HP = (L == 0) ? 1 : 2 * L;  // row pitch of hs
-  const StepParams p = *prm;
-  const size_t plane = (size_t)g.nx * g.ny;
-  const int ncell = B * g.nx;
-  // Two cells per thread per iteration with all 42 stencil loads issued before
-  // any use.  A missing neighbour (Neumann) loads the centre cell instead, so its
-  // difference is exactly 0 (reading Q11).
-  constexpr int CPI = 2;
-  for (int u0 = threadIdx.x; u0 < ncell; u0 += CPI * NT) {
-    float3 m[CPI], q[CPI][6];
-    size_t ic[CPI];
-    int bc[CPI], xc[CPI];
-    bool ok[CPI];
+    using PS = Pass<L, fft_npass(L) - 1, false, B, NT, false, 3>;
+    const ThreadMap<L, B, NT, false> tm;
+    PS ps;
+    fft_to_regs<L, B, NT, false, 3, true, false, true, false>(tm, smem, ld, tw, g.Lmax / L, ps);
+    const int row = row0 + tm.b;
+    if (PS::active(tm) && row < nrows) {
 #pragma unroll
-    for (int c = 0; c < CPI; ++c) {
-      const int u = u0 + c * NT;
-      const int b = u / g.nx, x = u - b * g.nx;
-      const int row = row0 + b;
-      ok[c] = u < ncell && row < nrows;
-      const int rr = ok[c] ? row : 0;
-      const int xx = ok[c] ? x : 0;
-      const int z = rr / g.ny, y = rr - z * g.ny;
-      const size_t i = (size_t)rr * g.nx + xx;
-      ic[c] = i;
-      bc[c] = ok[c] ? b : 0;
-      xc[c] = xx;
-      m[c] = ld3(M, N, i);
-      q[c][0] = ld3(M, N, xx > 0 ? i - 1 : i);
-      q[c][1] = ld3(M, N, xx + 1 < g.nx ? i + 1 : i);
-      q[c][2] = ld3(M, N, y > 0 ? i - g.nx : i);
-      q[c][3] = ld3(M, N, y + 1 < g.ny ? i + g.nx : i);
-      if (DIST && z == 0 && g.has_lo) q[c][4] = ld3(Hlo, plane, (size_t)y * g.nx + xx);
-      else q[c][4] = ld3(M, N, z > 0 ? i - plane : i);
-      if (DIST && z + 1 == g.nzl && g.has_hi) q[c][5] = ld3(Hhi, plane, (size_t)y * g.nx + xx);
-      else q[c][5] = ld3(M, N, z + 1 < g.nzl ? i + plane : i);
-    }
+      for (int q = 0; q < PS::UPT; ++q)
 #pragma unroll
-    for (int c = 0; c < CPI; ++c) {
-      if (!ok[c]) continue;
-      const size_t i = ic[c];
-      const int b = bc[c], x = xc[c];
-      const float3 mm = m[c];
-      // Eq. (2): H_eff = H_demag + H_exch + H_anis + H_ext
-      float hx = hs[(0 * B + b) * HP + x] + p.hext[0] + g.ck * mm.x;
-      float hy = hs[(1 * B + b) * HP + x] + p.hext[1];
-      float hz = hs[(2 * B + b) * HP + x] + p.hext[2];
-      // six-neighbour exchange (difference form: uniform M gives exactly 0)
-      float ex = 0.f, ey = 0.f, ez = 0.f;
-#pragma unroll
-      for (int k = 0; k < 6; ++k) {
-        const float ck = k < 2 ? g.cx : (k < 4 ? g.cy : g.cz);
-        ex += ck * (q[c][k].x - mm.x);
-        ey += ck * (q[c][k].y - mm.y);
-        ez += ck * (q[c][k].z - mm.z);
-      }
-      hx += ex;
-      hy += ey;
-      hz += ez;
-      if (mode == 1) {
-        Hout[i] = hx;
-        Hout[N + i] = hy;
-        Hout[2 * N + i] = hz;
-        continue;
-      }
-      // Eq. (3): dM/dt = c_prec (M x H) + c_damp M x (M x H)
-      const float ax = mm.y * hz - mm.z * hy, ay = mm.z * hx - mm.x * hz, az = mm.x * hy - mm.y * hx;
-      const float bx = mm.y * az - mm.z * ay, by = mm.z * ax - mm.x * az, bz = mm.x * ay - mm.y * ax;
-      const float sx = mm.x + p.dt * (p.c_prec * ax + p.c_damp * bx);
-      const float sy = mm.y + p.dt * (p.c_prec * ay + p.c_damp * by);
-      const float sz = mm.z + p.dt * (p.c_prec * az + p.c_damp * bz);
-      const float sc = g.Ms / sqrtf(sx * sx + sy * sy + sz * sz);  // renormalise to Ms (reading Q16)
-      const float ox = sx * sc, oy = sy * sc, oz = sz * sc;
-      Mn[i] = ox;
-      Mn[N + i] = oy;
-      Mn[2 * N + i] = oz;
-      if (!(isfinite(ox) && isfinite(oy) && isfinite(oz)))
-        atomicMin(flag, ((unsigned long long)(p.step - 1) << 36) | (unsigned long long)i);
+        for (int r = 0; r < PS::R / 2; ++r) {
+          const int n = PS::sb(tm) + PS::C2(q, r);
+          const int x0 = 2 * n;
+          if (x0 >= g.nx) continue;
+          const float hA[3] = {ps.v[q][0][r].x, ps.v[q][1][r].x, ps.v[q][2][r].x};
+          const float hB[3] = {ps.v[q][0][r].y, ps.v[q][1][r].y, ps.v[q][2][r].y};
+          cell_pair<DIST>(cc, g, p, row, x0, x0 + 1 < g.nx, hA, hB);
+        }
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// Tile choices and dispatch.  Every engine instance uses TPC = L/16 threads per
-// column, i.e. 16 complex values per thread per pass.
-// Complex values per thread per Stockham pass (EPT) and tile sizes, per kernel,
-// from the sweep in profiles/ (DESIGN.md §6).  TPC = L/EPT threads per column.
-#ifndef GRACE_EPT_X1
-#define GRACE_EPT_X1 16
+// Tile choices and dispatch.  EPT = complex values per thread
+// per pass and component.
+#ifndef GRACE_EPT_X
+#define GRACE_EPT_X 8
 #endif
-#ifndef GRACE_EPT_X5
-#define GRACE_EPT_X5 32
+#ifndef GRACE_MINB_K1
+#define GRACE_MINB_K1 3  // CTAs/SM the register budget of K1 (256 threads) is sized for
+#endif
+#ifndef GRACE_MINB_K5
+#define GRACE_MINB_K5 2
+#endif
+#ifndef GRACE_MINB_Z
+#define GRACE_MINB_Z 3
 #endif
 #ifndef GRACE_EPT_Y
 #define GRACE_EPT_Y 16
-#endif
-#ifndef GRACE_EPT_Z
-#define GRACE_EPT_Z 32
 #endif
 #ifndef GRACE_Y_ELEMS
 #define GRACE_Y_ELEMS 16384  // complex values per K2/K4 tile
@@ -503,23 +693,25 @@ __host__ __device__ constexpr int tpc_of(int L, int ept) { return L >= ept ? L /
 __host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 template <int L>
-struct XCfg {  // K1 rows / K5 rows (3 components per row)
-  static constexpr int TPC1 = tpc_of(L, GRACE_EPT_X1);
-  static constexpr int TPC5 = tpc_of(L, GRACE_EPT_X5);
-  static constexpr int B1 = (L == 0) ? 256 : cmax(1, 256 / TPC1);
-  static constexpr int NT1 = (L == 0) ? 256 : B1 * TPC1;
-  static constexpr int B5 = (L == 0) ? 64 : cmax(1, 128 / TPC5);
-  static constexpr int NT5 = (L == 0) ? 256 : 3 * B5 * TPC5;
+struct XCfg {  // K1 / K5: B spatial rows x 3 components per CTA
+  static constexpr int TPC = tpc_of(L, GRACE_EPT_X);
+  static constexpr int B = (L == 0) ? 64 : cmax(1, 256 / TPC);
+  static constexpr int NT = (L == 0) ? 64 : B * TPC;
+  static constexpr int MINB1 = NT <= 256 ? GRACE_MINB_K1 : (NT <= 512 ? 2 : 1);
+  static constexpr int MINB5 = NT <= 256 ? GRACE_MINB_K5 : (NT <= 512 ? 2 : 1);
 };
 template <int L>
 struct YCfg {  // K2/K4 columns
   static constexpr int NCOL = cmax(2, cmin(32, GRACE_Y_ELEMS / L));
   static constexpr int NT = cmin(1024, cmax(32, NCOL * tpc_of(L, GRACE_EPT_Y)));
+  static constexpr int MINB = NT <= 256 ? 4 : (NT <= 512 ? 2 : 1);
 };
 template <int L>
-struct ZCfg {  // K3 and K2' (3 components, B kx columns each)
-  static constexpr int B = cmax(1, cmin(32, 2048 / L));
-  static constexpr int NT = cmax(32, 3 * B * tpc_of(L, GRACE_EPT_Z));
+struct ZCfg {  // K3 and K2'
+  static constexpr int B = ZPlan<L>::B;
+  static constexpr int NT = ZPlan<L>::NT;
+  static constexpr int MINB = NT <= 256 ? GRACE_MINB_Z : (NT <= 512 ? 2 : 1);
+  static constexpr size_t SMEM = (size_t)3 * TileIdx<L, B, true>::ELEMS * 8 + (size_t)6 * (L / 2 + 1) * B * 4;
 };
 
 template <class K>
@@ -539,13 +731,13 @@ static cudaError_t prep(K kern, size_t smem) {
 template <int L, bool DIST>
 static cudaError_t k1_launch(const Geom& g, const float* M, float2* X1, const float2* tw, StepParams* bump,
                              cudaStream_t st) {
-  constexpr int B = XCfg<L>::B1, NT = XCfg<L>::NT1;
-  const size_t smem = (L == 0) ? 0 : (size_t)TileIdx<(L > 0 ? L : 1), B, false>::SMEM_ELEMS * sizeof(float2);
-  auto kern = k1_fwd_x<L, B, NT, DIST>;
+  using C = XCfg<L>;
+  const size_t smem = (L == 0) ? 0 : (size_t)3 * TileIdx<(L > 0 ? L : 1), C::B, false>::ELEMS * sizeof(float2);
+  auto kern = k1_fwd_x<L, C::B, C::NT, C::MINB1, DIST>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
-  const int nrows = 3 * g.nzl * g.ny;
-  kern<<<(nrows + B - 1) / B, NT, smem, st>>>(M, X1, tw, g, bump);
+  const int nrows = g.nzl * g.ny;
+  kern<<<(nrows + C::B - 1) / C::B, C::NT, smem, st>>>(M, X1, tw, g, bump);
   return cudaGetLastError();
 }
 
@@ -553,10 +745,10 @@ cudaError_t launch_k1(const Geom& g, const float* M, float2* X1, const float2* t
                       cudaStream_t st) {
   if (g.Px == 1) return g.kb ? k1_launch<0, true>(g, M, X1, tw, bump, st) : k1_launch<0, false>(g, M, X1, tw, bump, st);
   const int L = g.Px / 2;
-#define CASE(v)                                                                                         \
-  case v:                                                                                               \
-    return (v < 2) ? cudaErrorInvalidValue                                                              \
-           : g.kb  ? k1_launch<(v >= 2 ? v : 2), true>(g, M, X1, tw, bump, st)                          \
+#define CASE(v)                                                                \
+  case v:                                                                      \
+    return (v < 2) ? cudaErrorInvalidValue                                     \
+           : g.kb  ? k1_launch<(v >= 2 ? v : 2), true>(g, M, X1, tw, bump, st) \
                    : k1_launch<(v >= 2 ? v : 2), false>(g, M, X1, tw, bump, st);
   GRACE_L_SWITCH(L, CASE)
 #undef CASE
@@ -565,38 +757,116 @@ cudaError_t launch_k1(const Geom& g, const float* M, float2* X1, const float2* t
 template <int L, bool INV>
 static cudaError_t ky_launch(const Geom& g, const float2* in, float2* out, const float2* tw, cudaStream_t st,
                              int in_rows, int out_rows, int n_in, int n_out) {
-  constexpr int NCOL = YCfg<L>::NCOL, NT = YCfg<L>::NT;
-  const size_t smem = (size_t)TileIdx<L, NCOL, true>::SMEM_ELEMS * sizeof(float2);
-  auto kern = k_y<L, NCOL, NT, INV>;
+  using C = YCfg<L>;
+  const size_t smem = (size_t)TileIdx<L, C::NCOL, true>::ELEMS * sizeof(float2);
+  auto kern = k_y<L, C::NCOL, C::NT, C::MINB, INV>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((g.Kc + NCOL - 1) / NCOL, 3 * g.nz);
-  kern<<<grid, NT, smem, st>>>(in, out, tw, g, in_rows, out_rows, n_in, n_out);
+  dim3 grid((g.Kc + C::NCOL - 1) / C::NCOL, 3 * g.nz);
+  kern<<<grid, C::NT, smem, st>>>(in, out, tw, g, in_rows, out_rows, n_in, n_out);
   return cudaGetLastError();
 }
 
-cudaError_t launch_k2(const Geom& g, const float2* X1, float2* X2, const float2* tw, cudaStream_t st) {
+template <int L>
+__host__ __device__ constexpr int ytma_ncol() {
+  return L >= 8192 ? 1 : (8192 / L > 32 ? 32 : (8192 / L < 2 ? 2 : 8192 / L));
+}
+constexpr int kTmaMinL = 64;
+
+template <int L, bool INV>
+static cudaError_t ky_tma_launch(const Geom& g, float2* out, const float2* tw, cudaStream_t st, int n_out,
+                                 const TmapBlob* tmap) {
+  constexpr int NCOL = ytma_ncol<L>();
+  using Y = YTma<L, NCOL>;
+  auto kern = k_y_tma<L, NCOL, INV>;
+  cudaError_t e = prep(kern, Y::SMEM);
+  if (e != cudaSuccess) return e;
+  const int ntiles = ((g.Kc + NCOL - 1) / NCOL) * 3 * g.nz;
+  const int grid = ntiles < g.nsm ? ntiles : g.nsm;
+  CUtensorMap map;
+  static_assert(sizeof(CUtensorMap) == sizeof(TmapBlob), "tensor map size");
+  memcpy(&map, tmap->b, sizeof map);
+  kern<<<grid, Y::NT, Y::SMEM, st>>>(map, out, tw, g, n_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_k2(const Geom& g, const float2* X1, float2* X2, const float2* tw, cudaStream_t st,
+                      const TmapBlob* tmap) {
+  if (tmap != nullptr && g.Py >= kTmaMinL) {
+#define CASE(v) case v: return (v >= kTmaMinL) ? ky_tma_launch<(v >= kTmaMinL ? v : kTmaMinL), false>(g, X2, tw, st, g.Py, tmap) : cudaErrorInvalidValue;
+    GRACE_L_SWITCH(g.Py, CASE)
+#undef CASE
+  }
 #define CASE(v) case v: return ky_launch<v, false>(g, X1, X2, tw, st, g.ny, g.Py, g.ny, g.Py);
   GRACE_L_SWITCH(g.Py, CASE)
 #undef CASE
 }
 
-cudaError_t launch_k4(const Geom& g, const float2* X2, float2* X1, const float2* tw, cudaStream_t st) {
+cudaError_t launch_k4(const Geom& g, const float2* X2, float2* X1, const float2* tw, cudaStream_t st,
+                      const TmapBlob* tmap) {
+  if (tmap != nullptr && g.Py >= kTmaMinL) {
+#define CASE(v) case v: return (v >= kTmaMinL) ? ky_tma_launch<(v >= kTmaMinL ? v : kTmaMinL), true>(g, X1, tw, st, g.ny, tmap) : cudaErrorInvalidValue;
+    GRACE_L_SWITCH(g.Py, CASE)
+#undef CASE
+  }
 #define CASE(v) case v: return ky_launch<v, true>(g, X2, X1, tw, st, g.Py, g.ny, g.Py, g.ny);
+  GRACE_L_SWITCH(g.Py, CASE)
+#undef CASE
+}
+
+// Host: 5-D tensor maps {kx, rows, z, component, block} over 8-byte elements.
+static cudaError_t encode5(TmapBlob* out, const void* base, const unsigned long long dims[5],
+                           const unsigned long long strides[4], unsigned box_cols, unsigned box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+    enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  cuuint64_t gd[5], gs[4];
+  for (int i = 0; i < 5; ++i) gd[i] = dims[i];
+  for (int i = 0; i < 4; ++i) gs[i] = strides[i];
+  const cuuint32_t box[5] = {box_cols, box_rows, 1, 1, 1};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(out->b), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5,
+                   const_cast<void*>(base), gd, gs, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int L>
+static cudaError_t ky_maps(const Geom& g, const float2* k2_in, const float2* x2, TmapBlob* k2map, TmapBlob* k4map) {
+  constexpr int NCOL = ytma_ncol<L>();
+  using Y = YTma<L, NCOL>;
+  const int nq = g.kb ? (g.nz / g.nzl) : 1;
+  const unsigned long long p1 = 8ull * g.pitch1, p2 = 8ull * g.pitch2;
+  const unsigned long long d2[5] = {(unsigned long long)g.Kc, (unsigned long long)g.ny, (unsigned long long)g.nzl, 3,
+                                    (unsigned long long)nq};
+  const unsigned long long s2[4] = {p1, p1 * g.ny, p1 * g.ny * g.nzl, p1 * g.ny * g.nzl * 3};
+  cudaError_t e = encode5(k2map, k2_in, d2, s2, NCOL, Y::br(false));
+  if (e != cudaSuccess) return e;
+  const unsigned long long d4[5] = {(unsigned long long)g.Kc, (unsigned long long)g.Py, (unsigned long long)g.nz, 3, 1};
+  const unsigned long long s4[4] = {p2, p2 * g.Py, p2 * g.Py * g.nz, p2 * g.Py * g.nz * 3};
+  return encode5(k4map, x2, d4, s4, NCOL, Y::br(true));
+}
+
+cudaError_t make_ky_tmaps(const Geom& g, const float2* k2_in, const float2* x2, TmapBlob* k2map, TmapBlob* k4map) {
+  if (g.Py < kTmaMinL || g.Kc < 1) return cudaErrorNotSupported;
+#define CASE(v) case v: return (v >= kTmaMinL) ? ky_maps<(v >= kTmaMinL ? v : kTmaMinL)>(g, k2_in, x2, k2map, k4map) : cudaErrorNotSupported;
   GRACE_L_SWITCH(g.Py, CASE)
 #undef CASE
 }
 
 template <int L>
 static cudaError_t k3_launch(const Geom& g, float2* X2, const float* KS, const float2* tw, cudaStream_t st) {
-  constexpr int B = ZCfg<L>::B, NT = ZCfg<L>::NT;
-  const size_t smem = (size_t)TileIdx<L, 3 * B, true>::SMEM_ELEMS * sizeof(float2) +
-                      (size_t)6 * (L / 2 + 1) * B * sizeof(float);
-  auto kern = k3_z<L, B, NT>;
-  cudaError_t e = prep(kern, smem);
+  using C = ZCfg<L>;
+  auto kern = k3_z<L, C::B, C::NT, C::MINB>;
+  cudaError_t e = prep(kern, C::SMEM);
   if (e != cudaSuccess) return e;
-  dim3 grid((g.Kc + B - 1) / B, g.Kyh);
-  kern<<<grid, NT, smem, st>>>(X2, KS, tw, g);
+  dim3 grid((g.Kc + C::B - 1) / C::B, g.Kyh);
+  kern<<<grid, C::NT, C::SMEM, st>>>(X2, KS, tw, g);
   return cudaGetLastError();
 }
 
@@ -616,12 +886,11 @@ int kernel_count(const Geom& g) { return fused_y_path(g) ? 3 : 5; }
 
 template <int L>
 static cudaError_t k2f_launch(const Geom& g, float2* X1, const float* KS, const float2* tw, cudaStream_t st) {
-  constexpr int B = ZCfg<L>::B, NT = ZCfg<L>::NT;
-  const size_t smem = (size_t)TileIdx<L, 3 * B, true>::SMEM_ELEMS * sizeof(float2);
-  auto kern = k2f_y_fused<L, B, NT>;
-  cudaError_t e = prep(kern, smem);
+  using C = ZCfg<L>;
+  auto kern = k2f_y_fused<L, C::B, C::NT, C::MINB>;
+  cudaError_t e = prep(kern, C::SMEM);
   if (e != cudaSuccess) return e;
-  k2f_y_fused<L, B, NT><<<(g.Kx + B - 1) / B, NT, smem, st>>>(X1, KS, tw, g);
+  kern<<<(g.Kx + C::B - 1) / C::B, C::NT, C::SMEM, st>>>(X1, KS, tw, g);
   return cudaGetLastError();
 }
 
@@ -635,14 +904,13 @@ template <int L, bool DIST>
 static cudaError_t k5_launch(const Geom& g, int mode, const float2* X1, const float* M, float* Mn, float* Hout,
                              const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st,
                              const float* Hlo, const float* Hhi) {
-  constexpr int B = XCfg<L>::B5, NT = XCfg<L>::NT5;
-  const size_t smem = (L == 0) ? (size_t)3 * B * sizeof(float)
-                               : (size_t)TileIdx<(L > 0 ? L : 1), 3 * B, false>::SMEM_ELEMS * sizeof(float2);
-  auto kern = k5_inv_x_llg<L, B, NT, DIST>;
+  using C = XCfg<L>;
+  const size_t smem = (L == 0) ? 0 : (size_t)3 * TileIdx<(L > 0 ? L : 1), C::B, false>::ELEMS * sizeof(float2);
+  auto kern = k5_inv_x_llg<L, C::B, C::NT, C::MINB5, DIST>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
   const int nrows = g.nzl * g.ny;
-  kern<<<(nrows + B - 1) / B, NT, smem, st>>>(X1, M, Mn, Hout, tw, g, prm, flag, mode, Hlo, Hhi);
+  kern<<<(nrows + C::B - 1) / C::B, C::NT, smem, st>>>(X1, M, Mn, Hout, tw, g, prm, flag, mode, Hlo, Hhi);
   return cudaGetLastError();
 }
 
@@ -653,10 +921,10 @@ cudaError_t launch_k5(const Geom& g, int mode, const float2* X1, const float* M,
     return g.kb ? k5_launch<0, true>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi)
                 : k5_launch<0, false>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi);
   const int L = g.Px / 2;
-#define CASE(v)                                                                                                 \
-  case v:                                                                                                       \
-    return (v < 2) ? cudaErrorInvalidValue                                                                      \
-           : g.kb  ? k5_launch<(v >= 2 ? v : 2), true>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi)   \
+#define CASE(v)                                                                                               \
+  case v:                                                                                                     \
+    return (v < 2) ? cudaErrorInvalidValue                                                                    \
+           : g.kb  ? k5_launch<(v >= 2 ? v : 2), true>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi) \
                    : k5_launch<(v >= 2 ? v : 2), false>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi);
   GRACE_L_SWITCH(L, CASE)
 #undef CASE

@@ -44,6 +44,7 @@ def partition(nx, nz, rank, nranks):
     if nranks == 1:
         return Slab(rank, 1, nz, 0, 0, kx)
     kb = (kx + nranks - 1) // nranks
+    kb += kb & 1  # even, so TMA row strides are 16-byte multiples
     cols = max(0, min(kx, (rank + 1) * kb) - rank * kb)
     nzl = nz // nranks
     return Slab(rank, nranks, nzl, rank * nzl, kb, cols)

@@ -70,5 +70,5 @@ def test_partition_edge_cases():
     with pytest.raises(ValueError):
         partition(16, 6, 0, 4)
     s = [partition(2, 4, r, 4) for r in range(4)]  # Kx = 3 < 4 ranks: one rank owns no kx column
-    assert [x.kx_columns for x in s] == [1, 1, 1, 0]
-    assert partition(1024, 32, 7, 8) == type(s[0])(7, 8, 4, 28, 129, 122)
+    assert [x.kx_columns for x in s] == [2, 1, 0, 0]  # kx block rounded up to even
+    assert partition(1024, 32, 7, 8) == type(s[0])(7, 8, 4, 28, 130, 115)
