@@ -237,6 +237,15 @@ struct ThreadMap {
 
 enum { kExt = 0, kLin = 1, kPad = 2 };  // where a pass reads from / writes to
 
+// twiddle read from a shared-memory table
+__device__ __forceinline__ float2 tw_lds(const float2* p) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n"
+               : "=f"(v.x), "=f"(v.y)
+               : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+
 // One Stockham pass P of an L-point transform (plan REV) over V components per
 // thread.  The pieces (load / compute / store) are exposed so kernels can fuse
 // work between passes (K3: forward last pass -> k-space multiply -> inverse
@@ -299,7 +308,7 @@ struct Pass {
           else v[q][w][r] = s[w * T::ELEMS + T::at(tm.b, T::padrow(tm.jb + C))];
         }
   }
-  template <bool INV, bool HIN, bool HOUT>
+  template <bool INV, bool HIN, bool HOUT, bool TWS = false>
   __device__ __forceinline__ void compute(const TM& tm, const float2* __restrict__ tw, int twstride) {
     constexpr int RIN = HIN ? R / 2 : R;
 #pragma unroll
@@ -308,7 +317,7 @@ struct Pass {
         const int k1 = jm(tm, q) * ((L / (NS * R)) * twstride);
 #pragma unroll
         for (int r = 1; r < RIN; ++r) {
-          const float2 t = __ldg(tw + k1 * r);
+          const float2 t = TWS ? tw_lds(tw + k1 * r) : __ldg(tw + k1 * r);
 #pragma unroll
           for (int w = 0; w < V; ++w) v[q][w][r] = INV ? cmulc(v[q][w][r], t) : cmul(v[q][w][r], t);
         }
@@ -350,7 +359,7 @@ struct Pass {
 
 // Run pass P with sources/destinations SRC/DST (kExt functor, kLin / kPad smem).
 template <int L, int P, bool REV, int NCOL, int NT, bool COLMODE, int V, bool INV, bool HIN, bool HOUT, int SRC,
-          int DST, class LD, class ST>
+          int DST, bool TWS = false, class LD, class ST>
 __device__ __forceinline__ void fft_pass(const ThreadMap<L, NCOL, NT, COLMODE>& tm, const LD& ld, const ST& st,
                                          float2* s, const float2* __restrict__ tw, int twstride) {
   using PS = Pass<L, P, REV, NCOL, NT, COLMODE, V>;
@@ -366,33 +375,33 @@ __device__ __forceinline__ void fft_pass(const ThreadMap<L, NCOL, NT, COLMODE>& 
   constexpr bool DST_SMEM = (DST != kExt) || ST::kSmem();
   if constexpr (SRC_SMEM && DST_SMEM) __syncthreads();  // in-place hazard
   if (act) {
-    ps.template compute<INV, HIN, HOUT>(tm, tw, twstride);
+    ps.template compute<INV, HIN, HOUT, TWS>(tm, tw, twstride);
     if constexpr (DST == kExt) ps.template store_ext<ROUT>(tm, st);
     else ps.template store_smem<ROUT, DST == kPad>(tm, s);
   }
 }
 
 template <int L, int P, bool REV, int NCOL, int NT, bool COLMODE, int V, bool INV, bool HIN, bool HOUT, int SRC0,
-          int DSTN, class LD, class ST>
+          int DSTN, bool TWS = false, class LD, class ST>
 __device__ __forceinline__ void fft_passes(const ThreadMap<L, NCOL, NT, COLMODE>& tm, float2* s, const LD& ld,
                                            const ST& st, const float2* __restrict__ tw, int twstride) {
   constexpr int NP = fft_npass(L);
   constexpr bool first = (P == 0), last = (P == NP - 1);
   constexpr int IFACE0 = TileIdx<L, NCOL, COLMODE, Plan<L, REV>::R(0)>::PAD ? kPad : kLin;
   if constexpr (first && last) {
-    fft_pass<L, P, REV, NCOL, NT, COLMODE, V, INV, HIN, HOUT, SRC0, DSTN>(tm, ld, st, s, tw, twstride);
+    fft_pass<L, P, REV, NCOL, NT, COLMODE, V, INV, HIN, HOUT, SRC0, DSTN, TWS>(tm, ld, st, s, tw, twstride);
   } else if constexpr (first) {
-    fft_pass<L, P, REV, NCOL, NT, COLMODE, V, INV, HIN, false, SRC0, IFACE0>(tm, ld, st, s, tw, twstride);
+    fft_pass<L, P, REV, NCOL, NT, COLMODE, V, INV, HIN, false, SRC0, IFACE0, TWS>(tm, ld, st, s, tw, twstride);
     __syncthreads();
-    fft_passes<L, P + 1, REV, NCOL, NT, COLMODE, V, INV, HIN, HOUT, SRC0, DSTN>(tm, s, ld, st, tw, twstride);
+    fft_passes<L, P + 1, REV, NCOL, NT, COLMODE, V, INV, HIN, HOUT, SRC0, DSTN, TWS>(tm, s, ld, st, tw, twstride);
   } else {
     constexpr int SRCP = (P == 1) ? IFACE0 : kLin;
     if constexpr (last) {
-      fft_pass<L, P, REV, NCOL, NT, COLMODE, V, INV, false, HOUT, SRCP, DSTN>(tm, ld, st, s, tw, twstride);
+      fft_pass<L, P, REV, NCOL, NT, COLMODE, V, INV, false, HOUT, SRCP, DSTN, TWS>(tm, ld, st, s, tw, twstride);
     } else {
-      fft_pass<L, P, REV, NCOL, NT, COLMODE, V, INV, false, false, SRCP, kLin>(tm, ld, st, s, tw, twstride);
+      fft_pass<L, P, REV, NCOL, NT, COLMODE, V, INV, false, false, SRCP, kLin, TWS>(tm, ld, st, s, tw, twstride);
       __syncthreads();
-      fft_passes<L, P + 1, REV, NCOL, NT, COLMODE, V, INV, HIN, HOUT, SRC0, DSTN>(tm, s, ld, st, tw, twstride);
+      fft_passes<L, P + 1, REV, NCOL, NT, COLMODE, V, INV, HIN, HOUT, SRC0, DSTN, TWS>(tm, s, ld, st, tw, twstride);
     }
   }
 }
@@ -482,7 +491,7 @@ struct IsTileSt<SmemSt<L, N, C>> : std::true_type {};
 // itself (linear layout).  s holds V * TileIdx::ELEMS float2; the caller must
 // __syncthreads() before reusing s.  twstride = Lmax / L.  L == 1 is the identity.
 template <int L, int NCOL, int NT, bool COLMODE, bool INV, bool HIN = false, bool HOUT = false, int V = 1,
-          bool REV = false, class LD, class ST>
+          bool REV = false, bool TWS = false, class LD, class ST>
 __device__ __forceinline__ void fft_tile(float2* s, const LD& ld, const ST& st, const float2* __restrict__ tw,
                                          int twstride) {
   if constexpr (L == 1) {
@@ -493,7 +502,7 @@ __device__ __forceinline__ void fft_tile(float2* s, const LD& ld, const ST& st, 
     const ThreadMap<L, NCOL, NT, COLMODE> tm;
     constexpr int SRC0 = IsTileLd<LD>::value ? kLin : kExt;
     constexpr int DSTN = IsTileSt<ST>::value ? kLin : kExt;
-    fft_passes<L, 0, REV, NCOL, NT, COLMODE, V, INV, HIN, HOUT, SRC0, DSTN>(tm, s, ld, st, tw, twstride);
+    fft_passes<L, 0, REV, NCOL, NT, COLMODE, V, INV, HIN, HOUT, SRC0, DSTN, TWS>(tm, s, ld, st, tw, twstride);
   }
 }
 

@@ -192,7 +192,7 @@ template <int L, int NCOL>
 struct YTma {
   using T = TileIdx<L, NCOL, true>;
   static constexpr int TB = ((T::ELEMS * 8 + 1023) / 1024) * 1024;  // bytes per tile buffer
-  static constexpr size_t SMEM = 2 * (size_t)TB + 64;
+  static constexpr size_t SMEM = 2 * (size_t)TB + (size_t)L * 8 + 64;  // 2 tiles, twiddles w_L^k, barriers
   static constexpr int NT = NCOL * (L / 16);
   __host__ __device__ static constexpr int rows_in(bool inv) { return inv ? L : L / 2; }
   __host__ __device__ static constexpr int br(bool inv) { return rows_in(inv) < 256 ? rows_in(inv) : 256; }
@@ -210,7 +210,12 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, 1)
   constexpr unsigned TX = NCOL * ROWS * 8;
   extern __shared__ __align__(1024) unsigned char smraw[];
   float2* buf[2] = {reinterpret_cast<float2*>(smraw), reinterpret_cast<float2*>(smraw + Y::TB)};
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 2 * Y::TB);
+  float2* tws = reinterpret_cast<float2*>(smraw + 2 * Y::TB);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 2 * Y::TB + L * 8);
+  {
+    const int ts = g.Lmax / L;
+    for (int k = threadIdx.x; k < L; k += NT) tws[k] = __ldg(tw + k * ts);  // w_L^k
+  }
   const int ntx = (g.Kc + NCOL - 1) / NCOL;
   const int ntiles = ntx * 3 * g.nz;
   auto issue = [&](int t, float2* dst, uint64_t* b) {
@@ -253,7 +258,7 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, 1)
     const int kx0 = xt * NCOL;
     const St st{out + (INV ? xrow_slab(g, slab) : (size_t)slab * g.Py * g.pitch2) + kx0, INV ? g.pitch1 : g.pitch2,
                 n_out, g.Kc - kx0};
-    fft_tile<L, NCOL, NT, true, INV, !INV, INV>(cur, SmemLd<L, NCOL, true>{cur}, st, tw, g.Lmax / L);
+    fft_tile<L, NCOL, NT, true, INV, !INV, INV, 1, false, true>(cur, SmemLd<L, NCOL, true>{cur}, st, tws, 1);
     __syncthreads();
   }
 }
@@ -671,8 +676,11 @@ __global__ void __launch_bounds__(NT, MINB) k5_inv_x_llg(const float2* __restric
 // ---------------------------------------------------------------------------
 // Tile choices and dispatch.  EPT = complex values per thread
 // per pass and component.
-#ifndef GRACE_EPT_X
-#define GRACE_EPT_X 8
+#ifndef GRACE_EPT_K1
+#define GRACE_EPT_K1 8
+#endif
+#ifndef GRACE_EPT_K5
+#define GRACE_EPT_K5 8
 #endif
 #ifndef GRACE_MINB_K1
 #define GRACE_MINB_K1 3  // CTAs/SM the register budget of K1 (256 threads) is sized for
@@ -692,14 +700,17 @@ __global__ void __launch_bounds__(NT, MINB) k5_inv_x_llg(const float2* __restric
 __host__ __device__ constexpr int tpc_of(int L, int ept) { return L >= ept ? L / ept : 1; }
 __host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
-template <int L>
-struct XCfg {  // K1 / K5: B spatial rows x 3 components per CTA
-  static constexpr int TPC = tpc_of(L, GRACE_EPT_X);
+template <int L, int EPT, int MINB256>
+struct XCfgT {  // K1 / K5: B spatial rows x 3 components per CTA
+  static constexpr int TPC = tpc_of(L, EPT);
   static constexpr int B = (L == 0) ? 64 : cmax(1, 256 / TPC);
   static constexpr int NT = (L == 0) ? 64 : B * TPC;
-  static constexpr int MINB1 = NT <= 256 ? GRACE_MINB_K1 : (NT <= 512 ? 2 : 1);
-  static constexpr int MINB5 = NT <= 256 ? GRACE_MINB_K5 : (NT <= 512 ? 2 : 1);
+  static constexpr int MINB = NT <= 256 ? MINB256 : (NT <= 512 ? 2 : 1);
 };
+template <int L>
+using X1Cfg = XCfgT<L, GRACE_EPT_K1, GRACE_MINB_K1>;
+template <int L>
+using X5Cfg = XCfgT<L, GRACE_EPT_K5, GRACE_MINB_K5>;
 template <int L>
 struct YCfg {  // K2/K4 columns
   static constexpr int NCOL = cmax(2, cmin(32, GRACE_Y_ELEMS / L));
@@ -731,9 +742,9 @@ static cudaError_t prep(K kern, size_t smem) {
 template <int L, bool DIST>
 static cudaError_t k1_launch(const Geom& g, const float* M, float2* X1, const float2* tw, StepParams* bump,
                              cudaStream_t st) {
-  using C = XCfg<L>;
+  using C = X1Cfg<L>;
   const size_t smem = (L == 0) ? 0 : (size_t)3 * TileIdx<(L > 0 ? L : 1), C::B, false>::ELEMS * sizeof(float2);
-  auto kern = k1_fwd_x<L, C::B, C::NT, C::MINB1, DIST>;
+  auto kern = k1_fwd_x<L, C::B, C::NT, C::MINB, DIST>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
   const int nrows = g.nzl * g.ny;
@@ -904,9 +915,9 @@ template <int L, bool DIST>
 static cudaError_t k5_launch(const Geom& g, int mode, const float2* X1, const float* M, float* Mn, float* Hout,
                              const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st,
                              const float* Hlo, const float* Hhi) {
-  using C = XCfg<L>;
+  using C = X5Cfg<L>;
   const size_t smem = (L == 0) ? 0 : (size_t)3 * TileIdx<(L > 0 ? L : 1), C::B, false>::ELEMS * sizeof(float2);
-  auto kern = k5_inv_x_llg<L, C::B, C::NT, C::MINB5, DIST>;
+  auto kern = k5_inv_x_llg<L, C::B, C::NT, C::MINB, DIST>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
   const int nrows = g.nzl * g.ny;
