@@ -306,11 +306,14 @@ __device__ __forceinline__ void stage_ks(float* kss, const float* __restrict__ b
 // The forward input has n nonzero of L (HIN), the inverse keeps n outputs (HOUT).
 // FUSE (L <= 64): the forward last pass, the multiply and the inverse first pass
 // (reversed radix plan) run in registers without a shared-memory round trip.
+#ifndef GRACE_ZB
+#define GRACE_ZB 16  // kx columns per K3 / K2' CTA (at most)
+#endif
 template <int L>
 struct ZPlan {
   static constexpr bool FUSE = L >= 2 && L <= 64;
   static constexpr int RLAST = L <= 1 ? 1 : 1 << fft_pass_bits(L, fft_npass(L) - 1);
-  static constexpr int B = L <= 1 ? 32 : (2048 / L > 32 ? 32 : (2048 / L < 1 ? 1 : 2048 / L));
+  static constexpr int B = L <= 1 ? GRACE_ZB : (2048 / L > GRACE_ZB ? GRACE_ZB : (2048 / L < 1 ? 1 : 2048 / L));
   static constexpr int TPC = L <= 1 ? 1 : (FUSE ? L / RLAST : (L / 8 > 0 ? L / 8 : 1));
   static constexpr int NT = B * TPC < 32 ? 32 : B * TPC;
 };
@@ -680,7 +683,7 @@ __global__ void __launch_bounds__(NT, MINB) k5_inv_x_llg(const float2* __restric
 #define GRACE_EPT_K1 8
 #endif
 #ifndef GRACE_EPT_K5
-#define GRACE_EPT_K5 8
+#define GRACE_EPT_K5 16
 #endif
 #ifndef GRACE_MINB_K1
 #define GRACE_MINB_K1 3  // CTAs/SM the register budget of K1 (256 threads) is sized for
@@ -689,7 +692,7 @@ __global__ void __launch_bounds__(NT, MINB) k5_inv_x_llg(const float2* __restric
 #define GRACE_MINB_K5 2
 #endif
 #ifndef GRACE_MINB_Z
-#define GRACE_MINB_Z 3
+#define GRACE_MINB_Z 4
 #endif
 #ifndef GRACE_EPT_Y
 #define GRACE_EPT_Y 16
