@@ -198,8 +198,11 @@ struct YTma {
   __host__ __device__ static constexpr int br(bool inv) { return rows_in(inv) < 256 ? rows_in(inv) : 256; }
 };
 
+#ifndef GRACE_YT_MINB
+#define GRACE_YT_MINB 1
+#endif
 template <int L, int NCOL, bool INV>
-__global__ void __launch_bounds__(YTma<L, NCOL>::NT, 1)
+__global__ void __launch_bounds__(YTma<L, NCOL>::NT, GRACE_YT_MINB)
     k_y_tma(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, const float2* __restrict__ tw, Geom g,
             int n_out) {
   using Y = YTma<L, NCOL>;
@@ -781,9 +784,12 @@ static cudaError_t ky_launch(const Geom& g, const float2* in, float2* out, const
   return cudaGetLastError();
 }
 
+#ifndef GRACE_YT_ELEMS
+#define GRACE_YT_ELEMS 8192  // complex values per TMA y-pencil tile buffer
+#endif
 template <int L>
 __host__ __device__ constexpr int ytma_ncol() {
-  return L >= 8192 ? 1 : (8192 / L > 32 ? 32 : (8192 / L < 2 ? 2 : 8192 / L));
+  return GRACE_YT_ELEMS / L > 32 ? 32 : (GRACE_YT_ELEMS / L < 2 ? 2 : GRACE_YT_ELEMS / L);
 }
 constexpr int kTmaMinL = 64;
 
@@ -796,7 +802,9 @@ static cudaError_t ky_tma_launch(const Geom& g, float2* out, const float2* tw, c
   cudaError_t e = prep(kern, Y::SMEM);
   if (e != cudaSuccess) return e;
   const int ntiles = ((g.Kc + NCOL - 1) / NCOL) * 3 * g.nz;
-  const int grid = ntiles < g.nsm ? ntiles : g.nsm;
+  const int per_sm = (int)(220 * 1024 / Y::SMEM) < GRACE_YT_MINB ? (int)(220 * 1024 / Y::SMEM) : GRACE_YT_MINB;
+  const int cap = g.nsm * (per_sm > 0 ? per_sm : 1);
+  const int grid = ntiles < cap ? ntiles : cap;
   CUtensorMap map;
   static_assert(sizeof(CUtensorMap) == sizeof(TmapBlob), "tensor map size");
   memcpy(&map, tmap->b, sizeof map);
