@@ -41,19 +41,25 @@ UNIT = "cell-updates/s"
 
 # ------------------------------------------------------------------ helpers
 
-def algorithmic_bytes(geo, fused):
-    """Compulsory HBM bytes per launch of each kernel (DESIGN.md §7), unpadded Kx."""
+def algorithmic_bytes(geo, names):
+    """Compulsory HBM bytes per launch of each kernel (DESIGN.md §6), unpadded Kx."""
     nx, ny, nz = geo["nx"], geo["ny"], geo["nz"]
     Py, Kx, Kyh, Kzh = geo["Py"], geo["Kx"], geo["Kyh"], geo["Kzh"]
     N = nx * ny * nz
     x1 = 3 * nz * ny * Kx * 8
-    m = 12 * N
-    if fused:
-        ks = 4 * Kyh * Kx * 4
-        return {"K1": m + x1, "K2f": 2 * x1 + ks, "K5": x1 + 2 * m}
     x2 = 3 * nz * Py * Kx * 8
+    m = 12 * N
+    split = "K6" in names
     ks = 6 * Kzh * Kyh * Kx * 4 if geo["Pz"] > 1 else 4 * Kyh * Kx * 4
-    return {"K1": m + x1, "K2": x1 + x2, "K3": 2 * x2 + ks, "K4": x2 + x1, "K5": x1 + 2 * m}
+    b = {"K1": m + x1, "K2f": 2 * x1 + ks, "K2": x1 + x2, "K3": 2 * x2 + ks, "K4": x2 + x1,
+         "K5": x1 + (m if split else 2 * m), "K6": 3 * m}
+    return {k: b[k] for k in names}
+
+
+STEP_DESC = {"K1": "K1 x-R2C", "K2": "K2 y-FFT (TMA)", "K2f": "K2' y-FFT*N*iFFT", "K3": "K3 z-FFT*N*iFFT",
+             "K4": "K4 y-iFFT (TMA)", "K5": "K5 x-C2R (+LLG if fused)", "K6": "K6 exch+anis+Zeeman+LLG+Euler stencil"}
+KERNEL_NAMES = {3: ["K1", "K2f", "K5"], 4: ["K1", "K2f", "K5", "K6"], 5: ["K1", "K2", "K3", "K4", "K5"],
+                6: ["K1", "K2", "K3", "K4", "K5", "K6"]}
 
 
 def read_peaks():
@@ -225,8 +231,7 @@ def run_own(args, w):
     pb.grace_set_m_device(g.h, M0.data_ptr())
     g.set_hext(w.hext)
     geo = g.geometry
-    fused = geo["kernels"] == 3
-    names = ["K1", "K2f", "K5"] if fused else ["K1", "K2", "K3", "K4", "K5"]
+    names = KERNEL_NAMES[geo["kernels"]]
     g.step(args.warmup, w.dt)
     profile = not distributed
     if profile:
@@ -259,7 +264,7 @@ def run_own(args, w):
 
     # roofline of the dominant kernel
     peak, peak_src = read_peaks()
-    ab = algorithmic_bytes(geo, fused)
+    ab = algorithmic_bytes(geo, names)
     kern = {}
     if not profile:
         kms = [0.0] * len(names)
@@ -320,8 +325,7 @@ def run_own(args, w):
                    "parallelism": "single GPU" if world == 1 else
                    (f"z-slab x{world}: ncclAlltoAll transposes + halo planes (one grid)" if distributed
                     else f"{world} independent replicas (nz not divisible by {world})"),
-                   "step": "K1 x-R2C, K2 y-FFT, K3 z-FFT*N*iFFT, K4 y-iFFT, K5 x-C2R+exch+anis+Zeeman+LLG+Euler"
-                   if not fused else "K1 x-R2C, K2' y-FFT*N*iFFT, K5 x-C2R+local+LLG+Euler",
+                   "step": " | ".join(STEP_DESC[k] for k in names),
                    "timing": "libgrace profiling mode: eager launches, a CUDA event pair per kernel on the library stream"},
         "roofline": roofline,
         "kernels": kern,

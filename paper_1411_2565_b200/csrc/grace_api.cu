@@ -130,6 +130,7 @@ struct Rank {
   unsigned long long* flag = nullptr;  // [0] step non-finite, [1] set_m zero cell
   double* red = nullptr;               // mavg partials + 3 outputs
   float* Hbuf = nullptr;
+  float* Hd = nullptr;                 // H_demag [3][nzl][ny][nx] (split K5/K6 step)
   bool tma = false;                    // TMA descriptors of the K2 / K4 inputs built
   TmapBlob k2map{}, k4map{};
 };
@@ -278,11 +279,22 @@ struct grace_ctx {
   // One step M[c] -> M[1-c] (ev: optional 2 events per kernel, single mode).
   cudaError_t enqueue_step(int c, cudaStream_t s, cudaEvent_t* ev = nullptr) {
     CE(demag_stages(c, s, true, ev));
-    const int k5 = 2 * (kernel_count(g0) - 1);
+    const int nk = kernel_count(g0);
+    const int k5 = 2 * (nk - (g0.split_llg ? 2 : 1));
     if (ev) cudaEventRecord(ev[k5], s);
-    for (auto& rk : ranks)
-      CE(launch_k5(rk.g, 0, rk.A, rk.M[c], rk.M[1 - c], nullptr, tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+    for (auto& rk : ranks) {
+      if (g0.split_llg)
+        CE(launch_k5(rk.g, 2, rk.A, rk.M[c], nullptr, rk.Hd, tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+      else
+        CE(launch_k5(rk.g, 0, rk.A, rk.M[c], rk.M[1 - c], nullptr, tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+    }
     if (ev) cudaEventRecord(ev[k5 + 1], s);
+    if (g0.split_llg) {
+      if (ev) cudaEventRecord(ev[k5 + 2], s);
+      for (auto& rk : ranks)
+        CE(launch_k6(rk.g, 0, rk.Hd, rk.M[c], rk.M[1 - c], nullptr, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+      if (ev) cudaEventRecord(ev[k5 + 3], s);
+    }
     return cudaSuccess;
   }
 
@@ -309,7 +321,8 @@ struct grace_ctx {
     }
     for (auto e : ev) cudaEventDestroy(e);
     for (auto& rk : ranks) {
-      void* ptrs[] = {rk.M[0], rk.M[1], rk.A, rk.B, rk.X2, rk.KS, rk.Hlo, rk.Hhi, rk.prm, rk.flag, rk.red, rk.Hbuf};
+      void* ptrs[] = {rk.M[0], rk.M[1], rk.A,   rk.B,    rk.X2,  rk.KS,   rk.Hlo,
+                      rk.Hhi,  rk.prm,  rk.flag, rk.red, rk.Hbuf, rk.Hd};
       for (void* p : ptrs)
         if (p) cudaFree(p);
     }
@@ -353,6 +366,8 @@ int make_geom(int nx, int ny, int nz, double dx, double dy, double dz, double Ms
   g.Kc = g.Kx;
   g.pitch2 = g.Kxp;
   g.has_lo = g.has_hi = 0;
+  const char* fz = getenv("GRACE_K5_FUSED");
+  g.split_llg = (fz && fz[0] == '1') ? 0 : 1;
   int dev = 0, nsm = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   cudaGetLastError();
@@ -457,7 +472,8 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
         (g.has_lo && (rc = h->alloc((void**)&rk.Hlo, hb))) || (g.has_hi && (rc = h->alloc((void**)&rk.Hhi, hb))) ||
         (rc = h->alloc((void**)&rk.prm, sizeof(StepParams))) ||
         (rc = h->alloc((void**)&rk.flag, 2 * sizeof(unsigned long long))) ||
-        (rc = h->alloc((void**)&rk.red, sizeof(double) * (kMavgPartials + 3))))
+        (rc = h->alloc((void**)&rk.red, sizeof(double) * (kMavgPartials + 3))) ||
+        (g.split_llg && (rc = h->alloc((void**)&rk.Hd, mb))))
       return bail(rc);
   }
   if ((rc = h->alloc((void**)&h->tw, sizeof(float2) * g0.Lmax))) return bail(rc);
@@ -689,8 +705,14 @@ int grace_heff(grace_ctx* h, double* out) {
     }
   CUDA_OR(h->upload_params(1e-15));
   CUDA_OR(h->demag_stages(h->cur, s, false));
-  for (auto& rk : h->ranks)
-    CUDA_OR(launch_k5(rk.g, 1, rk.A, rk.M[h->cur], nullptr, rk.Hbuf, h->tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+  for (auto& rk : h->ranks) {
+    if (rk.g.split_llg) {
+      CUDA_OR(launch_k5(rk.g, 2, rk.A, rk.M[h->cur], nullptr, rk.Hd, h->tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+      CUDA_OR(launch_k6(rk.g, 1, rk.Hd, rk.M[h->cur], nullptr, rk.Hbuf, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+    } else {
+      CUDA_OR(launch_k5(rk.g, 1, rk.A, rk.M[h->cur], nullptr, rk.Hbuf, h->tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+    }
+  }
   for (auto& rk : h->ranks) {
     double* stage = reinterpret_cast<double*>(rk.A);
     const size_t off = slab_offset(h, rk);

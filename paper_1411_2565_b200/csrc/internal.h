@@ -38,6 +38,7 @@ struct Geom {
   int pitch2;       // row pitch of X2
   int has_lo, has_hi;  // z-1 / z+1 halo planes present
   int nsm;             // SMs of the device (persistent grids)
+  int split_llg;       // 1: K5 stores H_demag and K6 does the local terms + update (streaming)
   float cx, cy, cz; // exchange 2A/(mu0 Ms^2 d^2) per axis (0 for a singleton axis)
   float ck;         // anisotropy 2Ku/(mu0 Ms^2)
   float Ms;
@@ -63,11 +64,15 @@ cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* 
 cudaError_t launch_k4(const Geom& g, const float2* X2, float2* X1, const float2* tw, cudaStream_t st,
                       const TmapBlob* tmap = nullptr);
 cudaError_t launch_k2f(const Geom& g, float2* X1, const float* KS, const float2* tw, cudaStream_t st);
-// mode 0: LLG Euler step M -> Mn; mode 1: store H_eff into Hout.
+// mode 0: LLG Euler step M -> Mn; mode 1: store H_eff into Hout; mode 2: store H_demag into Hout.
 // Hlo / Hhi: halo planes [3][ny][nx] of z-1 / z+1 (used when g.has_lo / g.has_hi).
 cudaError_t launch_k5(const Geom& g, int mode, const float2* X1, const float* M, float* Mn, float* Hout,
                       const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st,
                       const float* Hlo = nullptr, const float* Hhi = nullptr);
+// K6 (split step): local terms + LLG + Euler from H_demag (mode 0: M -> Mn; mode 1: H_eff -> Hout).
+cudaError_t launch_k6(const Geom& g, int mode, const float* Hd, const float* M, float* Mn, float* Hout,
+                      const StepParams* prm, unsigned long long* flag, cudaStream_t st, const float* Hlo,
+                      const float* Hhi);
 bool fused_y_path(const Geom& g);  // nz == 1 and the y-pencils of 3 components fit one CTA
 int kernel_count(const Geom& g);   // kernels per step
 

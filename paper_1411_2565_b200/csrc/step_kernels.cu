@@ -514,8 +514,9 @@ struct CellCtx {
   int mode;
 };
 
-__device__ __forceinline__ float2 ld2(const float* p, bool pair_ok) {
-  // (p[0], p[1]); p[1] only if pair_ok.  8-byte aligned when pair_ok and nx even.
+__device__ __forceinline__ float2 ld2(const float* p, bool pair_ok, bool vec) {
+  // (p[0], p[1]); p[1] only if pair_ok.  vec: one 8-byte load (nx even, x0 even: aligned).
+  if (vec) return __ldg(reinterpret_cast<const float2*>(p));
   return pair_ok ? make_float2(__ldg(p), __ldg(p + 1)) : make_float2(__ldg(p), 0.f);
 }
 
@@ -537,25 +538,26 @@ __device__ __forceinline__ void cell_pair(const CellCtx& cc, const Geom& g, cons
   else if (DIST && g.has_hi) { zhi = cc.Hhi + (size_t)y * g.nx + x0; czhi = cc.plane; }
   else zhi = cc.M + i;
   const bool xm = x0 > 0, xp = x0 + 2 < g.nx;
+  const bool vec = hasB && ((g.nx & 1) == 0);
   float m[3][2], nx0[3], nx1[3], ny0[3][2], ny1[3][2], nz0[3][2], nz1[3][2];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     const float* mc = cc.M + c * cc.N;
-    const float2 mm = ld2(mc + i, hasB);
+    const float2 mm = ld2(mc + i, hasB, vec);
     m[c][0] = mm.x;
     m[c][1] = mm.y;
     nx0[c] = xm ? __ldg(mc + i - 1) : mm.x;
     nx1[c] = xp ? __ldg(mc + i + 2) : (hasB ? mm.y : mm.x);
-    const float2 a = ld2(mc + iy0, hasB), b = ld2(mc + iy1, hasB);
-    const float2 d = ld2(zlo + c * czlo, hasB), e = ld2(zhi + c * czhi, hasB);
+    const float2 a = ld2(mc + iy0, hasB, vec), b = ld2(mc + iy1, hasB, vec);
+    const float2 d = ld2(zlo + c * czlo, hasB, vec), e = ld2(zhi + c * czhi, hasB, vec);
     ny0[c][0] = a.x; ny0[c][1] = a.y;
     ny1[c][0] = b.x; ny1[c][1] = b.y;
     nz0[c][0] = d.x; nz0[c][1] = d.y;
     nz1[c][0] = e.x; nz1[c][1] = e.y;
   }
+  float out[2][3];
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
-    if (s == 1 && !hasB) break;
     const float* hd = s ? hB : hA;
     const float mx = m[0][s], my = m[1][s], mz = m[2][s];
     // Eq. (2): H_eff = H_demag + H_exch + H_anis + H_ext
@@ -567,7 +569,7 @@ __device__ __forceinline__ void cell_pair(const CellCtx& cc, const Geom& g, cons
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const float mc = m[c][s];
-      const float xl = s ? m[c][0] : nx0[c];                 // x-1
+      const float xl = s ? m[c][0] : nx0[c];                    // x-1
       const float xr = s ? nx1[c] : (hasB ? m[c][1] : nx1[c]);  // x+1
       float e = 0.f;
       e += g.cx * (xl - mc);
@@ -581,11 +583,10 @@ __device__ __forceinline__ void cell_pair(const CellCtx& cc, const Geom& g, cons
     hx += e3[0];
     hy += e3[1];
     hz += e3[2];
-    const size_t ic = i + s;
     if (cc.mode == 1) {
-      cc.Hout[ic] = hx;
-      cc.Hout[cc.N + ic] = hy;
-      cc.Hout[2 * cc.N + ic] = hz;
+      out[s][0] = hx;
+      out[s][1] = hy;
+      out[s][2] = hz;
       continue;
     }
     // Eq. (3): dM/dt = c_prec (M x H) + c_damp M x (M x H); Euler; renormalise (Q16)
@@ -595,12 +596,22 @@ __device__ __forceinline__ void cell_pair(const CellCtx& cc, const Geom& g, cons
     const float sy = my + p.dt * (p.c_prec * ay + p.c_damp * by);
     const float sz = mz + p.dt * (p.c_prec * az + p.c_damp * bz);
     const float sc = g.Ms / sqrtf(sx * sx + sy * sy + sz * sz);
-    const float ox = sx * sc, oy = sy * sc, oz = sz * sc;
-    cc.Mn[ic] = ox;
-    cc.Mn[cc.N + ic] = oy;
-    cc.Mn[2 * cc.N + ic] = oz;
-    if (!(isfinite(ox) && isfinite(oy) && isfinite(oz)))
-      atomicMin(cc.flag, ((unsigned long long)(p.step - 1) << 36) | (unsigned long long)ic);
+    out[s][0] = sx * sc;
+    out[s][1] = sy * sc;
+    out[s][2] = sz * sc;
+    if (!(isfinite(out[s][0]) && isfinite(out[s][1]) && isfinite(out[s][2])) && (s == 0 || hasB))
+      atomicMin(cc.flag, ((unsigned long long)(p.step - 1) << 36) | (unsigned long long)(i + s));
+  }
+  float* dst = cc.mode == 1 ? cc.Hout : cc.Mn;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    float* q = dst + c * cc.N + i;
+    if (vec) {
+      *reinterpret_cast<float2*>(q) = make_float2(out[0][c], out[1][c]);
+    } else {
+      q[0] = out[0][c];
+      if (hasB) q[1] = out[1][c];
+    }
   }
 }
 
@@ -626,6 +637,11 @@ __global__ void __launch_bounds__(NT, MINB) k5_inv_x_llg(const float2* __restric
       float h[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) h[c] = __ldg(X1 + c * cstrideX + (size_t)row * g.pitch1).x;
+      if (mode == 2) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) Hout[c * N + row] = h[c];
+        continue;
+      }
       cell_pair<DIST>(cc, g, p, row, 0, false, h, h);
     }
   } else {
@@ -663,6 +679,28 @@ __global__ void __launch_bounds__(NT, MINB) k5_inv_x_llg(const float2* __restric
     PS ps;
     fft_to_regs<L, B, NT, false, 3, true, false, true, false>(tm, smem, ld, tw, g.Lmax / L, ps);
     const int row = row0 + tm.b;
+    if (mode == 2) {  // split step: store H_demag, K6 applies the local terms and the update
+      if (PS::active(tm) && row < nrows) {
+        const bool vec = (g.nx & 1) == 0;
+#pragma unroll
+        for (int q = 0; q < PS::UPT; ++q)
+#pragma unroll
+          for (int r = 0; r < PS::R / 2; ++r) {
+            const int x0 = 2 * (PS::sb(tm) + PS::C2(q, r));
+            if (x0 >= g.nx) continue;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              float* h = Hout + c * N + (size_t)row * g.nx + x0;
+              if (vec) *reinterpret_cast<float2*>(h) = ps.v[q][c][r];
+              else {
+                h[0] = ps.v[q][c][r].x;
+                if (x0 + 1 < g.nx) h[1] = ps.v[q][c][r].y;
+              }
+            }
+          }
+      }
+      return;
+    }
     if (PS::active(tm) && row < nrows) {
 #pragma unroll
       for (int q = 0; q < PS::UPT; ++q)
@@ -676,6 +714,99 @@ __global__ void __launch_bounds__(NT, MINB) k5_inv_x_llg(const float2* __restric
           cell_pair<DIST>(cc, g, p, row, x0, x0 + 1 < g.nx, hA, hB);
         }
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6 (split step): Eq. (2) local terms + Eq. (3) + Euler from H_demag in HBM.
+// A streaming stencil: each thread owns 4 consecutive cells of a row (16-byte
+// loads), components are processed one after another to keep registers low.
+// mode 0: M -> Mn; mode 1: store H_eff into Hout.
+template <bool VEC, bool DIST>
+__global__ void __launch_bounds__(256) k6_llg(const float* __restrict__ Hd, const float* __restrict__ M,
+                                              float* __restrict__ Mn, float* __restrict__ Hout, Geom g,
+                                              const StepParams* __restrict__ prm, unsigned long long* __restrict__ flag,
+                                              int mode, const float* __restrict__ Hlo, const float* __restrict__ Hhi) {
+  constexpr int W = VEC ? 4 : 1;
+  const int nrows = g.nzl * g.ny;
+  const size_t N = (size_t)nrows * g.nx;
+  const size_t plane = (size_t)g.nx * g.ny;
+  const size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * W;
+  if (i >= N) return;
+  const StepParams p = *prm;
+  const int row = (int)(i / g.nx), x = (int)(i - (size_t)row * g.nx);
+  const int zl = row / g.ny, y = row - zl * g.ny;
+  auto ldw = [&](const float* q, float* o) {
+    if constexpr (VEC) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(q));
+      o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    } else {
+      o[0] = __ldg(q);
+    }
+  };
+  const float cxyz[3] = {g.cx, g.cy, g.cz};
+  float m[3][W], h[3][W];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const float* mc = M + c * N;
+    float a[W], t[W];
+    ldw(mc + i, a);
+    ldw(Hd + c * N + i, t);
+    const float xl = x > 0 ? __ldg(mc + i - 1) : a[0];
+    const float xr = x + W < g.nx ? __ldg(mc + i + W) : a[W - 1];
+    float ym[W], yp[W], zm[W], zp[W];
+    if (y > 0) ldw(mc + i - g.nx, ym); else { for (int s = 0; s < W; ++s) ym[s] = a[s]; }
+    if (y + 1 < g.ny) ldw(mc + i + g.nx, yp); else { for (int s = 0; s < W; ++s) yp[s] = a[s]; }
+    if (zl > 0) ldw(mc + i - plane, zm);
+    else if (DIST && g.has_lo) ldw(Hlo + c * plane + (size_t)y * g.nx + x, zm);
+    else { for (int s = 0; s < W; ++s) zm[s] = a[s]; }
+    if (zl + 1 < g.nzl) ldw(mc + i + plane, zp);
+    else if (DIST && g.has_hi) ldw(Hhi + c * plane + (size_t)y * g.nx + x, zp);
+    else { for (int s = 0; s < W; ++s) zp[s] = a[s]; }
+#pragma unroll
+    for (int s = 0; s < W; ++s) {
+      const float l = s > 0 ? a[s - 1] : xl, r = s + 1 < W ? a[s + 1] : xr;
+      // Eq. (2): H_demag + six-neighbour exchange (difference form, Q11) + Zeeman (+ x anisotropy)
+      float e = 0.f;
+      e += cxyz[0] * (l - a[s]);
+      e += cxyz[0] * (r - a[s]);
+      e += cxyz[1] * (ym[s] - a[s]);
+      e += cxyz[1] * (yp[s] - a[s]);
+      e += cxyz[2] * (zm[s] - a[s]);
+      e += cxyz[2] * (zp[s] - a[s]);
+      float hv = t[s] + p.hext[c];
+      if (c == 0) hv += g.ck * a[s];
+      h[c][s] = hv + e;
+      m[c][s] = a[s];
+    }
+  }
+  float o[3][W];
+#pragma unroll
+  for (int s = 0; s < W; ++s) {
+    if (mode == 1) {
+      for (int c = 0; c < 3; ++c) o[c][s] = h[c][s];
+      continue;
+    }
+    const float mx = m[0][s], my = m[1][s], mz = m[2][s];
+    const float hx = h[0][s], hy = h[1][s], hz = h[2][s];
+    // Eq. (3): dM/dt = c_prec (M x H) + c_damp M x (M x H); Euler; renormalise (Q16)
+    const float ax = my * hz - mz * hy, ay = mz * hx - mx * hz, az = mx * hy - my * hx;
+    const float bx = my * az - mz * ay, by = mz * ax - mx * az, bz = mx * ay - my * ax;
+    const float sx = mx + p.dt * (p.c_prec * ax + p.c_damp * bx);
+    const float sy = my + p.dt * (p.c_prec * ay + p.c_damp * by);
+    const float sz = mz + p.dt * (p.c_prec * az + p.c_damp * bz);
+    const float sc = g.Ms / sqrtf(sx * sx + sy * sy + sz * sz);
+    o[0][s] = sx * sc;
+    o[1][s] = sy * sc;
+    o[2][s] = sz * sc;
+    if (!(isfinite(o[0][s]) && isfinite(o[1][s]) && isfinite(o[2][s])))
+      atomicMin(flag, ((unsigned long long)(p.step - 1) << 36) | (unsigned long long)(i + s));
+  }
+  float* dst = mode == 1 ? Hout : Mn;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    if constexpr (VEC) *reinterpret_cast<float4*>(dst + c * N + i) = make_float4(o[c][0], o[c][1], o[c][2], o[c][3]);
+    else dst[c * N + i] = o[c][0];
   }
 }
 
@@ -904,7 +1035,24 @@ cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* 
 }
 
 bool fused_y_path(const Geom& g) { return g.Pz == 1 && g.Py <= 512; }
-int kernel_count(const Geom& g) { return fused_y_path(g) ? 3 : 5; }
+int kernel_count(const Geom& g) { return (fused_y_path(g) ? 3 : 5) + (g.split_llg ? 1 : 0); }
+
+cudaError_t launch_k6(const Geom& g, int mode, const float* Hd, const float* M, float* Mn, float* Hout,
+                      const StepParams* prm, unsigned long long* flag, cudaStream_t st, const float* Hlo,
+                      const float* Hhi) {
+  const long long N = (long long)g.nzl * g.ny * g.nx;
+  const bool vec = g.nx % 4 == 0;
+  const long long threads = vec ? N / 4 : N;
+  const unsigned grid = (unsigned)((threads + 255) / 256);
+  if (vec) {
+    if (g.kb) k6_llg<true, true><<<grid, 256, 0, st>>>(Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi);
+    else k6_llg<true, false><<<grid, 256, 0, st>>>(Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi);
+  } else {
+    if (g.kb) k6_llg<false, true><<<grid, 256, 0, st>>>(Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi);
+    else k6_llg<false, false><<<grid, 256, 0, st>>>(Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi);
+  }
+  return cudaGetLastError();
+}
 
 template <int L>
 static cudaError_t k2f_launch(const Geom& g, float2* X1, const float* KS, const float2* tw, cudaStream_t st) {
