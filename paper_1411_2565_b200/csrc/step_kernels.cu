@@ -723,7 +723,7 @@ __global__ void __launch_bounds__(NT, MINB) k5_inv_x_llg(const float2* __restric
 // loads), components are processed one after another to keep registers low.
 // mode 0: M -> Mn; mode 1: store H_eff into Hout.
 template <bool VEC, bool DIST>
-__global__ void __launch_bounds__(256) k6_llg(const float* __restrict__ Hd, const float* __restrict__ M,
+__global__ void __launch_bounds__(256, 3) k6_llg(const float* __restrict__ Hd, const float* __restrict__ M,
                                               float* __restrict__ Mn, float* __restrict__ Hout, Geom g,
                                               const StepParams* __restrict__ prm, unsigned long long* __restrict__ flag,
                                               int mode, const float* __restrict__ Hlo, const float* __restrict__ Hhi) {
@@ -745,39 +745,44 @@ __global__ void __launch_bounds__(256) k6_llg(const float* __restrict__ Hd, cons
     }
   };
   const float cxyz[3] = {g.cx, g.cy, g.cz};
-  float m[3][W], h[3][W];
+  // all 24 loads (3 components x centre, Hd, 4 neighbour rows, 2 row ends) first
+  float a[3][W], t[3][W], ym[3][W], yp[3][W], zm[3][W], zp[3][W], xl[3], xr[3];
+  const size_t iym = y > 0 ? i - g.nx : i, iyp = y + 1 < g.ny ? i + g.nx : i;
+  const float* zlo = zl > 0 ? M + (i - plane) : ((DIST && g.has_lo) ? Hlo + (size_t)y * g.nx + x : M + i);
+  const float* zhi = zl + 1 < g.nzl ? M + (i + plane) : ((DIST && g.has_hi) ? Hhi + (size_t)y * g.nx + x : M + i);
+  const size_t czlo = (zl > 0 || !(DIST && g.has_lo)) ? N : plane;
+  const size_t czhi = (zl + 1 < g.nzl || !(DIST && g.has_hi)) ? N : plane;
+  const size_t ixl = x > 0 ? i - 1 : i, ixr = x + W < g.nx ? i + W : i + W - 1;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     const float* mc = M + c * N;
-    float a[W], t[W];
-    ldw(mc + i, a);
-    ldw(Hd + c * N + i, t);
-    const float xl = x > 0 ? __ldg(mc + i - 1) : a[0];
-    const float xr = x + W < g.nx ? __ldg(mc + i + W) : a[W - 1];
-    float ym[W], yp[W], zm[W], zp[W];
-    if (y > 0) ldw(mc + i - g.nx, ym); else { for (int s = 0; s < W; ++s) ym[s] = a[s]; }
-    if (y + 1 < g.ny) ldw(mc + i + g.nx, yp); else { for (int s = 0; s < W; ++s) yp[s] = a[s]; }
-    if (zl > 0) ldw(mc + i - plane, zm);
-    else if (DIST && g.has_lo) ldw(Hlo + c * plane + (size_t)y * g.nx + x, zm);
-    else { for (int s = 0; s < W; ++s) zm[s] = a[s]; }
-    if (zl + 1 < g.nzl) ldw(mc + i + plane, zp);
-    else if (DIST && g.has_hi) ldw(Hhi + c * plane + (size_t)y * g.nx + x, zp);
-    else { for (int s = 0; s < W; ++s) zp[s] = a[s]; }
+    ldw(mc + i, a[c]);
+    ldw(Hd + c * N + i, t[c]);
+    ldw(mc + iym, ym[c]);
+    ldw(mc + iyp, yp[c]);
+    ldw(zlo + c * czlo, zm[c]);
+    ldw(zhi + c * czhi, zp[c]);
+    xl[c] = __ldg(mc + ixl);
+    xr[c] = __ldg(mc + ixr);
+  }
+  float m[3][W], h[3][W];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
 #pragma unroll
     for (int s = 0; s < W; ++s) {
-      const float l = s > 0 ? a[s - 1] : xl, r = s + 1 < W ? a[s + 1] : xr;
+      const float l = s > 0 ? a[c][s - 1] : xl[c], r = s + 1 < W ? a[c][s + 1] : xr[c];
       // Eq. (2): H_demag + six-neighbour exchange (difference form, Q11) + Zeeman (+ x anisotropy)
       float e = 0.f;
-      e += cxyz[0] * (l - a[s]);
-      e += cxyz[0] * (r - a[s]);
-      e += cxyz[1] * (ym[s] - a[s]);
-      e += cxyz[1] * (yp[s] - a[s]);
-      e += cxyz[2] * (zm[s] - a[s]);
-      e += cxyz[2] * (zp[s] - a[s]);
-      float hv = t[s] + p.hext[c];
-      if (c == 0) hv += g.ck * a[s];
+      e += cxyz[0] * (l - a[c][s]);
+      e += cxyz[0] * (r - a[c][s]);
+      e += cxyz[1] * (ym[c][s] - a[c][s]);
+      e += cxyz[1] * (yp[c][s] - a[c][s]);
+      e += cxyz[2] * (zm[c][s] - a[c][s]);
+      e += cxyz[2] * (zp[c][s] - a[c][s]);
+      float hv = t[c][s] + p.hext[c];
+      if (c == 0) hv += g.ck * a[c][s];
       h[c][s] = hv + e;
-      m[c][s] = a[s];
+      m[c][s] = a[c][s];
     }
   }
   float o[3][W];
