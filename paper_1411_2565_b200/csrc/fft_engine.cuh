@@ -46,15 +46,25 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
 }
 
 __host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
-__host__ __device__ constexpr int fft_npass(int L) { return (ilog2(L) + 3) / 4; }
-__host__ __device__ constexpr int fft_pass_bits(int L, int p) {
-  return ilog2(L) / fft_npass(L) + (p < ilog2(L) % fft_npass(L) ? 1 : 0);
+// Radix plan: npass = ceil(log2 L / RB) passes, bits spread as evenly as possible
+// (larger radices first); RB = 4 allows radix 16, RB = 3 caps the radix at 8.
+__host__ __device__ constexpr int fft_npass(int L, int RB = 4) { return (ilog2(L) + RB - 1) / RB; }
+__host__ __device__ constexpr int fft_pass_bits(int L, int p, int RB = 4) {
+  return ilog2(L) / fft_npass(L, RB) + (p < ilog2(L) % fft_npass(L, RB) ? 1 : 0);
 }
 // product of the radices of passes < p
-__host__ __device__ constexpr int fft_ns(int L, int p) {
-  return p == 0 ? 1 : fft_ns(L, p - 1) << fft_pass_bits(L, p - 1);
+__host__ __device__ constexpr int fft_ns(int L, int p, int RB = 4) {
+  return p == 0 ? 1 : fft_ns(L, p - 1, RB) << fft_pass_bits(L, p - 1, RB);
 }
-__host__ __device__ constexpr int fft_rmax(int L) { return L <= 1 ? 1 : 1 << fft_pass_bits(L, 0); }
+__host__ __device__ constexpr int fft_rmax(int L, int RB = 4) { return L <= 1 ? 1 : 1 << fft_pass_bits(L, 0, RB); }
+// Radix cap of row-mode kernels that carry the three components per thread.  A
+// radix-16 pass leaves half of their threads idle, but capping at 8 (one more
+// smem pass) measured slower on the slab (K1 0.431 vs 0.409 ms), so the default
+// keeps radix 16; the knob stays for other shapes.
+#ifndef GRACE_RB_ROWS3
+#define GRACE_RB_ROWS3 4
+#endif
+__host__ __device__ constexpr int rb_for(bool colmode, int V) { return (!colmode && V == 3) ? GRACE_RB_ROWS3 : 4; }
 
 // x * exp(-+2 pi i K/16) for compile-time K (forward sign -, INV conjugates).
 template <bool INV, int K>
@@ -163,10 +173,10 @@ __device__ __forceinline__ void dft_halfout(float2* a) {
 // Radix plan of an L-point transform; REV runs the same radices in reverse
 // order (an inverse that starts with the forward's last radix keeps every
 // thread's elements in place across a fused forward-last / inverse-first pass).
-template <int L, bool REV>
+template <int L, bool REV, int RB = 4>
 struct Plan {
-  static constexpr int NP = fft_npass(L);
-  __host__ __device__ static constexpr int bits(int p) { return fft_pass_bits(L, REV ? NP - 1 - p : p); }
+  static constexpr int NP = fft_npass(L, RB);
+  __host__ __device__ static constexpr int bits(int p) { return fft_pass_bits(L, REV ? NP - 1 - p : p, RB); }
   __host__ __device__ static constexpr int R(int p) { return 1 << bits(p); }
   __host__ __device__ static constexpr int NS(int p) { return p == 0 ? 1 : NS(p - 1) * R(p - 1); }
 };
@@ -188,7 +198,10 @@ struct TileIdx {
   static constexpr int RS = COLMODE ? NCOL : 1;
   // rows reserved per column: enough for the padding of either radix order
   // (the smallest radix of the plan pads the most)
-  static constexpr int RMIN = L <= 1 ? 1 : 1 << fft_pass_bits(L, fft_npass(L) - 1);
+  static constexpr int RMIN4 = L <= 1 ? 1 : 1 << fft_pass_bits(L, fft_npass(L, 4) - 1, 4);
+  static constexpr int RBR = GRACE_RB_ROWS3;  // row-mode V = 3 plans (see rb_for)
+  static constexpr int RMINR = L <= 1 ? 1 : 1 << fft_pass_bits(L, fft_npass(L, RBR) - 1, RBR);
+  static constexpr int RMIN = COLMODE ? RMIN4 : (RMINR < RMIN4 ? RMINR : RMIN4);
   static constexpr int ROWS = L + (PAD ? L / RMIN : 0);
   static constexpr int ELEMS = NCOL * ROWS;
   static constexpr int SMEM_ELEMS = ELEMS;
@@ -252,7 +265,8 @@ __device__ __forceinline__ float2 tw_lds(const float2* p) {
 // first pass, all in registers).
 template <int L, int P, bool REV, int NCOL, int NT, bool COLMODE, int V>
 struct Pass {
-  using PL = Plan<L, REV>;
+  static constexpr int RB = rb_for(COLMODE, V);
+  using PL = Plan<L, REV, RB>;
   using TM = ThreadMap<L, NCOL, NT, COLMODE>;
   using T = TileIdx<L, NCOL, COLMODE, PL::R(0)>;
   static constexpr int R = PL::R(P);
@@ -385,9 +399,10 @@ template <int L, int P, bool REV, int NCOL, int NT, bool COLMODE, int V, bool IN
           int DSTN, bool TWS = false, class LD, class ST>
 __device__ __forceinline__ void fft_passes(const ThreadMap<L, NCOL, NT, COLMODE>& tm, float2* s, const LD& ld,
                                            const ST& st, const float2* __restrict__ tw, int twstride) {
-  constexpr int NP = fft_npass(L);
+  constexpr int RB = rb_for(COLMODE, V);
+  constexpr int NP = fft_npass(L, RB);
   constexpr bool first = (P == 0), last = (P == NP - 1);
-  constexpr int IFACE0 = TileIdx<L, NCOL, COLMODE, Plan<L, REV>::R(0)>::PAD ? kPad : kLin;
+  constexpr int IFACE0 = TileIdx<L, NCOL, COLMODE, Plan<L, REV, RB>::R(0)>::PAD ? kPad : kLin;
   if constexpr (first && last) {
     fft_pass<L, P, REV, NCOL, NT, COLMODE, V, INV, HIN, HOUT, SRC0, DSTN, TWS>(tm, ld, st, s, tw, twstride);
   } else if constexpr (first) {
@@ -406,6 +421,25 @@ __device__ __forceinline__ void fft_passes(const ThreadMap<L, NCOL, NT, COLMODE>
   }
 }
 
+// Passes P .. NH-1 of a transform, each writing the smem tile (pass 0 reads `ld`).
+template <int L, int P, int NH, bool REV, int NCOL, int NT, bool COLMODE, int V, bool INV, bool HIN, class LD,
+          class ST>
+__device__ __forceinline__ void fft_head(const ThreadMap<L, NCOL, NT, COLMODE>& tm, float2* s, const LD& ld,
+                                         const ST& none, const float2* __restrict__ tw, int twstride) {
+  if constexpr (P < NH) {
+    constexpr int RB = rb_for(COLMODE, V);
+    constexpr int IFACE0 = TileIdx<L, NCOL, COLMODE, Plan<L, REV, RB>::R(0)>::PAD ? kPad : kLin;
+    if constexpr (P == 0) {
+      fft_pass<L, 0, REV, NCOL, NT, COLMODE, V, INV, HIN, false, kExt, IFACE0>(tm, ld, none, s, tw, twstride);
+    } else {
+      __syncthreads();
+      fft_pass<L, P, REV, NCOL, NT, COLMODE, V, INV, false, false, (P == 1 ? IFACE0 : kLin), kLin>(tm, ld, none, s,
+                                                                                                 tw, twstride);
+    }
+    fft_head<L, P + 1, NH, REV, NCOL, NT, COLMODE, V, INV, HIN>(tm, s, ld, none, tw, twstride);
+  }
+}
+
 // Passes 0 .. NP-2 of a transform (the first from `ld`, writing the smem tile),
 // then the last pass is loaded and computed into `ps` and left in registers:
 // output element i = PS::sb(tm) + PS::C2(q, r) of component w is ps.v[q][w][r].
@@ -413,8 +447,9 @@ template <int L, int NCOL, int NT, bool COLMODE, int V, bool INV, bool HIN, bool
           class PS>
 __device__ __forceinline__ void fft_to_regs(const ThreadMap<L, NCOL, NT, COLMODE>& tm, float2* s, const LD& ld,
                                             const float2* __restrict__ tw, int twstride, PS& ps) {
-  constexpr int NP = fft_npass(L);
-  constexpr int IFACE0 = TileIdx<L, NCOL, COLMODE, Plan<L, REV>::R(0)>::PAD ? kPad : kLin;
+  constexpr int RB = rb_for(COLMODE, V);
+  constexpr int NP = fft_npass(L, RB);
+  constexpr int IFACE0 = TileIdx<L, NCOL, COLMODE, Plan<L, REV, RB>::R(0)>::PAD ? kPad : kLin;
   if constexpr (NP == 1) {
     if (PS::active(tm)) {
       ps.template load_ext<HIN ? PS::R / 2 : PS::R>(tm, ld);
@@ -425,14 +460,7 @@ __device__ __forceinline__ void fft_to_regs(const ThreadMap<L, NCOL, NT, COLMODE
       __device__ static constexpr bool kSmem() { return true; }
       __device__ void operator()(int, int, int, int, float2) const {}
     } none;
-    if constexpr (NP == 2) {
-      fft_pass<L, 0, REV, NCOL, NT, COLMODE, V, INV, HIN, false, kExt, IFACE0>(tm, ld, none, s, tw, twstride);
-    } else {
-      fft_pass<L, 0, REV, NCOL, NT, COLMODE, V, INV, HIN, false, kExt, IFACE0>(tm, ld, none, s, tw, twstride);
-      __syncthreads();
-      fft_pass<L, 1, REV, NCOL, NT, COLMODE, V, INV, false, false, IFACE0, kLin>(tm, ld, none, s, tw, twstride);
-      static_assert(NP <= 3, "plans have at most 3 passes (L <= 4096)");
-    }
+    fft_head<L, 0, NP - 1, REV, NCOL, NT, COLMODE, V, INV, HIN>(tm, s, ld, none, tw, twstride);
     __syncthreads();
     if (PS::active(tm)) {
       ps.template load_smem<PS::R, NP == 2 && IFACE0 == kPad>(tm, s);
@@ -448,8 +476,9 @@ __device__ __forceinline__ void fft_to_regs(const ThreadMap<L, NCOL, NT, COLMODE
 template <int L, int NCOL, int NT, bool COLMODE, int V, bool INV, bool HOUT, bool REV, class ST, class PS>
 __device__ __forceinline__ void fft_from_regs(const ThreadMap<L, NCOL, NT, COLMODE>& tm, float2* s, const ST& st,
                                               const float2* __restrict__ tw, int twstride, PS& ps) {
-  constexpr int NP = fft_npass(L);
-  constexpr int IFACE0 = TileIdx<L, NCOL, COLMODE, Plan<L, REV>::R(0)>::PAD ? kPad : kLin;
+  constexpr int RB = rb_for(COLMODE, V);
+  constexpr int NP = fft_npass(L, RB);
+  constexpr int IFACE0 = TileIdx<L, NCOL, COLMODE, Plan<L, REV, RB>::R(0)>::PAD ? kPad : kLin;
   struct None {
     __device__ static constexpr bool kSmem() { return true; }
     __device__ float2 operator()(int, int, int, int) const { return make_float2(0.f, 0.f); }
@@ -465,13 +494,7 @@ __device__ __forceinline__ void fft_from_regs(const ThreadMap<L, NCOL, NT, COLMO
       ps.template store_smem<PS::R, IFACE0 == kPad>(tm, s);
     }
     __syncthreads();
-    if constexpr (NP == 2) {
-      fft_pass<L, 1, REV, NCOL, NT, COLMODE, V, INV, false, HOUT, IFACE0, kExt>(tm, none, st, s, tw, twstride);
-    } else {
-      fft_pass<L, 1, REV, NCOL, NT, COLMODE, V, INV, false, false, IFACE0, kLin>(tm, none, st, s, tw, twstride);
-      __syncthreads();
-      fft_pass<L, 2, REV, NCOL, NT, COLMODE, V, INV, false, HOUT, kLin, kExt>(tm, none, st, s, tw, twstride);
-    }
+    fft_passes<L, 1, REV, NCOL, NT, COLMODE, V, INV, false, HOUT, kExt, kExt>(tm, s, none, st, tw, twstride);
   }
 }
 

@@ -17,6 +17,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <type_traits>
 
 #include "fft_engine.cuh"
 #include "internal.h"
@@ -615,7 +616,7 @@ __device__ __forceinline__ void cell_pair(const CellCtx& cc, const Geom& g, cons
   }
 }
 
-template <int L, int B, int NT, int MINB, bool DIST>
+template <int L, int B, int NT, int MINB, bool DIST, bool EPI>
 __global__ void __launch_bounds__(NT, MINB) k5_inv_x_llg(const float2* __restrict__ X1, const float* __restrict__ M,
                                                          float* __restrict__ Mn, float* __restrict__ Hout,
                                                          const float2* __restrict__ tw, Geom g,
@@ -637,12 +638,12 @@ __global__ void __launch_bounds__(NT, MINB) k5_inv_x_llg(const float2* __restric
       float h[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) h[c] = __ldg(X1 + c * cstrideX + (size_t)row * g.pitch1).x;
-      if (mode == 2) {
+      if (!EPI || mode == 2) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) Hout[c * N + row] = h[c];
         continue;
       }
-      cell_pair<DIST>(cc, g, p, row, 0, false, h, h);
+      if constexpr (EPI) cell_pair<DIST>(cc, g, p, row, 0, false, h, h);
     }
   } else {
     const int twpx = g.Lmax / (2 * L);
@@ -674,12 +675,12 @@ __global__ void __launch_bounds__(NT, MINB) k5_inv_x_llg(const float2* __restric
         return make_float2(S.x - wD.y, S.y + wD.x);            // S + i w^-k D
       }
     } ld{X1, tw, cstrideX, row0, nrows, g.pitch1, twpx, g.kb, g.blk1};
-    using PS = Pass<L, fft_npass(L) - 1, false, B, NT, false, 3>;
+    using PS = Pass<L, fft_npass(L, rb_for(false, 3)) - 1, false, B, NT, false, 3>;
     const ThreadMap<L, B, NT, false> tm;
     PS ps;
     fft_to_regs<L, B, NT, false, 3, true, false, true, false>(tm, smem, ld, tw, g.Lmax / L, ps);
     const int row = row0 + tm.b;
-    if (mode == 2) {  // split step: store H_demag, K6 applies the local terms and the update
+    if (!EPI || mode == 2) {  // split step: store H_demag, K6 applies the local terms and the update
       if (PS::active(tm) && row < nrows) {
         const bool vec = (g.nx & 1) == 0;
 #pragma unroll
@@ -711,7 +712,7 @@ __global__ void __launch_bounds__(NT, MINB) k5_inv_x_llg(const float2* __restric
           if (x0 >= g.nx) continue;
           const float hA[3] = {ps.v[q][0][r].x, ps.v[q][1][r].x, ps.v[q][2][r].x};
           const float hB[3] = {ps.v[q][0][r].y, ps.v[q][1][r].y, ps.v[q][2][r].y};
-          cell_pair<DIST>(cc, g, p, row, x0, x0 + 1 < g.nx, hA, hB);
+          if constexpr (EPI) cell_pair<DIST>(cc, g, p, row, x0, x0 + 1 < g.nx, hA, hB);
         }
     }
   }
@@ -853,6 +854,14 @@ template <int L>
 using X1Cfg = XCfgT<L, GRACE_EPT_K1, GRACE_MINB_K1>;
 template <int L>
 using X5Cfg = XCfgT<L, GRACE_EPT_K5, GRACE_MINB_K5>;
+#ifndef GRACE_EPT_K5S
+#define GRACE_EPT_K5S 16
+#endif
+#ifndef GRACE_MINB_K5S
+#define GRACE_MINB_K5S 2
+#endif
+template <int L>
+using X5SCfg = XCfgT<L, GRACE_EPT_K5S, GRACE_MINB_K5S>;  // K5 of the split step (no LLG epilogue)
 template <int L>
 struct YCfg {  // K2/K4 columns
   static constexpr int NCOL = cmax(2, cmin(32, GRACE_Y_ELEMS / L));
@@ -1075,13 +1084,13 @@ cudaError_t launch_k2f(const Geom& g, float2* X1, const float* KS, const float2*
 #undef CASE
 }
 
-template <int L, bool DIST>
+template <int L, bool DIST, bool EPI>
 static cudaError_t k5_launch(const Geom& g, int mode, const float2* X1, const float* M, float* Mn, float* Hout,
                              const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st,
                              const float* Hlo, const float* Hhi) {
-  using C = X5Cfg<L>;
+  using C = std::conditional_t<EPI, X5Cfg<L>, X5SCfg<L>>;
   const size_t smem = (L == 0) ? 0 : (size_t)3 * TileIdx<(L > 0 ? L : 1), C::B, false>::ELEMS * sizeof(float2);
-  auto kern = k5_inv_x_llg<L, C::B, C::NT, C::MINB, DIST>;
+  auto kern = k5_inv_x_llg<L, C::B, C::NT, C::MINB, DIST, EPI>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
   const int nrows = g.nzl * g.ny;
@@ -1089,18 +1098,26 @@ static cudaError_t k5_launch(const Geom& g, int mode, const float2* X1, const fl
   return cudaGetLastError();
 }
 
+template <int L, bool DIST>
+static cudaError_t k5_launch2(const Geom& g, int mode, const float2* X1, const float* M, float* Mn, float* Hout,
+                              const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st,
+                              const float* Hlo, const float* Hhi) {
+  if (mode == 2) return k5_launch<L, DIST, false>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi);
+  return k5_launch<L, DIST, true>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi);
+}
+
 cudaError_t launch_k5(const Geom& g, int mode, const float2* X1, const float* M, float* Mn, float* Hout,
                       const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st,
                       const float* Hlo, const float* Hhi) {
   if (g.Px == 1)
-    return g.kb ? k5_launch<0, true>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi)
-                : k5_launch<0, false>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi);
+    return g.kb ? k5_launch2<0, true>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi)
+                : k5_launch2<0, false>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi);
   const int L = g.Px / 2;
 #define CASE(v)                                                                                               \
   case v:                                                                                                     \
     return (v < 2) ? cudaErrorInvalidValue                                                                    \
-           : g.kb  ? k5_launch<(v >= 2 ? v : 2), true>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi) \
-                   : k5_launch<(v >= 2 ? v : 2), false>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi);
+           : g.kb  ? k5_launch2<(v >= 2 ? v : 2), true>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi) \
+                   : k5_launch2<(v >= 2 ? v : 2), false>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi);
   GRACE_L_SWITCH(L, CASE)
 #undef CASE
 }
