@@ -213,7 +213,8 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, GRACE_YT_MINB)
   constexpr int NBOX = ROWS / BR;
   constexpr unsigned TX = NCOL * ROWS * 8;
   extern __shared__ __align__(1024) unsigned char smraw[];
-  float2* buf[2] = {reinterpret_cast<float2*>(smraw), reinterpret_cast<float2*>(smraw + Y::TB)};
+  // tile buffer k & 1 at smraw + (k & 1) * TB (pointer arithmetic on the shared
+  // array keeps every access in the shared address space: LDS/STS, not LD/ST)
   float2* tws = reinterpret_cast<float2*>(smraw + 2 * Y::TB);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 2 * Y::TB + L * 8);
   {
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, GRACE_YT_MINB)
   }
   __syncthreads();
   int t = blockIdx.x;
-  if (threadIdx.x == 0 && t < ntiles) issue(t, buf[0], bar);
+  if (threadIdx.x == 0 && t < ntiles) issue(t, reinterpret_cast<float2*>(smraw), bar);
   struct St {
     __device__ static constexpr bool kSmem() { return false; }
     float2* p;
@@ -252,10 +253,10 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, GRACE_YT_MINB)
     }
   };
   for (int k = 0; t < ntiles; ++k, t += gridDim.x) {
-    float2* cur = buf[k & 1];
+    float2* cur = reinterpret_cast<float2*>(smraw + (k & 1) * Y::TB);
     if (threadIdx.x == 0 && t + (int)gridDim.x < ntiles) {
       fence_proxy_async();
-      issue(t + gridDim.x, buf[(k + 1) & 1], bar + ((k + 1) & 1));
+      issue(t + gridDim.x, reinterpret_cast<float2*>(smraw + ((k + 1) & 1) * Y::TB), bar + ((k + 1) & 1));
     }
     mbar_wait(bar + (k & 1), (k >> 1) & 1);
     const int slab = t / ntx, xt = t - slab * ntx;
