@@ -179,7 +179,25 @@ struct Plan {
   __host__ __device__ static constexpr int bits(int p) { return fft_pass_bits(L, REV ? NP - 1 - p : p, RB); }
   __host__ __device__ static constexpr int R(int p) { return 1 << bits(p); }
   __host__ __device__ static constexpr int NS(int p) { return p == 0 ? 1 : NS(p - 1) * R(p - 1); }
+  // per-pass twiddle tables: pass p >= 1 holds w_{NS R}^{jm r} at [r][jm], R(p) NS(p) entries
+  __host__ __device__ static constexpr int twoff(int p) { return p <= 1 ? 0 : twoff(p - 1) + R(p - 1) * NS(p - 1); }
+  static constexpr int TW_ELEMS = twoff(NP);
 };
+
+// Fill the per-pass twiddle tables of Plan PL from the global table w_Lmax^k
+// (tw, twstride = Lmax / L) with threads [tid, nt).
+template <class PL, int L>
+__device__ __forceinline__ void fill_pass_twiddles(float2* dst, const float2* __restrict__ tw, int twstride, int tid,
+                                                   int nt) {
+#pragma unroll
+  for (int p = 1; p < PL::NP; ++p) {
+    const int R = PL::R(p), NS = PL::NS(p);
+    for (int e = tid; e < R * NS; e += nt) {
+      const int r = e / NS, jm = e - r * NS;
+      dst[PL::twoff(p) + e] = __ldg(tw + ((jm * r * (L / (NS * R))) % L) * twstride);
+    }
+  }
+}
 
 // Shared-memory tile addressing.  A tile holds NCOL columns of ROWS rows; row
 // stride RS and column stride CS depend on the mode:
@@ -328,10 +346,12 @@ struct Pass {
 #pragma unroll
     for (int q = 0; q < UPT; ++q) {
       if constexpr (NS > 1) {
-        const int k1 = jm(tm, q) * ((L / (NS * R)) * twstride);
+        const int jmq = jm(tm, q);
+        const int k1 = jmq * ((L / (NS * R)) * twstride);
 #pragma unroll
         for (int r = 1; r < RIN; ++r) {
-          const float2 t = TWS ? tw_lds(tw + k1 * r) : __ldg(tw + k1 * r);
+          // TWS: per-pass shared table [r][jm] (consecutive lanes -> consecutive words)
+          const float2 t = TWS ? tw_lds(tw + PL::twoff(P) + r * NS + jmq) : __ldg(tw + k1 * r);
 #pragma unroll
           for (int w = 0; w < V; ++w) v[q][w][r] = INV ? cmulc(v[q][w][r], t) : cmul(v[q][w][r], t);
         }

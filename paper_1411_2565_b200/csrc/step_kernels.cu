@@ -193,7 +193,9 @@ template <int L, int NCOL>
 struct YTma {
   using T = TileIdx<L, NCOL, true>;
   static constexpr int TB = ((T::ELEMS * 8 + 1023) / 1024) * 1024;  // bytes per tile buffer
-  static constexpr size_t SMEM = 2 * (size_t)TB + (size_t)L * 8 + 64;  // 2 tiles, twiddles w_L^k, barriers
+  using PL = Plan<L, false, 4>;
+  static constexpr int TWE = PL::TW_ELEMS > 1 ? PL::TW_ELEMS : 1;
+  static constexpr size_t SMEM = 2 * (size_t)TB + (size_t)TWE * 8 + 64;  // 2 tiles, per-pass twiddles, barriers
   static constexpr int NT = NCOL * (L / 16);
   __host__ __device__ static constexpr int rows_in(bool inv) { return inv ? L : L / 2; }
   __host__ __device__ static constexpr int br(bool inv) { return rows_in(inv) < 256 ? rows_in(inv) : 256; }
@@ -216,11 +218,8 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, GRACE_YT_MINB)
   // tile buffer k & 1 at smraw + (k & 1) * TB (pointer arithmetic on the shared
   // array keeps every access in the shared address space: LDS/STS, not LD/ST)
   float2* tws = reinterpret_cast<float2*>(smraw + 2 * Y::TB);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 2 * Y::TB + L * 8);
-  {
-    const int ts = g.Lmax / L;
-    for (int k = threadIdx.x; k < L; k += NT) tws[k] = __ldg(tw + k * ts);  // w_L^k
-  }
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 2 * Y::TB + Y::TWE * 8);
+  fill_pass_twiddles<typename Y::PL, L>(tws, tw, g.Lmax / L, threadIdx.x, NT);
   const int ntx = (g.Kc + NCOL - 1) / NCOL;
   const int ntiles = ntx * 3 * g.nz;
   auto issue = [&](int t, float2* dst, uint64_t* b) {
