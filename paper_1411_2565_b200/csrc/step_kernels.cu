@@ -719,6 +719,163 @@ __global__ void __launch_bounds__(NT, MINB) k5_inv_x_llg(const float2* __restric
 }
 
 // ---------------------------------------------------------------------------
+// K1 / K5 (split step) as persistent bulk-copy kernels.  One tile = RB rows of
+// the flattened (component, z, y) row index (each row transformed on its own,
+// V = 1), 512 threads, two tile buffers: while the FFT of tile t runs in place
+// in one buffer, one-dimensional bulk copies (cp.async.bulk, mbarrier
+// completion) bring the CTA's next tile into the other, so the row reads of
+// HBM overlap the radix passes instead of stalling the first one.
+//   FWD (K1): rows of M (nx floats) -> R2C post-process -> X1 rows
+//   !FWD (K5, mode 2): X1 rows (Kx = L + 1 complex; DIST: P blocks of kb)
+//              -> C2R pre-process -> H_demag rows (nx floats)
+// Requires nx % 4 == 0 (16-byte row copies); the launchers fall back to the
+// non-persistent kernels otherwise.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int L>
+struct XBulk {
+  static constexpr int RB = 8192 / L;  // rows per tile: 512 threads at 16 elements each
+  static constexpr int NT = RB * (L / 16);
+  using T = TileIdx<L, RB, false>;
+  static constexpr int TB = ((T::ELEMS * 8 + 1023) / 1024) * 1024;
+  using PL = Plan<L, false, 4>;
+  static constexpr int TWE = PL::TW_ELEMS > 1 ? PL::TW_ELEMS : 1;
+  static constexpr size_t SMEM = 2 * (size_t)TB + (size_t)TWE * 8 + 64;
+};
+constexpr int kXBulkMinL = 64, kXBulkMaxL = 4096;
+
+template <int L, bool FWD, bool DIST>
+__global__ void __launch_bounds__(XBulk<L>::NT, 1)
+    k_x_bulk(const void* __restrict__ in, void* __restrict__ out, const float2* __restrict__ tw, Geom g,
+             StepParams* bump) {
+  using X = XBulk<L>;
+  using T = typename X::T;
+  constexpr int RB = X::RB, NT = X::NT;
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  float2* tws = reinterpret_cast<float2*>(smraw + 2 * X::TB);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 2 * X::TB + X::TWE * 8);
+  if (FWD && bump != nullptr && blockIdx.x == 0 && threadIdx.x == 0) bump->step += 1;
+  fill_pass_twiddles<typename X::PL, L>(tws, tw, g.Lmax / L, threadIdx.x, NT);
+  const int nrows = g.nzl * g.ny;
+  const int total = 3 * nrows;
+  const int ntiles = (total + RB - 1) / RB;
+  const int nseg = (!FWD && DIST) ? g.nz / g.nzl : 1;
+  const unsigned seg = FWD ? 4u * g.nx : (DIST ? 8u * g.kb : 8u * (L + 2));
+  const int lane = threadIdx.x & 31;
+  const bool issuer = threadIdx.x < 32;
+  auto issue = [&](int t, unsigned char* dst, uint64_t* b) {  // warp 0
+    const int r0 = t * RB;
+    const int nv = total - r0 < RB ? total - r0 : RB;
+    if (lane == 0) mbar_expect_tx(b, (unsigned)(nv * nseg) * seg);
+    __syncwarp();
+    for (int u = lane; u < nv * nseg; u += 32) {
+      const int bb = u / nseg, q = u - bb * nseg;
+      const size_t gr = (size_t)(r0 + bb);
+      const void* src;
+      if constexpr (FWD) src = static_cast<const float*>(in) + gr * g.nx;
+      else if constexpr (DIST) src = static_cast<const float2*>(in) + q * g.blk1 + gr * g.pitch1;
+      else src = static_cast<const float2*>(in) + gr * g.pitch1;
+      bulk_load(dst + ((size_t)bb * T::ROWS + (size_t)q * g.kb) * 8, src, seg, b);
+    }
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  int t = blockIdx.x;
+  if (issuer && t < ntiles) issue(t, smraw, bar);
+  const int twpx = g.Lmax / (2 * L);
+  for (int k = 0; t < ntiles; ++k, t += gridDim.x) {
+    float2* cur = reinterpret_cast<float2*>(smraw + (k & 1) * X::TB);
+    if (issuer && t + (int)gridDim.x < ntiles) {
+      if (lane == 0) fence_proxy_async();
+      __syncwarp();
+      issue(t + gridDim.x, smraw + ((k + 1) & 1) * X::TB, bar + ((k + 1) & 1));
+    }
+    mbar_wait(bar + (k & 1), (k >> 1) & 1);
+    const int r0 = t * RB;
+    const int nv = total - r0 < RB ? total - r0 : RB;
+    if constexpr (FWD) {
+      struct Ld {
+        __device__ static constexpr bool kSmem() { return true; }
+        const float2* s;
+        int nh;  // nx / 2 complex inputs per row
+        __device__ float2 operator()(int b, int, int ib, int C) const {
+          const int i = ib + C;
+          return i < nh ? s[b * T::ROWS + i] : make_float2(0.f, 0.f);
+        }
+      } ld{cur, g.nx >> 1};
+      fft_tile<L, RB, NT, false, false, true, false, 1, false, true>(cur, ld, SmemSt<L, RB, false>{cur}, tws, 1);
+      __syncthreads();
+      // X[k] and X[L-k] from the same pair Z[k], Z[L-k] (w^(L-k) = -conj w^k);
+      // a thread keeps the row the FFT mapped to it.
+      constexpr int TPC = NT / RB;
+      const int b = threadIdx.x / TPC, jb = threadIdx.x - b * TPC;
+      if (b < nv) {
+        float2* X1 = static_cast<float2*>(out);
+        const size_t gr = (size_t)(r0 + b);
+        auto at = [&](int kk) -> size_t {
+          if constexpr (DIST) {
+            const int q = kk / g.kb;
+            return q * g.blk1 + gr * g.pitch1 + (kk - q * g.kb);
+          } else {
+            return gr * g.pitch1 + kk;
+          }
+        };
+        const float2* z = cur + b * T::ROWS;
+        auto post = [](float2 Zk, float2 Zn, float2 w) {
+          const float2 E = make_float2(0.5f * (Zk.x + Zn.x), 0.5f * (Zk.y - Zn.y));
+          const float2 D = make_float2(0.5f * (Zk.x - Zn.x), 0.5f * (Zk.y + Zn.y));
+          const float2 wD = cmul(w, D);
+          return make_float2(E.x + wD.y, E.y - wD.x);
+        };
+        for (int kk = jb; kk <= L / 2; kk += TPC) {
+          const float2 w = __ldg(tw + kk * twpx);
+          const float2 Zk = z[kk], Zn = z[(L - kk) & (L - 1)];
+          X1[at(kk)] = post(Zk, Zn, w);
+          if (kk < L / 2) X1[at(L - kk)] = post(Zn, Zk, make_float2(-w.x, w.y));
+        }
+      }
+    } else {
+      struct Ld {
+        __device__ static constexpr bool kSmem() { return true; }
+        const float2* s;
+        const float2* tw;
+        int twpx;
+        __device__ float2 operator()(int b, int, int ib, int C) const {
+          const int kk = ib + C;
+          const float2 a = s[b * T::ROWS + kk];
+          const float2 m = s[b * T::ROWS + (L - kk)];
+          const float2 S = make_float2(a.x + m.x, a.y - m.y);  // X[k] + conj X[L-k]
+          const float2 D = make_float2(a.x - m.x, a.y + m.y);  // X[k] - conj X[L-k]
+          const float2 w = __ldg(tw + kk * twpx);                // exp(-2 pi i k/Px)
+          const float2 wD = cmulc(D, w);
+          return make_float2(S.x - wD.y, S.y + wD.x);  // S + i w^-k D
+        }
+      } ld{cur, tw, twpx};
+      struct St {
+        __device__ static constexpr bool kSmem() { return false; }
+        float* H;
+        int nx, nv;
+        __device__ void operator()(int b, int, int ib, int C, float2 v) const {
+          const int x0 = 2 * (ib + C);
+          if (b < nv && x0 < nx) *reinterpret_cast<float2*>(H + (size_t)b * nx + x0) = v;
+        }
+      } st{static_cast<float*>(out) + (size_t)r0 * g.nx, g.nx, nv};
+      fft_tile<L, RB, NT, false, true, false, true, 1, false, true>(cur, ld, st, tws, 1);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K6 (split step): Eq. (2) local terms + Eq. (3) + Euler from H_demag in HBM.
 // A streaming stencil: each thread owns 4 consecutive cells of a row (16-byte
 // loads), components are processed one after another to keep registers low.
@@ -884,6 +1041,36 @@ static cudaError_t prep(K kern, size_t smem) {
   return e;
 }
 
+// Persistent bulk-copy x kernels: 16-byte row copies and the raw X1 row
+// (P blocks of kb on the distributed path) inside one tile row.
+template <int L>
+static bool xbulk_ok(const Geom& g, bool fwd) {
+#ifdef GRACE_NO_XBULK
+  return false;
+#endif
+#ifndef GRACE_XBULK_FWD
+  if (fwd) return false;  // K1: the V = 3 kernel measured faster (0.41 vs 0.48 ms on the slab)
+#endif
+  constexpr int ROWS = XBulk<L>::T::ROWS;
+  if (g.nx % 4 != 0) return false;
+  if (fwd) return true;
+  if (g.kb) return (g.kb % 2 == 0) && (g.blk1 % 2 == 0) && (long long)(g.nz / g.nzl) * g.kb <= ROWS;
+  return g.pitch1 % 2 == 0 && g.pitch1 >= L + 2 && ROWS >= L + 2;
+}
+
+template <int L, bool FWD, bool DIST>
+static cudaError_t xbulk_launch(const Geom& g, const void* in, void* out, const float2* tw, StepParams* bump,
+                                cudaStream_t st) {
+  using X = XBulk<L>;
+  auto kern = k_x_bulk<L, FWD, DIST>;
+  cudaError_t e = prep(kern, X::SMEM);
+  if (e != cudaSuccess) return e;
+  const int ntiles = (3 * g.nzl * g.ny + X::RB - 1) / X::RB;
+  const int grid = ntiles < g.nsm ? ntiles : g.nsm;
+  kern<<<grid, X::NT, X::SMEM, st>>>(in, out, tw, g, bump);
+  return cudaGetLastError();
+}
+
 #define GRACE_L_SWITCH(Lval, CASE) \
   switch (Lval) {                   \
     CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64) CASE(128) CASE(256) CASE(512) CASE(1024) CASE(2048) CASE(4096) \
@@ -895,6 +1082,9 @@ static cudaError_t k1_launch(const Geom& g, const float* M, float2* X1, const fl
                              cudaStream_t st) {
   using C = X1Cfg<L>;
   const size_t smem = (L == 0) ? 0 : (size_t)3 * TileIdx<(L > 0 ? L : 1), C::B, false>::ELEMS * sizeof(float2);
+  if constexpr (L >= kXBulkMinL && L <= kXBulkMaxL) {
+    if (xbulk_ok<L>(g, true)) return xbulk_launch<L, true, DIST>(g, M, X1, tw, bump, st);
+  }
   auto kern = k1_fwd_x<L, C::B, C::NT, C::MINB, DIST>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
@@ -982,6 +1172,9 @@ cudaError_t launch_k4(const Geom& g, const float2* X2, float2* X1, const float2*
 }
 
 // Host: 5-D tensor maps {kx, rows, z, component, block} over 8-byte elements.
+#ifndef GRACE_TMA_PROMO
+#define GRACE_TMA_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+#endif
 static cudaError_t encode5(TmapBlob* out, const void* base, const unsigned long long dims[5],
                            const unsigned long long strides[4], unsigned box_cols, unsigned box_rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
@@ -999,7 +1192,7 @@ static cudaError_t encode5(TmapBlob* out, const void* base, const unsigned long 
   const cuuint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r = enc(reinterpret_cast<CUtensorMap*>(out->b), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5,
                    const_cast<void*>(base), gd, gs, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   GRACE_TMA_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
@@ -1102,6 +1295,9 @@ template <int L, bool DIST>
 static cudaError_t k5_launch2(const Geom& g, int mode, const float2* X1, const float* M, float* Mn, float* Hout,
                               const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st,
                               const float* Hlo, const float* Hhi) {
+  if constexpr (L >= kXBulkMinL && L <= kXBulkMaxL) {
+    if (mode == 2 && xbulk_ok<L>(g, false)) return xbulk_launch<L, false, DIST>(g, X1, Hout, tw, nullptr, st);
+  }
   if (mode == 2) return k5_launch<L, DIST, false>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi);
   return k5_launch<L, DIST, true>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi);
 }

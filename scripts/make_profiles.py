@@ -36,6 +36,8 @@ def label(name):
         return "K2f"
     if "k5_inv_x_llg" in name:
         return "K5"
+    if "k6_llg" in name:
+        return "K6"
     return None
 
 

@@ -92,6 +92,9 @@ HEFF_CASES = [
     ((64, 48, 8), (5e-9, 5e-9, 3e-9), 8e5, 1.3e-11, 0.0, (0, 0, 0)),
     ((130, 3, 2), (1e-9, 1e-9, 1e-9), 1e6, 1e-11, 0.0, (0, 0, 0)),
     ((300, 7, 1), (1e-9, 1e-9, 1e-9), 1e6, 1e-11, 0.0, (0, 0, 0)),
+    ((6, 5, 40), (1e-9, 1e-9, 1e-9), 1e6, 1e-11, 0.0, (0, 0, 0)),      # Pz = 128: unfused K3
+    ((20, 300, 1), (2e-9, 1e-9, 1e-9), 8e5, 1.3e-11, 0.0, (0, 0, 0)),  # nz = 1, Py = 1024: K2/multiply/K4
+    ((9, 31, 3), (1e-9, 1e-9, 1e-9), 8e5, 1.3e-11, 1e4, (0, 0, 0)),    # odd nx: scalar load/store paths
 ]
 
 
