@@ -745,7 +745,8 @@ struct XBulk {
   static constexpr int TB = ((T::ELEMS * 8 + 1023) / 1024) * 1024;
   using PL = Plan<L, false, 4>;
   static constexpr int TWE = PL::TW_ELEMS > 1 ? PL::TW_ELEMS : 1;
-  static constexpr size_t SMEM = 2 * (size_t)TB + (size_t)TWE * 8 + 64;
+  static constexpr int PPE = L / 2 + 1;  // R2C post-process twiddles w^k, k = 0..L/2
+  static constexpr size_t SMEM = 2 * (size_t)TB + (size_t)(TWE + PPE) * 8 + 64;
 };
 constexpr int kXBulkMinL = 64, kXBulkMaxL = 4096;
 
@@ -758,9 +759,12 @@ __global__ void __launch_bounds__(XBulk<L>::NT, 1)
   constexpr int RB = X::RB, NT = X::NT;
   extern __shared__ __align__(1024) unsigned char smraw[];
   float2* tws = reinterpret_cast<float2*>(smraw + 2 * X::TB);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 2 * X::TB + X::TWE * 8);
+  float2* twp = tws + X::TWE;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 2 * X::TB + (X::TWE + X::PPE) * 8);
   if (FWD && bump != nullptr && blockIdx.x == 0 && threadIdx.x == 0) bump->step += 1;
   fill_pass_twiddles<typename X::PL, L>(tws, tw, g.Lmax / L, threadIdx.x, NT);
+  if constexpr (FWD)
+    for (int kk = threadIdx.x; kk < X::PPE; kk += NT) twp[kk] = __ldg(tw + kk * (g.Lmax / (2 * L)));
   const int nrows = g.nzl * g.ny;
   const int total = 3 * nrows;
   const int ntiles = (total + RB - 1) / RB;
@@ -836,11 +840,17 @@ __global__ void __launch_bounds__(XBulk<L>::NT, 1)
           const float2 wD = cmul(w, D);
           return make_float2(E.x + wD.y, E.y - wD.x);
         };
-        for (int kk = jb; kk <= L / 2; kk += TPC) {
-          const float2 w = __ldg(tw + kk * twpx);
+#pragma unroll
+        for (int i = 0; i < (L / 2) / TPC; ++i) {
+          const int kk = jb + i * TPC;
+          const float2 w = twp[kk];
           const float2 Zk = z[kk], Zn = z[(L - kk) & (L - 1)];
           X1[at(kk)] = post(Zk, Zn, w);
-          if (kk < L / 2) X1[at(L - kk)] = post(Zn, Zk, make_float2(-w.x, w.y));
+          X1[at(L - kk)] = post(Zn, Zk, make_float2(-w.x, w.y));
+        }
+        if (jb == 0) {  // k = L/2 pairs with itself
+          const float2 Zk = z[L / 2];
+          X1[at(L / 2)] = post(Zk, Zk, twp[L / 2]);
         }
       }
     } else {
@@ -1048,8 +1058,8 @@ static bool xbulk_ok(const Geom& g, bool fwd) {
 #ifdef GRACE_NO_XBULK
   return false;
 #endif
-#ifndef GRACE_XBULK_FWD
-  if (fwd) return false;  // K1: the V = 3 kernel measured faster (0.41 vs 0.48 ms on the slab)
+#ifdef GRACE_NO_XBULK_FWD
+  if (fwd) return false;
 #endif
   constexpr int ROWS = XBulk<L>::T::ROWS;
   if (g.nx % 4 != 0) return false;
