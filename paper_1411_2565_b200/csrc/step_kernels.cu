@@ -251,6 +251,12 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, GRACE_YT_MINB)
       if (i < n_out && b < ncol_valid) p[b + i * pitch] = v;
     }
   };
+  struct StFull {  // every column valid and every produced row kept: no per-element guard
+    __device__ static constexpr bool kSmem() { return false; }
+    float2* p;
+    int pitch;
+    __device__ void operator()(int b, int, int ib, int C, float2 v) const { p[b + (ib + C) * pitch] = v; }
+  };
   for (int k = 0; t < ntiles; ++k, t += gridDim.x) {
     float2* cur = reinterpret_cast<float2*>(smraw + (k & 1) * Y::TB);
     if (threadIdx.x == 0 && t + (int)gridDim.x < ntiles) {
@@ -260,9 +266,14 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, GRACE_YT_MINB)
     mbar_wait(bar + (k & 1), (k >> 1) & 1);
     const int slab = t / ntx, xt = t - slab * ntx;
     const int kx0 = xt * NCOL;
-    const St st{out + (INV ? xrow_slab(g, slab) : (size_t)slab * g.Py * g.pitch2) + kx0, INV ? g.pitch1 : g.pitch2,
-                n_out, g.Kc - kx0};
-    fft_tile<L, NCOL, NT, true, INV, !INV, INV, 1, false, true>(cur, SmemLd<L, NCOL, true>{cur}, st, tws, 1);
+    float2* o = out + (INV ? xrow_slab(g, slab) : (size_t)slab * g.Py * g.pitch2) + kx0;
+    const int pitch = INV ? g.pitch1 : g.pitch2;
+    if (g.Kc - kx0 >= NCOL && n_out >= (INV ? L / 2 : L))
+      fft_tile<L, NCOL, NT, true, INV, !INV, INV, 1, false, true>(cur, SmemLd<L, NCOL, true>{cur}, StFull{o, pitch},
+                                                                   tws, 1);
+    else
+      fft_tile<L, NCOL, NT, true, INV, !INV, INV, 1, false, true>(cur, SmemLd<L, NCOL, true>{cur},
+                                                                   St{o, pitch, n_out, g.Kc - kx0}, tws, 1);
     __syncthreads();
   }
 }
@@ -737,6 +748,30 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
                : "memory");
 }
 
+// K1 loader: packed pairs z[i] = (x[2i], x[2i+1]) of raw row b (nh = nx/2 of them).
+template <int ROWS, bool GUARD>
+struct XbLd {
+  __device__ static constexpr bool kSmem() { return true; }
+  const float2* s;
+  int nh;
+  __device__ float2 operator()(int b, int, int ib, int C) const {
+    const int i = ib + C;
+    if (GUARD && i >= nh) return make_float2(0.f, 0.f);
+    return s[b * ROWS + i];
+  }
+};
+// K5 store: output pair n -> H_demag x = 2n, 2n+1 of row b (nv valid rows).
+template <bool GUARD>
+struct XbSt {
+  __device__ static constexpr bool kSmem() { return false; }
+  float* H;
+  int nx, nv;
+  __device__ void operator()(int b, int, int ib, int C, float2 v) const {
+    const int x0 = 2 * (ib + C);
+    if (!GUARD || (b < nv && x0 < nx)) *reinterpret_cast<float2*>(H + (size_t)b * nx + x0) = v;
+  }
+};
+
 template <int L>
 struct XBulk {
   static constexpr int RB = 8192 / L;  // rows per tile: 512 threads at 16 elements each
@@ -807,16 +842,12 @@ __global__ void __launch_bounds__(XBulk<L>::NT, 1)
     const int r0 = t * RB;
     const int nv = total - r0 < RB ? total - r0 : RB;
     if constexpr (FWD) {
-      struct Ld {
-        __device__ static constexpr bool kSmem() { return true; }
-        const float2* s;
-        int nh;  // nx / 2 complex inputs per row
-        __device__ float2 operator()(int b, int, int ib, int C) const {
-          const int i = ib + C;
-          return i < nh ? s[b * T::ROWS + i] : make_float2(0.f, 0.f);
-        }
-      } ld{cur, g.nx >> 1};
-      fft_tile<L, RB, NT, false, false, true, false, 1, false, true>(cur, ld, SmemSt<L, RB, false>{cur}, tws, 1);
+      if (g.nx == L)  // the pruned first pass reads exactly the nx/2 packed inputs
+        fft_tile<L, RB, NT, false, false, true, false, 1, false, true>(cur, XbLd<T::ROWS, false>{cur, g.nx >> 1},
+                                                                       SmemSt<L, RB, false>{cur}, tws, 1);
+      else
+        fft_tile<L, RB, NT, false, false, true, false, 1, false, true>(cur, XbLd<T::ROWS, true>{cur, g.nx >> 1},
+                                                                       SmemSt<L, RB, false>{cur}, tws, 1);
       __syncthreads();
       // X[k] and X[L-k] from the same pair Z[k], Z[L-k] (w^(L-k) = -conj w^k);
       // a thread keeps the row the FFT mapped to it.
@@ -870,16 +901,11 @@ __global__ void __launch_bounds__(XBulk<L>::NT, 1)
           return make_float2(S.x - wD.y, S.y + wD.x);  // S + i w^-k D
         }
       } ld{cur, tw, twpx};
-      struct St {
-        __device__ static constexpr bool kSmem() { return false; }
-        float* H;
-        int nx, nv;
-        __device__ void operator()(int b, int, int ib, int C, float2 v) const {
-          const int x0 = 2 * (ib + C);
-          if (b < nv && x0 < nx) *reinterpret_cast<float2*>(H + (size_t)b * nx + x0) = v;
-        }
-      } st{static_cast<float*>(out) + (size_t)r0 * g.nx, g.nx, nv};
-      fft_tile<L, RB, NT, false, true, false, true, 1, false, true>(cur, ld, st, tws, 1);
+      float* H = static_cast<float*>(out) + (size_t)r0 * g.nx;
+      if (nv == RB && g.nx == L)  // the pruned last pass produces exactly the nx outputs
+        fft_tile<L, RB, NT, false, true, false, true, 1, false, true>(cur, ld, XbSt<false>{H, g.nx, nv}, tws, 1);
+      else
+        fft_tile<L, RB, NT, false, true, false, true, 1, false, true>(cur, ld, XbSt<true>{H, g.nx, nv}, tws, 1);
     }
     __syncthreads();
   }

@@ -15,7 +15,9 @@ def main(rep, kre, top=25):
                          capture_output=True, text=True).stdout
     lines = out.splitlines()
     name = lines[0]
-    rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
+    # the page repeats a "Kernel Name" block per matching launch: keep the first
+    nxt = next((i for i in range(1, len(lines)) if lines[i].startswith('"Kernel Name"')), len(lines))
+    rows = list(csv.reader(io.StringIO("\n".join(lines[1:nxt]))))
     hdr = rows[0]
     ix = {h: i for i, h in enumerate(hdr)}
     ops = Counter()
