@@ -26,6 +26,9 @@ UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "
 
 
 def label(name):
+    m = re.search(r"k_x_bulk<(?:\(int\))?\d+, (?:\(bool\))?(\w+)", name)
+    if m:  # persistent bulk-copy x kernels: FWD = K1, else K5
+        return "K1" if m.group(1) in ("1", "true") else "K5"
     if "k1_fwd_x" in name:
         return "K1"
     if "k_y" in name:
