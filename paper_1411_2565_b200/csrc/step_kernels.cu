@@ -949,8 +949,11 @@ __global__ void __launch_bounds__(XBulk<L>::NT, 1)
 // A streaming stencil: each thread owns 4 consecutive cells of a row (16-byte
 // loads), components are processed one after another to keep registers low.
 // mode 0: M -> Mn; mode 1: store H_eff into Hout.
+#ifndef GRACE_K6_MINB
+#define GRACE_K6_MINB 4
+#endif
 template <bool VEC, bool DIST>
-__global__ void __launch_bounds__(256, 3) k6_llg(const float* __restrict__ Hd, const float* __restrict__ M,
+__global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __restrict__ Hd, const float* __restrict__ M,
                                               float* __restrict__ Mn, float* __restrict__ Hout, Geom g,
                                               const StepParams* __restrict__ prm, unsigned long long* __restrict__ flag,
                                               int mode, const float* __restrict__ Hlo, const float* __restrict__ Hhi) {
