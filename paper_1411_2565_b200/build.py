@@ -17,7 +17,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path
 COMMON += os.environ.get("GRACE_NVCC_FLAGS", "").split()  # tuning experiments only
 UNITS = {
     "grace_api.cu": [],
-    "step_kernels.cu": ["-Xptxas", "-v"] if os.environ.get("GRACE_PTXAS_V") else [],
+    "step_kernels.cu": ["--split-compile=0"] + (["-Xptxas", "-v"] if os.environ.get("GRACE_PTXAS_V") else []),
     "tensor_setup.cu": ["-fmad=false"],
 }
 HEADERS = ["fft_engine.cuh", "internal.h"]

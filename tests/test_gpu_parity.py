@@ -170,6 +170,7 @@ STEP_CASES = [
     ((100, 25, 1), (5e-9, 5e-9, 3e-9), 8e5, 1.3e-11, 0.0, 0.02, 2.5e-14, (-19576.058, 3421.831, 0)),
     ((33, 17, 5), (1e-9, 1.5e-9, 2e-9), 1e6, 1e-11, 6.2832e4, 0.5, 1e-15, (0, 0, 0)),
     ((64, 64, 8), (5e-9, 5e-9, 3e-9), 8e5, 1.3e-11, 0.0, 0.5, 1e-14, (0, 0, 0)),
+    ((37, 50, 1), (2e-9, 2e-9, 3e-9), 8e5, 1.3e-11, 5e4, 0.1, 1e-14, (1e4, -2e4, 3e3)),  # nz = 1, odd nx
 ]
 
 
