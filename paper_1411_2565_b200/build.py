@@ -17,7 +17,9 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path
 COMMON += os.environ.get("GRACE_NVCC_FLAGS", "").split()  # tuning experiments only
 UNITS = {
     "grace_api.cu": [],
-    "step_kernels.cu": ["--split-compile=0"] + (["-Xptxas", "-v"] if os.environ.get("GRACE_PTXAS_V") else []),
+    # --split-compile halves the build time but measured slower code (K3 1.08 -> 1.21 ms): dev only
+    "step_kernels.cu": (["--split-compile=0"] if os.environ.get("GRACE_SPLIT_COMPILE") else [])
+    + (["-Xptxas", "-v"] if os.environ.get("GRACE_PTXAS_V") else []),
     "tensor_setup.cu": ["-fmad=false"],
 }
 HEADERS = ["fft_engine.cuh", "internal.h"]
