@@ -340,14 +340,34 @@ __device__ __forceinline__ void stage_ks(float* kss, const float* __restrict__ b
 // FUSE (L <= 64): the forward last pass, the multiply and the inverse first pass
 // (reversed radix plan) run in registers without a shared-memory round trip.
 #ifndef GRACE_ZB
-#define GRACE_ZB 16  // kx columns per K3 / K2' CTA (at most)
+#define GRACE_ZB 16  // kx columns per K3 / K2' CTA (at most, except short pencils)
+#endif
+#ifndef GRACE_Z_MINNT
+#define GRACE_Z_MINNT 128
+#endif
+#ifndef GRACE_ZB_128
+#define GRACE_ZB_128 8
+#endif
+#ifndef GRACE_ZB_256
+#define GRACE_ZB_256 4
+#endif
+#ifndef GRACE_ZB_512
+#define GRACE_ZB_512 8
 #endif
 template <int L>
 struct ZPlan {
   static constexpr bool FUSE = L >= 2 && L <= 64;
   static constexpr int RLAST = L <= 1 ? 1 : 1 << fft_pass_bits(L, fft_npass(L) - 1);
-  static constexpr int B = L <= 1 ? GRACE_ZB : (2048 / L > GRACE_ZB ? GRACE_ZB : (2048 / L < 1 ? 1 : 2048 / L));
   static constexpr int TPC = L <= 1 ? 1 : (FUSE ? L / RLAST : (L / 8 > 0 ? L / 8 : 1));
+  // fused (short) pencils: at least GRACE_Z_MINNT threads per CTA; unfused:
+  // GRACE_Z_ELEMS values per component per CTA (smem: 3 components resident)
+  static constexpr int BF = (GRACE_Z_MINNT / TPC > GRACE_ZB ? GRACE_Z_MINNT / TPC : GRACE_ZB);
+  // unfused columns per CTA by length, measured on the Table-1 cubes (K3 ms,
+  // B = 2 / 4 / 8 / 16): L = 128 (64^3) 8 best (0.025 vs 0.040 at 16);
+  // L = 256 (128^3) 4 (0.32 vs 0.43 at 8); L = 512 (256^3) 8 (1.45 vs 1.50 at 4,
+  // 2.17 at 2); L = 1024 (512^3) 4 (20.7 vs 26.9 at 2)
+  static constexpr int BN = L <= 128 ? GRACE_ZB_128 : (L == 256 ? GRACE_ZB_256 : (L == 512 ? GRACE_ZB_512 : (L == 1024 ? 4 : (2048 / L > 1 ? 2048 / L : 1))));
+  static constexpr int B = L <= 1 ? GRACE_ZB : (FUSE ? (BF < 2048 / L ? BF : 2048 / L) : BN);
   static constexpr int NT = B * TPC < 32 ? 32 : B * TPC;
 };
 
