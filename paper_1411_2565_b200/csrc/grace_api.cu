@@ -151,6 +151,8 @@ struct grace_ctx {
   float2* tw = nullptr;
   size_t bytes = 0;
   cudaStream_t own = nullptr, stream = nullptr, cap = nullptr;
+  cudaStream_t hs = nullptr;                  // distributed: halo exchange (C3) side stream
+  cudaEvent_t evM = nullptr, evH = nullptr;   // fork (M[c] ready) / join (halos landed)
   cudaGraphExec_t g1[2] = {nullptr, nullptr}, gc[2] = {nullptr, nullptr};
   ncclComm_t comm = nullptr;
   bool profiling = false;
@@ -235,6 +237,16 @@ struct grace_ctx {
     return bad ? cudaErrorUnknown : cudaSuccess;
   }
 
+  // C3 on the side stream: it needs only M[c], so it runs under K1..K4 and the
+  // transposes; the stencil kernel joins it (halo_join) before reading Hlo/Hhi.
+  cudaError_t halo_start(int c, cudaStream_t s) {
+    CE(cudaEventRecord(evM, s));
+    CE(cudaStreamWaitEvent(hs, evM, 0));
+    CE(halo(c, hs));
+    return cudaEventRecord(evH, hs);
+  }
+  cudaError_t halo_join(cudaStream_t s) { return mode == kSingle ? cudaSuccess : cudaStreamWaitEvent(s, evH, 0); }
+
   // H~ for every rank: K1 .. K4 plus the transposes.  M[c] is the input.
   cudaError_t demag_stages(int c, cudaStream_t s, bool bump, cudaEvent_t* ev = nullptr) {
     auto rec = [&](int idx) {
@@ -262,6 +274,7 @@ struct grace_ctx {
       }
       return cudaSuccess;
     }
+    CE(halo_start(c, s));  // C3: one M plane to each neighbour, overlapped
     for (auto& rk : ranks) CE(launch_k1(rk.g, rk.M[c], rk.A, tw, bump ? rk.prm : nullptr, s));
     CE(alltoall(&Rank::A, &Rank::B, s));  // C1: z slabs -> kx blocks
     for (auto& rk : ranks) {
@@ -272,7 +285,6 @@ struct grace_ctx {
       }
     }
     CE(alltoall(&Rank::B, &Rank::A, s));  // C2: kx blocks -> z slabs
-    CE(halo(c, s));                       // C3: one M plane to each neighbour
     return cudaSuccess;
   }
 
@@ -282,6 +294,7 @@ struct grace_ctx {
     const int nk = kernel_count(g0);
     const int k5 = 2 * (nk - (g0.split_llg ? 2 : 1));
     if (ev) cudaEventRecord(ev[k5], s);
+    CE(halo_join(s));
     for (auto& rk : ranks) {
       if (g0.split_llg)
         CE(launch_k5(rk.g, 2, rk.A, rk.M[c], nullptr, rk.Hd, tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
@@ -330,6 +343,9 @@ struct grace_ctx {
     if (comm) g_nccl.commDestroy(comm);
     if (own) cudaStreamDestroy(own);
     if (cap) cudaStreamDestroy(cap);
+    if (hs) cudaStreamDestroy(hs);
+    if (evM) cudaEventDestroy(evM);
+    if (evH) cudaEventDestroy(evH);
   }
 };
 
@@ -443,6 +459,9 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
   {
     cudaError_t e = cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking);
+    if (e == cudaSuccess && mode != grace_ctx::kSingle) e = cudaStreamCreateWithFlags(&h->hs, cudaStreamNonBlocking);
+    if (e == cudaSuccess && mode != grace_ctx::kSingle) e = cudaEventCreateWithFlags(&h->evM, cudaEventDisableTiming);
+    if (e == cudaSuccess && mode != grace_ctx::kSingle) e = cudaEventCreateWithFlags(&h->evH, cudaEventDisableTiming);
     if (e != cudaSuccess) return bail(fail(GRACE_ECUDA, "stream creation: %s", cudaGetErrorString(e)));
   }
   h->stream = h->own;
@@ -705,6 +724,7 @@ int grace_heff(grace_ctx* h, double* out) {
     }
   CUDA_OR(h->upload_params(1e-15));
   CUDA_OR(h->demag_stages(h->cur, s, false));
+  CUDA_OR(h->halo_join(s));
   for (auto& rk : h->ranks) {
     if (rk.g.split_llg) {
       CUDA_OR(launch_k5(rk.g, 2, rk.A, rk.M[h->cur], nullptr, rk.Hd, h->tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));

@@ -95,6 +95,9 @@ HEFF_CASES = [
     ((6, 5, 40), (1e-9, 1e-9, 1e-9), 1e6, 1e-11, 0.0, (0, 0, 0)),      # Pz = 128: unfused K3
     ((20, 300, 1), (2e-9, 1e-9, 1e-9), 8e5, 1.3e-11, 0.0, (0, 0, 0)),  # nz = 1, Py = 1024: K2/multiply/K4
     ((9, 31, 3), (1e-9, 1e-9, 1e-9), 8e5, 1.3e-11, 1e4, (0, 0, 0)),    # odd nx: scalar load/store paths
+    ((4, 3, 100), (1e-9, 1e-9, 1e-9), 1e6, 1e-11, 0.0, (0, 0, 0)),     # Pz = 256: K3 4-column tiles
+    ((3, 2, 200), (1e-9, 1e-9, 1e-9), 1e6, 1e-11, 0.0, (0, 0, 0)),     # Pz = 512: 8-column tiles
+    ((2, 2, 300), (1e-9, 1e-9, 1e-9), 1e6, 1e-11, 0.0, (0, 0, 0)),     # Pz = 1024
 ]
 
 
