@@ -104,6 +104,24 @@ int grace_get_m_device(grace_ctx *h, float *d_m_out);
 /* <M>/Ms (3 doubles) by a fixed-order two-stage reduction (deterministic). */
 int grace_mavg(grace_ctx *h, double *out3);
 
+/* Diagnostics; both evaluate H_demag of the current M with the
+ * step's own kernels, then reduce in fp64 in a fixed order.
+ * grace_energy: the discrete Eq. (1) energy, joules,
+ *   out5 = {total, exchange, anisotropy, demag, Zeeman}: exchange
+ *   V A sum over +x/+y/+z bonds |m_nb - m|^2 / Delta^2, anisotropy V Ku sum (1 - m_x^2),
+ *   demag -mu0/2 V sum H_demag.M, Zeeman -mu0 V sum H_ext.M (m = M/Ms).
+ * grace_max_torque: max over cells |M x H_eff| / (Ms |H_eff| + 1e-30), the SPEC
+ *   relaxation criterion (eps S:L331), H_eff as the step forms it. */
+int grace_energy(grace_ctx *h, double *out5);
+int grace_max_torque(grace_ctx *h, double *out);
+
+/* SPEC relax: Euler steps of dt at damping alpha_relax until the max
+ * torque is below tol (checked every check_every steps) or max_steps are taken;
+ * alpha is restored afterwards.  steps_taken / torque receive the outcome
+ * (torque < tol: converged).  Errors as grace_step. */
+int grace_relax(grace_ctx *h, double alpha_relax, double dt, long long max_steps, double tol, int check_every,
+                long long *steps_taken, double *torque);
+
 /* Steps taken so far (t = steps * dt). */
 int grace_step_count(grace_ctx *h, long long *steps);
 

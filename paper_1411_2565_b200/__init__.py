@@ -47,6 +47,9 @@ SIGNATURES = [
     ("grace_get_m_device", _I, [_P, _P]),
     ("grace_mavg", _I, [_P, _PD]),
     ("grace_step_count", _I, [_P, _PLL]),
+    ("grace_energy", _I, [_P, _PD]),
+    ("grace_max_torque", _I, [_P, _PD]),
+    ("grace_relax", _I, [_P, _D, _D, ctypes.c_longlong, _D, _I, _PLL, _PD]),
     ("grace_last_nonfinite", _I, [_P, _PLL, _PLL]),
     ("grace_geometry", _I, [_P, _PLL]),
     ("grace_device_bytes", _I, [_P, ctypes.POINTER(ctypes.c_size_t)]),
@@ -188,6 +191,26 @@ def grace_mavg(h):
     return out
 
 
+def grace_energy(h):
+    """(total, exchange, anisotropy, demag, zeeman) in joules."""
+    out = (ctypes.c_double * 5)()
+    _check(load().grace_energy(h, out))
+    return tuple(out)
+
+
+def grace_max_torque(h):
+    v = ctypes.c_double()
+    _check(load().grace_max_torque(h, ctypes.byref(v)))
+    return v.value
+
+
+def grace_relax(h, alpha_relax, dt, max_steps, tol, check_every):
+    n, t = ctypes.c_longlong(), ctypes.c_double()
+    _check(load().grace_relax(h, float(alpha_relax), float(dt), int(max_steps), float(tol), int(check_every),
+                              ctypes.byref(n), ctypes.byref(t)))
+    return n.value, t.value
+
+
 def grace_step_count(h):
     v = ctypes.c_longlong()
     _check(load().grace_step_count(h, ctypes.byref(v)))
@@ -304,3 +327,14 @@ class Grace:
     @property
     def geometry(self):
         return grace_geometry(self.h)
+
+    def energy(self):
+        """Eq. (1) energy terms in joules: dict total/exchange/anisotropy/demag/zeeman."""
+        return dict(zip(("total", "exchange", "anisotropy", "demag", "zeeman"), grace_energy(self.h)))
+
+    def max_torque(self):
+        return grace_max_torque(self.h)
+
+    def relax(self, alpha_relax=1.0, dt=1e-13, max_steps=1_000_000, tol=1e-4, check_every=100):
+        """SPEC relax: returns (steps taken, final max torque)."""
+        return grace_relax(self.h, alpha_relax, dt, max_steps, tol, check_every)

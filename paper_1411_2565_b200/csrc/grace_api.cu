@@ -71,7 +71,7 @@ typedef int ncclResult_t;
 struct ncclUniqueId {
   char internal[128];
 };
-enum { kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0 };
+enum { kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0, kNcclMax = 2 };
 struct Nccl {
   void* h = nullptr;
   ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
@@ -129,6 +129,7 @@ struct Rank {
   StepParams* prm = nullptr;
   unsigned long long* flag = nullptr;  // [0] step non-finite, [1] set_m zero cell
   double* red = nullptr;               // mavg partials + 3 outputs
+  double* dred = nullptr;              // diagnostics partials + 5 outputs (allocated on first use)
   float* Hbuf = nullptr;
   float* Hd = nullptr;                 // H_demag [3][nzl][ny][nx] (split K5/K6 step)
   bool tma = false;                    // TMA descriptors of the K2 / K4 inputs built
@@ -335,7 +336,7 @@ struct grace_ctx {
     for (auto e : ev) cudaEventDestroy(e);
     for (auto& rk : ranks) {
       void* ptrs[] = {rk.M[0], rk.M[1], rk.A,   rk.B,    rk.X2,  rk.KS,   rk.Hlo,
-                      rk.Hhi,  rk.prm,  rk.flag, rk.red, rk.Hbuf, rk.Hd};
+                      rk.Hhi,  rk.prm,  rk.flag, rk.red, rk.Hbuf, rk.Hd,  rk.dred};
       for (void* p : ptrs)
         if (p) cudaFree(p);
     }
@@ -830,6 +831,90 @@ int grace_mavg(grace_ctx* h, double* out3) {
   }
   for (int q = 0; q < 3; ++q) out3[q] = acc[q] / h->P;  // equal slabs: mean of the slab means
   return GRACE_OK;
+}
+
+// Energy sums and max torque over the whole grid (all ranks): S[0..3] sums, S[4] max.
+static int diagnostics(grace_ctx* h, double S[5]) {
+  cudaStream_t s = h->stream;
+  for (auto& rk : h->ranks) {
+    if (!rk.Hd) {
+      int rc = h->alloc((void**)&rk.Hd, sizeof(float) * 3 * (size_t)rk.Nl);
+      if (rc) return rc;
+    }
+    if (!rk.dred) {
+      int rc = h->alloc((void**)&rk.dred, sizeof(double) * (kDiagPartials + 8));
+      if (rc) return rc;
+    }
+  }
+  CUDA_OR(h->upload_params(1e-15));
+  CUDA_OR(h->demag_stages(h->cur, s, false));
+  CUDA_OR(h->halo_join(s));
+  for (auto& rk : h->ranks)
+    CUDA_OR(launch_k5(rk.g, 2, rk.A, rk.M[h->cur], nullptr, rk.Hd, h->tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+  for (int q = 0; q < 4; ++q) S[q] = 0.0;
+  S[4] = 0.0;
+  for (auto& rk : h->ranks) {
+    double* out = rk.dred + kDiagPartials;
+    CUDA_OR(launch_diag(rk.g, rk.M[h->cur], rk.Hd, rk.prm, rk.Hlo, rk.Hhi, h->dx, h->dy, h->dz, rk.dred, out, s));
+    if (h->mode == grace_ctx::kNccl) {
+      ncclResult_t r = g_nccl.allReduce(out, out, 4, kNcclFloat64, kNcclSum, h->comm, s);
+      if (r == 0) r = g_nccl.allReduce(out + 4, out + 4, 1, kNcclFloat64, kNcclMax, h->comm, s);
+      if (r != 0) return fail(GRACE_ECUDA, "ncclAllReduce: %s", g_nccl.errStr(r));
+    }
+    double v[5];
+    CUDA_OR(cudaMemcpyAsync(v, out, sizeof v, cudaMemcpyDeviceToHost, s));
+    CUDA_OR(cudaStreamSynchronize(s));
+    for (int q = 0; q < 4; ++q) S[q] += v[q];
+    S[4] = std::max(S[4], v[4]);
+  }
+  return GRACE_OK;
+}
+
+int grace_energy(grace_ctx* h, double* out5) {
+  if (!h || !out5) return fail(GRACE_EINVAL, "NULL argument");
+  double S[5];
+  int rc = diagnostics(h, S);
+  if (rc) return rc;
+  const double V = (h->dx * h->dy) * h->dz, Ms2 = h->Ms * h->Ms, mu0 = 4e-7 * 3.14159265358979323846;
+  out5[1] = V * h->A * S[0] / Ms2;      // exchange
+  out5[2] = V * h->Ku * S[1] / Ms2;     // anisotropy Ku (1 - m_x^2)
+  out5[3] = -0.5 * mu0 * V * S[2];      // demag
+  out5[4] = -mu0 * V * S[3];            // Zeeman
+  out5[0] = out5[1] + out5[2] + out5[3] + out5[4];
+  return GRACE_OK;
+}
+
+int grace_max_torque(grace_ctx* h, double* out) {
+  if (!h || !out) return fail(GRACE_EINVAL, "NULL argument");
+  double S[5];
+  int rc = diagnostics(h, S);
+  if (rc) return rc;
+  *out = S[4];
+  return GRACE_OK;
+}
+
+int grace_relax(grace_ctx* h, double alpha_relax, double dt, long long max_steps, double tol, int check_every,
+                long long* steps_taken, double* torque) {
+  if (!h || !steps_taken || !torque) return fail(GRACE_EINVAL, "NULL argument");
+  if (!(alpha_relax > 0) || !finite_pos(tol) || max_steps < 0 || check_every < 1)
+    return fail(GRACE_EINVAL, "relax needs alpha_relax > 0, tol > 0, max_steps >= 0, check_every >= 1");
+  const double alpha0 = h->alpha;
+  h->alpha = alpha_relax;
+  long long done = 0;
+  double t = 0.0;
+  int rc = grace_max_torque(h, &t);
+  while (rc == GRACE_OK && t >= tol && done < max_steps) {
+    const int k = (int)std::min<long long>(check_every, max_steps - done);
+    rc = grace_step(h, k, dt);
+    if (rc == GRACE_OK) {
+      done += k;
+      rc = grace_max_torque(h, &t);
+    }
+  }
+  h->alpha = alpha0;
+  *steps_taken = done;
+  *torque = t;
+  return rc;
 }
 
 int grace_step_count(grace_ctx* h, long long* steps) {

@@ -84,6 +84,12 @@ cudaError_t launch_set_m_f32(const float* src, float* M, long long n, float Ms, 
                              cudaStream_t st);
 cudaError_t launch_mavg(const float* M, long long n, double Ms, double* partial, double* out, cudaStream_t st);
 constexpr int kMavgPartials = 3 * 296;
+// Eq. (1) energy sums and the relax torque of the current state (out[5], see step_kernels.cu);
+// partial holds kDiagPartials doubles.
+cudaError_t launch_diag(const Geom& g, const float* M, const float* Hd, const StepParams* prm, const float* Hlo,
+                        const float* Hhi, double dx, double dy, double dz, double* partial, double* out,
+                        cudaStream_t st);
+constexpr int kDiagPartials = 5 * 296;
 cudaError_t launch_fill_uniform_x(float* M, long long n, float Ms, cudaStream_t st);
 cudaError_t launch_widen(const float* src, double* dst, long long n, cudaStream_t st);
 

@@ -1539,6 +1539,98 @@ cudaError_t launch_mavg(const float* M, long long n, double Ms, double* partial,
   return cudaGetLastError();
 }
 
+// Diagnostics: the discrete Eq. (1) energy terms
+// (per bond to the +x/+y/+z neighbour, per cell otherwise) and the
+// SPEC relax torque max_c |M x H_eff| / (Ms |H_eff| + eps),
+// per cell in fp64, fixed-order two-stage reduction.  Sums out[0..3] =
+// sum |M_nb - M|^2 / Delta^2, sum (Ms^2 - Mx^2), sum H_d.M, sum H_ext.M (the host
+// applies V, A/Ms^2, Ku/Ms^2, -mu0/2, -mu0); out[4] = max torque.
+template <bool DIST>
+__global__ void k_diag_partial(const float* __restrict__ M, const float* __restrict__ Hd, Geom g,
+                               const StepParams* __restrict__ prm, const float* __restrict__ Hlo,
+                               const float* __restrict__ Hhi, double idx2, double idy2, double idz2,
+                               double* __restrict__ partial) {
+  __shared__ double sh[5][kRedThreads];
+  const long long n = (long long)g.nzl * g.ny * g.nx;
+  const long long plane = (long long)g.ny * g.nx;
+  const long long chunk = (n + gridDim.x - 1) / gridDim.x;
+  const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+  const StepParams p = *prm;
+  double acc[4] = {0, 0, 0, 0}, tmax = 0;
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const long long row = i / g.nx;
+    const int x = (int)(i - row * g.nx);
+    const int zl = (int)(row / g.ny), y = (int)(row - (long long)zl * g.ny);
+    const long long ip = i - (long long)zl * plane;  // in-plane index (halo buffers)
+    float a[3], nb[6][3];
+    for (int c = 0; c < 3; ++c) a[c] = M[c * n + i];
+    for (int c = 0; c < 3; ++c) {
+      nb[0][c] = x > 0 ? M[c * n + i - 1] : a[c];
+      nb[1][c] = x + 1 < g.nx ? M[c * n + i + 1] : a[c];
+      nb[2][c] = y > 0 ? M[c * n + i - g.nx] : a[c];
+      nb[3][c] = y + 1 < g.ny ? M[c * n + i + g.nx] : a[c];
+      nb[4][c] = zl > 0 ? M[c * n + i - plane] : ((DIST && g.has_lo) ? Hlo[c * plane + ip] : a[c]);
+      nb[5][c] = zl + 1 < g.nzl ? M[c * n + i + plane] : ((DIST && g.has_hi) ? Hhi[c * plane + ip] : a[c]);
+    }
+    // bonds to the +x, +y, +z neighbours (a missing neighbour adds nothing)
+    const double w[3] = {idx2, idy2, idz2};
+    for (int ax = 0; ax < 3; ++ax)
+      for (int c = 0; c < 3; ++c) {
+        const double d = (double)nb[2 * ax + 1][c] - (double)a[c];
+        acc[0] += w[ax] * d * d;
+      }
+    acc[1] += (double)g.Ms * g.Ms - (double)a[0] * a[0];
+    float h[3];
+    for (int c = 0; c < 3; ++c) {
+      acc[2] += (double)Hd[c * n + i] * a[c];
+      acc[3] += (double)p.hext[c] * a[c];
+      // H_eff as the step kernels form it (Eq. (2), six-neighbour difference form)
+      float e = 0.f;
+      e += g.cx * (nb[0][c] - a[c]);
+      e += g.cx * (nb[1][c] - a[c]);
+      e += g.cy * (nb[2][c] - a[c]);
+      e += g.cy * (nb[3][c] - a[c]);
+      e += g.cz * (nb[4][c] - a[c]);
+      e += g.cz * (nb[5][c] - a[c]);
+      h[c] = Hd[c * n + i] + p.hext[c] + (c == 0 ? g.ck * a[0] : 0.f) + e;
+    }
+    const double tx = (double)a[1] * h[2] - (double)a[2] * h[1];
+    const double ty = (double)a[2] * h[0] - (double)a[0] * h[2];
+    const double tz = (double)a[0] * h[1] - (double)a[1] * h[0];
+    const double hn = sqrt((double)h[0] * h[0] + (double)h[1] * h[1] + (double)h[2] * h[2]);
+    const double t = sqrt(tx * tx + ty * ty + tz * tz) / ((double)g.Ms * hn + 1e-30);
+    tmax = t > tmax ? t : tmax;
+  }
+  for (int q = 0; q < 4; ++q) sh[q][threadIdx.x] = acc[q];
+  sh[4][threadIdx.x] = tmax;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+      for (int q = 0; q < 4; ++q) sh[q][threadIdx.x] += sh[q][threadIdx.x + st];
+      sh[4][threadIdx.x] = fmax(sh[4][threadIdx.x], sh[4][threadIdx.x + st]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < 5) partial[threadIdx.x * gridDim.x + blockIdx.x] = sh[threadIdx.x][0];
+}
+__global__ void k_diag_final(const double* __restrict__ partial, int nb, double* out) {
+  if (threadIdx.x < 5) {
+    double s = 0;
+    for (int i = 0; i < nb; ++i)
+      s = threadIdx.x < 4 ? s + partial[threadIdx.x * nb + i] : fmax(s, partial[threadIdx.x * nb + i]);
+    out[threadIdx.x] = s;
+  }
+}
+cudaError_t launch_diag(const Geom& g, const float* M, const float* Hd, const StepParams* prm, const float* Hlo,
+                        const float* Hhi, double dx, double dy, double dz, double* partial, double* out,
+                        cudaStream_t st) {
+  const double ix = 1.0 / (dx * dx), iy = 1.0 / (dy * dy), iz = 1.0 / (dz * dz);
+  if (g.kb) k_diag_partial<true><<<kRedBlocks, kRedThreads, 0, st>>>(M, Hd, g, prm, Hlo, Hhi, ix, iy, iz, partial);
+  else k_diag_partial<false><<<kRedBlocks, kRedThreads, 0, st>>>(M, Hd, g, prm, Hlo, Hhi, ix, iy, iz, partial);
+  k_diag_final<<<1, 32, 0, st>>>(partial, kRedBlocks, out);
+  return cudaGetLastError();
+}
+
 __global__ void k_fill_uniform_x(float* M, long long n, float Ms) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     M[i] = Ms;
