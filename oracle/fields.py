@@ -53,3 +53,16 @@ def zeeman(M, hext):
 def heff(M, demag_op, A, Ms, Ku, d, hext):
     """Eq. (2): H_eff = H_exch + H_anis + H_demag + H_extern."""
     return exchange(M, A, Ms, d) + anisotropy(M, Ku, Ms) + demag_op(M) + zeeman(M, hext)
+
+
+def schedule_amplitude(k, start, decay, stop):
+    """SPEC FieldSchedule (paper §5 input "Hx Hy Hz startTime decayTime
+    stopTime"): amplitude at timestep index k -- 0 before start, 1 in [start, decay),
+    a linear ramp from 1 to 0 across [decay, stop), 0 at and after stop."""
+    if not (0 <= start <= decay <= stop):
+        raise ValueError("schedule needs 0 <= start <= decay <= stop")
+    if k < start or k >= stop:
+        return 0.0
+    if k < decay:
+        return 1.0
+    return 1.0 - (k - decay) / (stop - decay)

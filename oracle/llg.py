@@ -16,6 +16,7 @@ A non-finite result aborts with the step index and cell.
 import numpy as np
 
 from .fields import heff as _heff
+from .fields import schedule_amplitude
 
 
 class NonFinite(RuntimeError):
@@ -42,18 +43,29 @@ def renormalize(M, Ms):
 class Sim:
     """State + parameters of one fp64 run (the oracle twin of a grace context)."""
 
-    def __init__(self, M, demag_op, Ms, A, Ku, alpha, gamma0, d, hext=(0.0, 0.0, 0.0)):
+    def __init__(self, M, demag_op, Ms, A, Ku, alpha, gamma0, d, hext=(0.0, 0.0, 0.0), schedule=None):
         self.M = np.array(M, dtype=np.float64)
         self.demag = demag_op
         self.Ms, self.A, self.Ku = Ms, A, Ku
         self.alpha, self.gamma0 = alpha, gamma0
         self.d = tuple(d)
         self.hext = tuple(hext)
+        # optional SPEC FieldSchedule (S:L182-187): (H0, start, decay, stop); the
+        # applied field at step k is hext + amplitude(k) H0
+        self.schedule = schedule
         self.step_count = 0
+
+    def field(self, k=None):
+        k = self.step_count if k is None else k
+        if self.schedule is None:
+            return self.hext
+        H0, start, decay, stop = self.schedule
+        a = schedule_amplitude(k, start, decay, stop)
+        return tuple(self.hext[q] + a * H0[q] for q in range(3))
 
     def heff(self, M=None):
         M = self.M if M is None else M
-        return _heff(M, self.demag, self.A, self.Ms, self.Ku, self.d, self.hext)
+        return _heff(M, self.demag, self.A, self.Ms, self.Ku, self.d, self.field())
 
     def euler_step(self, dt):
         H = self.heff()

@@ -20,6 +20,7 @@ from oracle.energy import energy
 from oracle.fields import anisotropy, exchange, heff
 from oracle.llg import NonFinite, Sim, llg_rhs
 from oracle.tensor import tensor_octant
+from workloads import GAMMA0, random_m
 
 RNG = np.random.default_rng(7)
 MS, A = 8e5, 1.3e-11
@@ -188,3 +189,36 @@ def test_nonfinite_abort_reports_step_and_cell():
     with pytest.raises(NonFinite) as e:
         sim.euler_step(1e-13)
     assert e.value.step == 0 and e.value.cell == 0
+
+
+# ---------------------------------------------------------------- field schedule
+
+def test_schedule_amplitude_piecewise_definition():
+    """0 before start, H0 in [start, decay), linear ramp to 0
+    across [decay, stop), 0 at and after stop (values written out by hand)."""
+    from oracle.fields import schedule_amplitude as amp
+    s, d, e = 10, 20, 30
+    assert [amp(k, s, d, e) for k in (0, 9)] == [0.0, 0.0]
+    assert [amp(k, s, d, e) for k in (10, 15, 19)] == [1.0, 1.0, 1.0]
+    assert amp(20, s, d, e) == 1.0 and amp(25, s, d, e) == 0.5 and amp(29, s, d, e) == pytest.approx(0.1)
+    assert [amp(k, s, d, e) for k in (30, 31, 10 ** 9)] == [0.0, 0.0, 0.0]
+    assert amp(5, 5, 5, 5) == 0.0               # empty window: never on
+    assert amp(5, 5, 5, 6) == 1.0               # one-step ramp starts at full amplitude
+    assert amp(7, 5, 9, 9) == 1.0 and amp(9, 5, 9, 9) == 0.0  # no ramp: a step switch-off
+    with pytest.raises(ValueError):
+        amp(0, 3, 2, 4)
+
+
+def test_sim_schedule_enters_zeeman_only():
+    """The scheduled field adds amplitude(k) H0 to H_ext at step k and nothing else:
+    H_eff(step k) - H_eff(no schedule) is that uniform vector."""
+    n, d = (4, 3, 2), (1e-9, 1e-9, 1e-9)
+    M = random_m(n, 8e5, seed=2)
+    op = DemagFFT(tensor_octant(*n, *d))
+    base = Sim(M, op, 8e5, 1.3e-11, 1e4, 0.1, GAMMA0, d, (1e3, 0, 0))
+    sch = Sim(M, op, 8e5, 1.3e-11, 1e4, 0.1, GAMMA0, d, (1e3, 0, 0), schedule=((0, 2e4, -4e4), 1, 2, 6))
+    for k, a in ((0, 0.0), (1, 1.0), (2, 1.0), (4, 0.5), (6, 0.0)):
+        sch.step_count = k
+        diff = sch.heff() - base.heff()
+        for q, h0 in enumerate((0, 2e4, -4e4)):
+            np.testing.assert_allclose(diff[q], a * h0, rtol=0, atol=1e-9 * 4e4)
