@@ -122,6 +122,17 @@ int grace_max_torque(grace_ctx *h, double *out);
 int grace_relax(grace_ctx *h, double alpha_relax, double dt, long long max_steps, double tol, int check_every,
                 long long *steps_taken, double *torque);
 
+/* Time-scheduled applied field, the paper's "Hx Hy Hz startTime decayTime stopTime"
+ * input (paper Sec. 5; SPEC FieldSchedule S:L182-187).  At timestep index k (the
+ * step computing M_{k+1} from M_k; grace_heff / grace_energy evaluate k = steps
+ * taken) the applied field is H_ext + a(k) H0 (A/m, added to grace_set_hext's
+ * constant field): a = 1 on [start, decay), a linear ramp 1 - (k - decay)/(stop - decay)
+ * on [decay, stop), 0 otherwise.  Requires 0 <= start <= decay <= stop (else
+ * GRACE_EINVAL); H0 = 0 or stop == start disables it.  Indices count
+ * grace_step_count, which grace_set_m does not reset. */
+int grace_set_field_schedule(grace_ctx *h, double h0x, double h0y, double h0z, long long start, long long decay,
+                             long long stop);
+
 /* Steps taken so far (t = steps * dt). */
 int grace_step_count(grace_ctx *h, long long *steps);
 

@@ -48,6 +48,7 @@ SIGNATURES = [
     ("grace_mavg", _I, [_P, _PD]),
     ("grace_step_count", _I, [_P, _PLL]),
     ("grace_energy", _I, [_P, _PD]),
+    ("grace_set_field_schedule", _I, [_P, _D, _D, _D, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong]),
     ("grace_max_torque", _I, [_P, _PD]),
     ("grace_relax", _I, [_P, _D, _D, ctypes.c_longlong, _D, _I, _PLL, _PD]),
     ("grace_last_nonfinite", _I, [_P, _PLL, _PLL]),
@@ -191,6 +192,11 @@ def grace_mavg(h):
     return out
 
 
+def grace_set_field_schedule(h, h0, start, decay, stop):
+    _check(load().grace_set_field_schedule(h, float(h0[0]), float(h0[1]), float(h0[2]), int(start), int(decay),
+                                           int(stop)))
+
+
 def grace_energy(h):
     """(total, exchange, anisotropy, demag, zeeman) in joules."""
     out = (ctypes.c_double * 5)()
@@ -327,6 +333,10 @@ class Grace:
     @property
     def geometry(self):
         return grace_geometry(self.h)
+
+    def set_field_schedule(self, h0, start, decay, stop):
+        """Paper/SPEC field schedule: + a(k) h0 (A/m) on top of set_hext's field."""
+        grace_set_field_schedule(self.h, h0, start, decay, stop)
 
     def energy(self):
         """Eq. (1) energy terms in joules: dict total/exchange/anisotropy/demag/zeeman."""

@@ -142,6 +142,9 @@ struct grace_ctx {
   int myrank = 0;  // nccl mode: this process's rank
   double dx, dy, dz, Ms, A, Ku, alpha, gamma0;
   double hext[3] = {0, 0, 0};
+  double h0[3] = {0, 0, 0};       // field schedule (grace_set_field_schedule)
+  long long sched[3] = {0, 0, 0};
+  bool has_sched = false;
   long long steps = 0;
   long long nf_step = -1, nf_cell = -1;
   long long N = 0;  // cells addressed by set_m/get_m/heff (whole grid, or the local slab in nccl mode)
@@ -180,10 +183,18 @@ struct grace_ctx {
     hprm.c_prec = (float)(-gamma0 / a2);
     hprm.c_damp = (float)(-alpha * gamma0 / (a2 * Ms));
     for (int q = 0; q < 3; ++q) hprm.hext[q] = (float)hext[q];
+    for (int q = 0; q < 3; ++q) hprm.h0[q] = (float)h0[q];
+    hprm.sched = has_sched ? 1 : 0;
+    hprm.t0 = sched[0];
+    hprm.t1 = sched[1];
+    hprm.t2 = sched[2];
     hprm.step = steps;
   }
-  cudaError_t upload_params(double dt) {
+  // eval: H_eff of the current state (grace_heff / diagnostics), i.e. at timestep
+  // index `steps` -- the value the step counter has once K1 has advanced it
+  cudaError_t upload_params(double dt, bool eval = false) {
     fill_params(dt);
+    if (eval) hprm.step = steps + 1;
     for (auto& rk : ranks) CE(cudaMemcpyAsync(rk.prm, &hprm, sizeof(StepParams), cudaMemcpyHostToDevice, stream));
     return cudaSuccess;
   }
@@ -708,6 +719,23 @@ int grace_set_hext(grace_ctx* h, double hx, double hy, double hz) {
   return GRACE_OK;
 }
 
+int grace_set_field_schedule(grace_ctx* h, double h0x, double h0y, double h0z, long long start, long long decay,
+                             long long stop) {
+  if (!h) return fail(GRACE_EINVAL, "NULL context");
+  if (!std::isfinite(h0x) || !std::isfinite(h0y) || !std::isfinite(h0z))
+    return fail(GRACE_EINVAL, "scheduled field must be finite");
+  if (!(0 <= start && start <= decay && decay <= stop))
+    return fail(GRACE_EINVAL, "schedule needs 0 <= start <= decay <= stop (got %lld, %lld, %lld)", start, decay, stop);
+  h->h0[0] = h0x;
+  h->h0[1] = h0y;
+  h->h0[2] = h0z;
+  h->sched[0] = start;
+  h->sched[1] = decay;
+  h->sched[2] = stop;
+  h->has_sched = (h0x != 0 || h0y != 0 || h0z != 0) && stop > start;
+  return GRACE_OK;
+}
+
 int grace_set_alpha(grace_ctx* h, double alpha) {
   if (!h) return fail(GRACE_EINVAL, "NULL context");
   if (!std::isfinite(alpha) || alpha < 0) return fail(GRACE_EINVAL, "alpha must be finite and >= 0");
@@ -723,7 +751,7 @@ int grace_heff(grace_ctx* h, double* out) {
       int rc = h->alloc((void**)&rk.Hbuf, sizeof(float) * 3 * (size_t)rk.Nl);
       if (rc) return rc;
     }
-  CUDA_OR(h->upload_params(1e-15));
+  CUDA_OR(h->upload_params(1e-15, true));
   CUDA_OR(h->demag_stages(h->cur, s, false));
   CUDA_OR(h->halo_join(s));
   for (auto& rk : h->ranks) {
@@ -846,7 +874,7 @@ static int diagnostics(grace_ctx* h, double S[5]) {
       if (rc) return rc;
     }
   }
-  CUDA_OR(h->upload_params(1e-15));
+  CUDA_OR(h->upload_params(1e-15, true));
   CUDA_OR(h->demag_stages(h->cur, s, false));
   CUDA_OR(h->halo_join(s));
   for (auto& rk : h->ranks)

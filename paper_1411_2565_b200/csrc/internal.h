@@ -17,7 +17,22 @@ struct StepParams {
   float c_damp;   // -alpha gamma0/((1+alpha^2) Ms)       (Eq. (3) damping prefactor)
   float hext[3];  // A/m
   long long step; // steps started so far; K1 increments it, K5 reports step - 1
+  // SPEC FieldSchedule: at timestep k = step - 1 the applied field is
+  // hext + a(k) h0, a = 1 on [t0, t1), 1 - (k - t1)/(t2 - t1) on [t1, t2), else 0
+  float h0[3];
+  int sched;
+  long long t0, t1, t2;
 };
+
+// Applied field of the step being computed (constant part + scheduled part).
+__host__ __device__ inline void applied_field(const StepParams& p, float h[3]) {
+  float a = 0.f;
+  if (p.sched) {
+    const long long k = p.step - 1;
+    if (k >= p.t0 && k < p.t2) a = k < p.t1 ? 1.f : 1.f - (float)(k - p.t1) / (float)(p.t2 - p.t1);
+  }
+  for (int q = 0; q < 3; ++q) h[q] = p.hext[q] + a * p.h0[q];
+}
 
 // Geometry and the constant material coefficients (fp32, rounded once from fp64 on the host).
 struct Geom {

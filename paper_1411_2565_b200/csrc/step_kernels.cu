@@ -612,14 +612,16 @@ __device__ __forceinline__ void cell_pair(const CellCtx& cc, const Geom& g, cons
     nz1[c][0] = e.x; nz1[c][1] = e.y;
   }
   float out[2][3];
+  float ha[3];
+  applied_field(p, ha);
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
     const float* hd = s ? hB : hA;
     const float mx = m[0][s], my = m[1][s], mz = m[2][s];
     // Eq. (2): H_eff = H_demag + H_exch + H_anis + H_ext
-    float hx = hd[0] + p.hext[0] + g.ck * mx;
-    float hy = hd[1] + p.hext[1];
-    float hz = hd[2] + p.hext[2];
+    float hx = hd[0] + ha[0] + g.ck * mx;
+    float hy = hd[1] + ha[1];
+    float hz = hd[2] + ha[2];
     // six-neighbour exchange (difference form: uniform M gives exactly 0; reading Q11)
     float e3[3];
 #pragma unroll
@@ -997,6 +999,8 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
     }
   };
   const float cxyz[3] = {g.cx, g.cy, g.cz};
+  float ha[3];
+  applied_field(p, ha);
   // all 24 loads (3 components x centre, Hd, 4 neighbour rows, 2 row ends) first
   float a[3][W], t[3][W], ym[3][W], yp[3][W], zm[3][W], zp[3][W], xl[3], xr[3];
   const size_t iym = y > 0 ? i - g.nx : i, iyp = y + 1 < g.ny ? i + g.nx : i;
@@ -1031,7 +1035,7 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
       e += cxyz[1] * (yp[c][s] - a[c][s]);
       e += cxyz[2] * (zm[c][s] - a[c][s]);
       e += cxyz[2] * (zp[c][s] - a[c][s]);
-      float hv = t[c][s] + p.hext[c];
+      float hv = t[c][s] + ha[c];
       if (c == 0) hv += g.ck * a[c][s];
       h[c][s] = hv + e;
       m[c][s] = a[c][s];
@@ -1556,6 +1560,8 @@ __global__ void k_diag_partial(const float* __restrict__ M, const float* __restr
   const long long chunk = (n + gridDim.x - 1) / gridDim.x;
   const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
   const StepParams p = *prm;
+  float ha[3];
+  applied_field(p, ha);
   double acc[4] = {0, 0, 0, 0}, tmax = 0;
   for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     const long long row = i / g.nx;
@@ -1583,7 +1589,7 @@ __global__ void k_diag_partial(const float* __restrict__ M, const float* __restr
     float h[3];
     for (int c = 0; c < 3; ++c) {
       acc[2] += (double)Hd[c * n + i] * a[c];
-      acc[3] += (double)p.hext[c] * a[c];
+      acc[3] += (double)ha[c] * a[c];
       // H_eff as the step kernels form it (Eq. (2), six-neighbour difference form)
       float e = 0.f;
       e += g.cx * (nb[0][c] - a[c]);
@@ -1592,7 +1598,7 @@ __global__ void k_diag_partial(const float* __restrict__ M, const float* __restr
       e += g.cy * (nb[3][c] - a[c]);
       e += g.cz * (nb[4][c] - a[c]);
       e += g.cz * (nb[5][c] - a[c]);
-      h[c] = Hd[c * n + i] + p.hext[c] + (c == 0 ? g.ck * a[0] : 0.f) + e;
+      h[c] = Hd[c * n + i] + ha[c] + (c == 0 ? g.ck * a[0] : 0.f) + e;
     }
     const double tx = (double)a[1] * h[2] - (double)a[2] * h[1];
     const double ty = (double)a[2] * h[0] - (double)a[0] * h[2];

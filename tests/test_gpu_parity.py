@@ -335,3 +335,26 @@ def test_heff_full_size_sampled_direct_sum(name, nsample):
         got = H[:, k, j, i]
         # fp32 FFT of a 16.8M-point padded grid: error relative to the field scale Ms
         assert np.abs(got - want).max() <= 2e-5 * w.Ms, (i, j, k, got, want)
+
+
+def test_field_schedule_steps_and_heff_match_oracle():
+    """Paper Sec. 5 / SPEC S:L182-187 field schedule: the GPU steps and H_eff at a
+    scheduled time against the oracle Sim with the same schedule."""
+    n, d, Ms, A, Ku, alpha, dt = (24, 10, 3), (2e-9, 2e-9, 3e-9), 8e5, 1.3e-11, 1e4, 0.1, 5e-14
+    hext, h0, sch = (2e3, 0.0, 0.0), (0.0, 3e5, -2e5), (2, 5, 9)
+    M = random_m(n, Ms, seed=13)
+    g = pb.Grace(n, d, Ms, A, Ku, alpha, GAMMA0)
+    g.set_m(M)
+    g.set_hext(hext)
+    g.set_field_schedule(h0, *sch)
+    sim = Sim(g.get_m(), DemagFFT(tensor_octant(*n, *d)), Ms, A, Ku, alpha, GAMMA0, d, hext, schedule=(h0, *sch))
+    for k in range(12):
+        if k in (0, 3, 6, 9):
+            Hg, Ho = g.heff(), sim.heff()
+            assert relL2(Hg, Ho) <= 1e-5, k
+        g.step(1, dt)
+        sim.euler_step(dt)
+        assert np.abs(g.get_m() - sim.M).max() <= 1e-4 * Ms, k
+    with pytest.raises(pb.GraceError):
+        g.set_field_schedule(h0, 5, 4, 9)
+    g.close()
