@@ -77,9 +77,30 @@ class Sim:
         self.M = Mn
         self.step_count += 1
 
-    def run(self, n, dt):
+    def heun_step(self, dt):
+        """Heun (explicit trapezoid, RK2) with the same renormalisation -- SURVEY
+        §8(f) #4(iv), beyond the paper's Euler (SPEC lists higher-order integrators
+        as future work):
+            f0 = rhs(M, H(M, t_k));  M* = renorm(M + dt f0)
+            f1 = rhs(M*, H(M*, t_{k+1}));  M' = renorm(M + dt (f0 + f1) / 2)."""
+        f0 = llg_rhs(self.M, self.heff(), self.alpha, self.gamma0, self.Ms)
+        Mstar = renormalize(self.M + dt * f0, self.Ms)
+        k = self.step_count
+        self.step_count = k + 1  # the corrector's field is the next timestep's
+        H1 = self.heff(Mstar)
+        self.step_count = k
+        f1 = llg_rhs(Mstar, H1, self.alpha, self.gamma0, self.Ms)
+        Mn = renormalize(self.M + (0.5 * dt) * (f0 + f1), self.Ms)
+        bad = ~np.isfinite(Mn).all(axis=0)
+        if bad.any():
+            raise NonFinite(self.step_count, int(np.flatnonzero(bad.ravel())[0]))
+        self.M = Mn
+        self.step_count += 1
+
+    def run(self, n, dt, method="euler"):
+        step = self.heun_step if method == "heun" else self.euler_step
         for _ in range(n):
-            self.euler_step(dt)
+            step(dt)
 
     def mavg(self):
         """<M>/Ms, summed in fixed (C) order (S:L94)."""
