@@ -133,6 +133,14 @@ int grace_relax(grace_ctx *h, double alpha_relax, double dt, long long max_steps
 int grace_set_field_schedule(grace_ctx *h, double h0x, double h0y, double h0z, long long start, long long decay,
                              long long stop);
 
+/* Time integrator of grace_step: 0 = explicit Euler +
+ * renormalisation (the paper's; default), 1 = Heun (explicit trapezoid,
+ * second order) with the same renormalisation: f0 = dM/dt(M_k, t_k),
+ * M* = renorm(M_k + dt f0), M_{k+1} = renorm(M_k + dt (f0 + dM/dt(M*, t_{k+1}))/2);
+ * two H_eff evaluations per step.  GRACE_EINVAL for another kind,
+ * GRACE_EUNSUPPORTED with GRACE_K5_FUSED=1 or in profiling mode. */
+int grace_set_integrator(grace_ctx *h, int kind);
+
 /* Steps taken so far (t = steps * dt). */
 int grace_step_count(grace_ctx *h, long long *steps);
 

@@ -48,6 +48,7 @@ SIGNATURES = [
     ("grace_mavg", _I, [_P, _PD]),
     ("grace_step_count", _I, [_P, _PLL]),
     ("grace_energy", _I, [_P, _PD]),
+    ("grace_set_integrator", _I, [_P, _I]),
     ("grace_set_field_schedule", _I, [_P, _D, _D, _D, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong]),
     ("grace_max_torque", _I, [_P, _PD]),
     ("grace_relax", _I, [_P, _D, _D, ctypes.c_longlong, _D, _I, _PLL, _PD]),
@@ -197,6 +198,10 @@ def grace_set_field_schedule(h, h0, start, decay, stop):
                                            int(stop)))
 
 
+def grace_set_integrator(h, kind):
+    _check(load().grace_set_integrator(h, {"euler": 0, "heun": 1}.get(kind, kind)))
+
+
 def grace_energy(h):
     """(total, exchange, anisotropy, demag, zeeman) in joules."""
     out = (ctypes.c_double * 5)()
@@ -337,6 +342,10 @@ class Grace:
     def set_field_schedule(self, h0, start, decay, stop):
         """Paper/SPEC field schedule: + a(k) h0 (A/m) on top of set_hext's field."""
         grace_set_field_schedule(self.h, h0, start, decay, stop)
+
+    def set_integrator(self, kind):
+        """'euler' (the paper's, default) or 'heun' (second order, two H_eff per step)."""
+        grace_set_integrator(self.h, kind)
 
     def energy(self):
         """Eq. (1) energy terms in joules: dict total/exchange/anisotropy/demag/zeeman."""

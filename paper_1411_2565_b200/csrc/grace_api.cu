@@ -132,6 +132,7 @@ struct Rank {
   double* dred = nullptr;              // diagnostics partials + 5 outputs (allocated on first use)
   float* Hbuf = nullptr;
   float* Hd = nullptr;                 // H_demag [3][nzl][ny][nx] (split K5/K6 step)
+  float* F = nullptr;                  // Heun: dM/dt of the predictor stage
   bool tma = false;                    // TMA descriptors of the K2 / K4 inputs built
   TmapBlob k2map{}, k4map{};
 };
@@ -145,6 +146,7 @@ struct grace_ctx {
   double h0[3] = {0, 0, 0};       // field schedule (grace_set_field_schedule)
   long long sched[3] = {0, 0, 0};
   bool has_sched = false;
+  int integrator = 0;             // 0 Euler (the paper's), 1 Heun (grace_set_integrator)
   long long steps = 0;
   long long nf_step = -1, nf_cell = -1;
   long long N = 0;  // cells addressed by set_m/get_m/heff (whole grid, or the local slab in nccl mode)
@@ -300,8 +302,29 @@ struct grace_ctx {
     return cudaSuccess;
   }
 
+  // One Heun step, M[c] -> M[c]: predictor M* = renorm(M + dt f0) into M[1-c]
+  // (f0 kept in F), then H(M*) and the corrector updates M[c] in place.
+  cudaError_t enqueue_heun(int c, cudaStream_t s) {
+    CE(demag_stages(c, s, true));
+    CE(halo_join(s));
+    for (auto& rk : ranks) {
+      CE(launch_k5(rk.g, 2, rk.A, rk.M[c], nullptr, rk.Hd, tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+      CE(launch_k6(rk.g, 3, rk.Hd, rk.M[c], rk.M[1 - c], rk.F, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+    }
+    CE(demag_stages(1 - c, s, false));
+    CE(halo_join(s));
+    for (auto& rk : ranks) {
+      CE(launch_k5(rk.g, 2, rk.A, rk.M[1 - c], nullptr, rk.Hd, tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+      CE(launch_k6(rk.g, 4, rk.Hd, rk.M[1 - c], rk.M[c], rk.F, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+    }
+    return cudaSuccess;
+  }
+  // buffer index after one step from c
+  int next(int c) const { return integrator == 1 ? c : 1 - c; }
+
   // One step M[c] -> M[1-c] (ev: optional 2 events per kernel, single mode).
   cudaError_t enqueue_step(int c, cudaStream_t s, cudaEvent_t* ev = nullptr) {
+    if (integrator == 1) return enqueue_heun(c, s);
     CE(demag_stages(c, s, true, ev));
     const int nk = kernel_count(g0);
     const int k5 = 2 * (nk - (g0.split_llg ? 2 : 1));
@@ -327,7 +350,7 @@ struct grace_ctx {
     cudaGraph_t graph = nullptr;
     CE(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
     cudaError_t e = cudaSuccess;
-    for (int i = 0; i < nsteps && e == cudaSuccess; ++i) e = enqueue_step((c + i) & 1, cap);
+    for (int i = 0, cc = c; i < nsteps && e == cudaSuccess; ++i, cc = next(cc)) e = enqueue_step(cc, cap);
     cudaError_t e2 = cudaStreamEndCapture(cap, &graph);
     if (e != cudaSuccess) {
       if (graph) cudaGraphDestroy(graph);
@@ -347,7 +370,7 @@ struct grace_ctx {
     for (auto e : ev) cudaEventDestroy(e);
     for (auto& rk : ranks) {
       void* ptrs[] = {rk.M[0], rk.M[1], rk.A,   rk.B,    rk.X2,  rk.KS,   rk.Hlo,
-                      rk.Hhi,  rk.prm,  rk.flag, rk.red, rk.Hbuf, rk.Hd,  rk.dred};
+                      rk.Hhi,  rk.prm,  rk.flag, rk.red, rk.Hbuf, rk.Hd,  rk.dred, rk.F};
       for (void* p : ptrs)
         if (p) cudaFree(p);
     }
@@ -736,6 +759,27 @@ int grace_set_field_schedule(grace_ctx* h, double h0x, double h0y, double h0z, l
   return GRACE_OK;
 }
 
+int grace_set_integrator(grace_ctx* h, int kind) {
+  if (!h) return fail(GRACE_EINVAL, "NULL context");
+  if (kind != 0 && kind != 1) return fail(GRACE_EINVAL, "integrator must be 0 (Euler) or 1 (Heun)");
+  if (kind == h->integrator) return GRACE_OK;
+  if (kind == 1) {
+    if (!h->g0.split_llg) return fail(GRACE_EUNSUPPORTED, "Heun needs the split K5/K6 step (GRACE_K5_FUSED unset)");
+    for (auto& rk : h->ranks)
+      if (!rk.F) {
+        int rc = h->alloc((void**)&rk.F, sizeof(float) * 3 * (size_t)rk.Nl);
+        if (rc) return rc;
+      }
+  }
+  for (int c = 0; c < 2; ++c) {  // captured step graphs belong to the old integrator
+    if (h->g1[c]) cudaGraphExecDestroy(h->g1[c]);
+    if (h->gc[c]) cudaGraphExecDestroy(h->gc[c]);
+    h->g1[c] = h->gc[c] = nullptr;
+  }
+  h->integrator = kind;
+  return GRACE_OK;
+}
+
 int grace_set_alpha(grace_ctx* h, double alpha) {
   if (!h) return fail(GRACE_EINVAL, "NULL context");
   if (!std::isfinite(alpha) || alpha < 0) return fail(GRACE_EINVAL, "alpha must be finite and >= 0");
@@ -786,8 +830,10 @@ int grace_step(grace_ctx* h, int n, double dt) {
     for (int i = 0; i < n; ++i) {
       cudaError_t e = h->enqueue_step(h->cur, s);
       if (e != cudaSuccess) return fail(GRACE_ECUDA, "distributed step: %s", cudaGetErrorString(e));
-      h->cur ^= 1;
+      h->cur = h->next(h->cur);
     }
+  } else if (h->profiling && h->integrator != 0) {
+    return fail(GRACE_EUNSUPPORTED, "profiling mode times the Euler step only");
   } else if (h->profiling) {
     // eager launches with an event pair around every kernel; events are read in
     // batches of kProfBatch steps so the host never waits inside a batch
@@ -826,7 +872,7 @@ int grace_step(grace_ctx* h, int n, double dt) {
       CUDA_OR(cudaGraphLaunch(*gx, s));
       const int done = chunk ? kChunk : 1;
       left -= done;
-      h->cur ^= (done & 1);
+      if (h->integrator == 0) h->cur ^= (done & 1);
     }
   }
   unsigned long long f;

@@ -974,7 +974,10 @@ __global__ void __launch_bounds__(XBulk<L>::NT, 1)
 #ifndef GRACE_K6_MINB
 #define GRACE_K6_MINB 4
 #endif
-template <bool VEC, bool DIST>
+// HEUN = 3: predictor (also stores f = dM/dt into Hout); HEUN = 4: corrector,
+// M' = renorm(M0 + dt (f0 + f(M*)) / 2) with M0 = Mn (updated in place), f0 = Hout,
+// M* = M; the applied field of the next timestep.  HEUN = 0: modes 0 / 1.
+template <bool VEC, bool DIST, int HEUN = 0>
 __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __restrict__ Hd, const float* __restrict__ M,
                                               float* __restrict__ Mn, float* __restrict__ Hout, Geom g,
                                               const StepParams* __restrict__ prm, unsigned long long* __restrict__ flag,
@@ -1000,7 +1003,11 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
   };
   const float cxyz[3] = {g.cx, g.cy, g.cz};
   float ha[3];
-  applied_field(p, ha);
+  {
+    StepParams pf = p;
+    if (HEUN == 4) pf.step += 1;  // the corrector's field: timestep k + 1
+    applied_field(pf, ha);
+  }
   // all 24 loads (3 components x centre, Hd, 4 neighbour rows, 2 row ends) first
   float a[3][W], t[3][W], ym[3][W], yp[3][W], zm[3][W], zp[3][W], xl[3], xr[3];
   const size_t iym = y > 0 ? i - g.nx : i, iyp = y + 1 < g.ny ? i + g.nx : i;
@@ -1041,10 +1048,17 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
       m[c][s] = a[c][s];
     }
   }
-  float o[3][W];
+  float o[3][W], f[3][W], m0[3][W];
+  if constexpr (HEUN == 4) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      ldw(Hout + c * N + i, f[c]);
+      ldw(Mn + c * N + i, m0[c]);
+    }
+  }
 #pragma unroll
   for (int s = 0; s < W; ++s) {
-    if (mode == 1) {
+    if (HEUN == 0 && mode == 1) {
       for (int c = 0; c < 3; ++c) o[c][s] = h[c][s];
       continue;
     }
@@ -1053,9 +1067,24 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
     // Eq. (3): dM/dt = c_prec (M x H) + c_damp M x (M x H); Euler; renormalise (Q16)
     const float ax = my * hz - mz * hy, ay = mz * hx - mx * hz, az = mx * hy - my * hx;
     const float bx = my * az - mz * ay, by = mz * ax - mx * az, bz = mx * ay - my * ax;
-    const float sx = mx + p.dt * (p.c_prec * ax + p.c_damp * bx);
-    const float sy = my + p.dt * (p.c_prec * ay + p.c_damp * by);
-    const float sz = mz + p.dt * (p.c_prec * az + p.c_damp * bz);
+    float sx, sy, sz;
+    if constexpr (HEUN == 4) {
+      const float dx = p.c_prec * ax + p.c_damp * bx, dy = p.c_prec * ay + p.c_damp * by,
+                  dz = p.c_prec * az + p.c_damp * bz;
+      const float hdt = 0.5f * p.dt;
+      sx = m0[0][s] + hdt * (f[0][s] + dx);
+      sy = m0[1][s] + hdt * (f[1][s] + dy);
+      sz = m0[2][s] + hdt * (f[2][s] + dz);
+    } else {
+      if constexpr (HEUN == 3) {
+        f[0][s] = p.c_prec * ax + p.c_damp * bx;
+        f[1][s] = p.c_prec * ay + p.c_damp * by;
+        f[2][s] = p.c_prec * az + p.c_damp * bz;
+      }
+      sx = mx + p.dt * (p.c_prec * ax + p.c_damp * bx);
+      sy = my + p.dt * (p.c_prec * ay + p.c_damp * by);
+      sz = mz + p.dt * (p.c_prec * az + p.c_damp * bz);
+    }
     const float sc = g.Ms / sqrtf(sx * sx + sy * sy + sz * sz);
     o[0][s] = sx * sc;
     o[1][s] = sy * sc;
@@ -1063,11 +1092,15 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
     if (!(isfinite(o[0][s]) && isfinite(o[1][s]) && isfinite(o[2][s])))
       atomicMin(flag, ((unsigned long long)(p.step - 1) << 36) | (unsigned long long)(i + s));
   }
-  float* dst = mode == 1 ? Hout : Mn;
+  float* dst = (HEUN == 0 && mode == 1) ? Hout : Mn;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     if constexpr (VEC) *reinterpret_cast<float4*>(dst + c * N + i) = make_float4(o[c][0], o[c][1], o[c][2], o[c][3]);
     else dst[c * N + i] = o[c][0];
+    if constexpr (HEUN == 3) {
+      if constexpr (VEC) *reinterpret_cast<float4*>(Hout + c * N + i) = make_float4(f[c][0], f[c][1], f[c][2], f[c][3]);
+      else Hout[c * N + i] = f[c][0];
+    }
   }
 }
 
@@ -1372,21 +1405,32 @@ cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* 
 bool fused_y_path(const Geom& g) { return g.Pz == 1 && g.Py <= 512; }
 int kernel_count(const Geom& g) { return (fused_y_path(g) ? 3 : 5) + (g.split_llg ? 1 : 0); }
 
-cudaError_t launch_k6(const Geom& g, int mode, const float* Hd, const float* M, float* Mn, float* Hout,
-                      const StepParams* prm, unsigned long long* flag, cudaStream_t st, const float* Hlo,
-                      const float* Hhi) {
+template <int HEUN>
+static cudaError_t k6_launch(const Geom& g, int mode, const float* Hd, const float* M, float* Mn, float* Hout,
+                             const StepParams* prm, unsigned long long* flag, cudaStream_t st, const float* Hlo,
+                             const float* Hhi) {
   const long long N = (long long)g.nzl * g.ny * g.nx;
   const bool vec = g.nx % 4 == 0;
   const long long threads = vec ? N / 4 : N;
   const unsigned grid = (unsigned)((threads + 255) / 256);
   if (vec) {
-    if (g.kb) GRACE_TRY(launch_k(32, k6_llg<true, true>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
-    else GRACE_TRY(launch_k(32, k6_llg<true, false>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
+    if (g.kb) GRACE_TRY(launch_k(32, k6_llg<true, true, HEUN>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
+    else GRACE_TRY(launch_k(32, k6_llg<true, false, HEUN>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
   } else {
-    if (g.kb) GRACE_TRY(launch_k(32, k6_llg<false, true>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
-    else GRACE_TRY(launch_k(32, k6_llg<false, false>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
+    if (g.kb) GRACE_TRY(launch_k(32, k6_llg<false, true, HEUN>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
+    else GRACE_TRY(launch_k(32, k6_llg<false, false, HEUN>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
   }
   return cudaGetLastError();
+}
+
+// mode 0: Euler step M -> Mn; 1: H_eff -> Hout; 3: Heun predictor (M* -> Mn,
+// dM/dt -> Hout); 4: Heun corrector (M = M*, Mn = M_k updated in place, Hout = f0).
+cudaError_t launch_k6(const Geom& g, int mode, const float* Hd, const float* M, float* Mn, float* Hout,
+                      const StepParams* prm, unsigned long long* flag, cudaStream_t st, const float* Hlo,
+                      const float* Hhi) {
+  if (mode == 3) return k6_launch<3>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
+  if (mode == 4) return k6_launch<4>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
+  return k6_launch<0>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
 }
 
 template <int L>

@@ -16,6 +16,8 @@ from workloads import WORKLOADS, random_m  # noqa: E402
 w = WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "slab_1024x1024x32"]
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 g = pb.Grace(w.n, w.d, w.Ms, w.A, w.Ku, w.alpha, w.gamma0)
+integ = os.environ.get("GRACE_INTEGRATOR", "euler")
+g.set_integrator(integ)
 s = torch.cuda.Stream()
 pb.grace_set_stream(g.h, s.cuda_stream)
 g.set_m(random_m(w.n, w.Ms))
@@ -31,4 +33,4 @@ for _ in range(3):
     torch.cuda.synchronize()
     res.append(e0.elapsed_time(e1) / steps)
 print(f"{w.name} graph-mode ms/step {min(res):.4f} (runs {', '.join('%.4f' % r for r in res)}) "
-      f"PDL={'off' if os.environ.get('GRACE_NO_PDL') else 'on'}")
+      f"PDL={'off' if os.environ.get('GRACE_NO_PDL') else 'on'} integrator={integ}")

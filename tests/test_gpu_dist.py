@@ -84,3 +84,19 @@ def test_virtual_errors():
         g.set_m(M)
     assert e.value.code == pb.GRACE_EZEROCELL and "cell 106" in str(e.value)
     g.close()
+
+
+def test_virtual_ranks_heun_matches_single():
+    """Heun on the partitioned path: the predictor's halos are re-exchanged for M*."""
+    n, d, Ms = (16, 12, 8), (1e-9, 1e-9, 1e-9), 8e5
+    M = random_m(n, Ms, seed=47)
+    out = []
+    for kw in ({}, {"virtual_ranks": 4}):
+        g = pb.Grace(n, d, Ms, 1.3e-11, 2e4, 0.3, GAMMA0, **kw)
+        g.set_integrator("heun")
+        g.set_m(M)
+        g.set_hext((1e4, 0, -5e3))
+        g.step(12, 2e-14)
+        out.append(g.get_m())
+        g.close()
+    assert np.abs(out[0] - out[1]).max() <= 1e-6 * Ms

@@ -358,3 +358,53 @@ def test_field_schedule_steps_and_heff_match_oracle():
     with pytest.raises(pb.GraceError):
         g.set_field_schedule(h0, 5, 4, 9)
     g.close()
+
+
+# ---------------------------------------------------------------- Heun (RK2)
+
+def test_heun_precession_closed_form_single_cell():
+    """Heun + renormalisation rotates by the exact angle of tests/test_oracle_fields_llg.py."""
+    g0, Hm, Ms, dt = GAMMA0, 1e5, 8e5, 1e-13
+    phi = g0 * Hm * dt
+    th = np.arctan(phi)
+    psi = np.arctan2(0.5 * phi * (1 + np.cos(th)), 1 - 0.5 * phi * np.sin(th))
+    g = pb.Grace((1, 1, 1), (2e-9, 2e-9, 2e-9), Ms, 0.0, 0.0, 0.0, g0)
+    g.set_integrator("heun")
+    M = np.zeros((3, 1, 1, 1))
+    M[0] = Ms
+    g.set_m(M)
+    g.set_hext((0, 0, Hm))
+    for n in (1, 10, 100, 1000):
+        g.step(n - g.steps, dt)
+        want = Ms * np.array([np.cos(n * psi), np.sin(n * psi), 0.0])
+        assert np.abs(g.get_m()[:, 0, 0, 0] - want).max() <= 2e-6 * Ms * max(1, n / 100)
+    g.close()
+
+
+@pytest.mark.parametrize("n,d", [((24, 10, 3), (2e-9, 2e-9, 3e-9)), ((100, 25, 1), (5e-9, 5e-9, 3e-9))])
+def test_heun_steps_match_oracle(n, d):
+    Ms, A, Ku, alpha, dt = 8e5, 1.3e-11, 1e4, 0.1, 5e-14
+    hext, h0, sch = (2e3, 0.0, 0.0), (0.0, 3e5, -2e5), (2, 4, 8)
+    g = pb.Grace(n, d, Ms, A, Ku, alpha, GAMMA0)
+    g.set_integrator("heun")
+    g.set_m(random_m(n, Ms, seed=19))
+    g.set_hext(hext)
+    g.set_field_schedule(h0, *sch)
+    sim = Sim(g.get_m(), DemagFFT(tensor_octant(*n, *d)), Ms, A, Ku, alpha, GAMMA0, d, hext, schedule=(h0, *sch))
+    g.step(1, dt)
+    sim.heun_step(dt)
+    assert np.abs(g.get_m() - sim.M).max() <= 2e-5 * Ms
+    g.step(9, dt)
+    sim.run(9, dt, "heun")
+    Mg = g.get_m()
+    assert np.abs(Mg - sim.M).max() <= 1e-4 * Ms
+    assert relL2(Mg, sim.M) <= 1e-5
+    assert g.steps == 10
+    # switching back to Euler continues from the same state
+    g.set_integrator("euler")
+    g.step(2, dt)
+    sim.run(2, dt)
+    assert np.abs(g.get_m() - sim.M).max() <= 1e-4 * Ms
+    with pytest.raises(pb.GraceError):
+        g.set_integrator(7)
+    g.close()
