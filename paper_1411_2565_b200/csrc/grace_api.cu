@@ -166,6 +166,14 @@ struct grace_ctx {
   std::vector<long long> klaunch;
   std::vector<cudaEvent_t> ev;
   StepParams hprm{};
+  // pinned staging for the small per-call transfers (params up; flag, <M> and
+  // diagnostics down): truly asynchronous copies instead of pageable staging
+  struct Pinned {
+    StepParams prm;
+    unsigned long long flag;
+    double red[8];
+  };
+  Pinned* pin = nullptr;
 
   int alloc(void** p, size_t b) {
     if (b == 0) b = 16;
@@ -197,7 +205,8 @@ struct grace_ctx {
   cudaError_t upload_params(double dt, bool eval = false) {
     fill_params(dt);
     if (eval) hprm.step = steps + 1;
-    for (auto& rk : ranks) CE(cudaMemcpyAsync(rk.prm, &hprm, sizeof(StepParams), cudaMemcpyHostToDevice, stream));
+    pin->prm = hprm;  // every caller synchronises the stream before the next upload
+    for (auto& rk : ranks) CE(cudaMemcpyAsync(rk.prm, &pin->prm, sizeof(StepParams), cudaMemcpyHostToDevice, stream));
     return cudaSuccess;
   }
 
@@ -378,6 +387,7 @@ struct grace_ctx {
     if (comm) g_nccl.commDestroy(comm);
     if (own) cudaStreamDestroy(own);
     if (cap) cudaStreamDestroy(cap);
+    if (pin) cudaFreeHost(pin);
     if (hs) cudaStreamDestroy(hs);
     if (evM) cudaEventDestroy(evM);
     if (evH) cudaEventDestroy(evH);
@@ -494,6 +504,7 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
   {
     cudaError_t e = cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMallocHost((void**)&h->pin, sizeof(grace_ctx::Pinned));
     if (e == cudaSuccess && mode != grace_ctx::kSingle) e = cudaStreamCreateWithFlags(&h->hs, cudaStreamNonBlocking);
     if (e == cudaSuccess && mode != grace_ctx::kSingle) e = cudaEventCreateWithFlags(&h->evM, cudaEventDisableTiming);
     if (e == cudaSuccess && mode != grace_ctx::kSingle) e = cudaEventCreateWithFlags(&h->evH, cudaEventDisableTiming);
@@ -595,8 +606,9 @@ int check_flags(grace_ctx* h, int which, unsigned long long* first) {
   *first = kNoFlag;
   for (auto& rk : h->ranks) {
     unsigned long long f = kNoFlag;
-    CUDA_OR(cudaMemcpyAsync(&f, rk.flag + which, sizeof f, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_OR(cudaMemcpyAsync(&h->pin->flag, rk.flag + which, sizeof f, cudaMemcpyDeviceToHost, h->stream));
     CUDA_OR(cudaStreamSynchronize(h->stream));
+    f = h->pin->flag;
     if (f == kNoFlag) continue;
     CUDA_OR(cudaMemsetAsync(rk.flag + which, 0xff, sizeof f, h->stream));
     CUDA_OR(cudaStreamSynchronize(h->stream));
@@ -899,8 +911,10 @@ int grace_mavg(grace_ctx* h, double* out3) {
                                               kNcclSum, h->comm, h->stream);
       if (r != 0) return fail(GRACE_ECUDA, "ncclAllReduce: %s", g_nccl.errStr(r));
     }
-    CUDA_OR(cudaMemcpyAsync(part, rk.red + kMavgPartials, 3 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_OR(cudaMemcpyAsync(h->pin->red, rk.red + kMavgPartials, 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                            h->stream));
     CUDA_OR(cudaStreamSynchronize(h->stream));
+    std::memcpy(part, h->pin->red, sizeof part);
     for (int q = 0; q < 3; ++q) acc[q] += part[q];
   }
   for (int q = 0; q < 3; ++q) out3[q] = acc[q] / h->P;  // equal slabs: mean of the slab means
@@ -936,8 +950,9 @@ static int diagnostics(grace_ctx* h, double S[5]) {
       if (r != 0) return fail(GRACE_ECUDA, "ncclAllReduce: %s", g_nccl.errStr(r));
     }
     double v[5];
-    CUDA_OR(cudaMemcpyAsync(v, out, sizeof v, cudaMemcpyDeviceToHost, s));
+    CUDA_OR(cudaMemcpyAsync(h->pin->red, out, sizeof v, cudaMemcpyDeviceToHost, s));
     CUDA_OR(cudaStreamSynchronize(s));
+    std::memcpy(v, h->pin->red, sizeof v);
     for (int q = 0; q < 4; ++q) S[q] += v[q];
     S[4] = std::max(S[4], v[4]);
   }
