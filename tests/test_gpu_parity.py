@@ -269,6 +269,21 @@ def test_errors_and_nonfinite_report():
     g.close()
 
 
+def test_size_limits_unsupported_and_out_of_memory():
+    """Padded lengths beyond the compiled FFT set -> GRACE_EUNSUPPORTED; a grid whose
+    working set exceeds HBM (4096 x 2048 x 512: X2 alone ~207 GB) -> GRACE_ENOMEM
+    with everything released, so a following create succeeds."""
+    with pytest.raises(pb.GraceError) as e:
+        pb.grace_create(5000, 4, 4, 1e-9, 1e-9, 1e-9, 8e5, 1e-11, 0, 0.5, GAMMA0)
+    assert e.value.code == pb.GRACE_EUNSUPPORTED
+    with pytest.raises(pb.GraceError) as e:
+        pb.grace_create(4096, 2048, 512, 1e-9, 1e-9, 1e-9, 8e5, 1e-11, 0, 0.5, GAMMA0)
+    assert e.value.code == pb.GRACE_ENOMEM
+    g = pb.Grace((8, 8, 8), (1e-9,) * 3, 8e5, 1e-11, 0.0, 0.5, GAMMA0)
+    g.step(2, 1e-14)
+    g.close()
+
+
 # ---------------------------------------------------------------- SP4 trajectories
 
 def _golden(name):
