@@ -346,7 +346,7 @@ __device__ __forceinline__ void stage_ks(float* kss, const float* __restrict__ b
 #define GRACE_Z_MINNT 128
 #endif
 #ifndef GRACE_ZB_128
-#define GRACE_ZB_128 8
+#define GRACE_ZB_128 16
 #endif
 #ifndef GRACE_ZB_256
 #define GRACE_ZB_256 4
@@ -358,13 +358,18 @@ template <int L>
 struct ZPlan {
   static constexpr bool FUSE = L >= 2 && L <= 64;
   static constexpr int RLAST = L <= 1 ? 1 : 1 << fft_pass_bits(L, fft_npass(L) - 1);
-  static constexpr int TPC = L <= 1 ? 1 : (FUSE ? L / RLAST : (L / 8 > 0 ? L / 8 : 1));
+  // threads per column, unfused: L / R for the plan's largest radix R up to
+  // L = 512, so no pass leaves threads idle (L / 8 idled half of them in the
+  // radix-16 passes: 128^3 cube K3 0.32 -> 0.17 ms, block 17.9 -> 12.1 ms);
+  // L / 8 for L = 1024 (16.8.8: more threads beat the idle pass, 20.7 vs 23.0 ms)
+  static constexpr int R0 = L <= 1 ? 1 : 1 << fft_pass_bits(L, 0);
+  static constexpr int TPC = L <= 1 ? 1 : (FUSE ? L / RLAST : (L <= 512 ? L / R0 : L / 8));
   // fused (short) pencils: at least GRACE_Z_MINNT threads per CTA; unfused:
   // GRACE_Z_ELEMS values per component per CTA (smem: 3 components resident)
   static constexpr int BF = (GRACE_Z_MINNT / TPC > GRACE_ZB ? GRACE_Z_MINNT / TPC : GRACE_ZB);
-  // unfused columns per CTA by length, measured on the Table-1 cubes (K3 ms,
-  // B = 2 / 4 / 8 / 16): L = 128 (64^3) 8 best (0.025 vs 0.040 at 16);
-  // L = 256 (128^3) 4 (0.32 vs 0.43 at 8); L = 512 (256^3) 8 (1.45 vs 1.50 at 4,
+  // unfused columns per CTA by length, measured (K3 ms): L = 128 16 (block
+  // 2048x2048x64: 12.1 vs 15.9 at 8; the 64^3 cube prefers 8, 0.021 vs 0.025);
+  // L = 256 (128^3) 4 (0.17, same at 8); L = 512 (256^3) 8 (1.45 vs 1.50 at 4,
   // 2.17 at 2); L = 1024 (512^3) 4 (20.7 vs 26.9 at 2)
   static constexpr int BN = L <= 128 ? GRACE_ZB_128 : (L == 256 ? GRACE_ZB_256 : (L == 512 ? GRACE_ZB_512 : (L == 1024 ? 4 : (2048 / L > 1 ? 2048 / L : 1))));
   static constexpr int B = L <= 1 ? GRACE_ZB : (FUSE ? (BF < 2048 / L ? BF : 2048 / L) : BN);
@@ -1310,7 +1315,11 @@ static cudaError_t ky_tma_launch(const Geom& g, float2* out, const float2* tw, c
 
 cudaError_t launch_k2(const Geom& g, const float2* X1, float2* X2, const float2* tw, cudaStream_t st,
                       const TmapBlob* tmap) {
-  if (tmap != nullptr && g.Py >= kTmaMinL) {
+  // The TMA tiles hold GRACE_YT_ELEMS / L columns; below 4 (L >= 4096) K2's row
+  // stores are 16-byte half sectors and cost L2 read-modify-writes (block
+  // 2048x2048x64: 22.3 ms, 4.6x the input read from DRAM), so K2 takes the
+  // 4-column non-TMA kernel there (11.4 ms); K4 keeps TMA (7.9 vs 13.6 ms).
+  if (tmap != nullptr && g.Py >= kTmaMinL && GRACE_YT_ELEMS / g.Py >= 4) {
 #define CASE(v) case v: return (v >= kTmaMinL) ? ky_tma_launch<(v >= kTmaMinL ? v : kTmaMinL), false>(g, X2, tw, st, g.Py, tmap) : cudaErrorInvalidValue;
     GRACE_L_SWITCH(g.Py, CASE)
 #undef CASE
