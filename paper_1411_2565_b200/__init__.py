@@ -74,10 +74,27 @@ class GraceError(RuntimeError):
         self.code = code
 
 
+def _torch_nccl():
+    """torch's bundled libnccl (the NCCL torch.distributed uses), if installed."""
+    try:
+        import nvidia.nccl
+
+        for d in nvidia.nccl.__path__:
+            p = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(p):
+                return p
+    except ImportError:
+        pass
+    return None
+
+
 def load(path=LIB_PATH):
     """Load libgrace.so (raises if it was not built: there is no fallback)."""
     global _lib
     if _lib is None:
+        # one NCCL per process: libgrace dlopens the library torch.distributed uses
+        if "GRACE_NCCL_LIB" not in os.environ and _torch_nccl():
+            os.environ["GRACE_NCCL_LIB"] = _torch_nccl()
         if not os.path.exists(path):
             raise ImportError(f"{path} not built; run __graft_entry__.build() (no CPU fallback exists)")
         lib = ctypes.CDLL(path)

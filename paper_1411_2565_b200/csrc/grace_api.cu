@@ -77,13 +77,15 @@ struct Nccl {
   ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
-  ncclResult_t (*allToAll)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*allReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*groupStart)() = nullptr;
   ncclResult_t (*groupEnd)() = nullptr;
   const char* (*errStr)(ncclResult_t) = nullptr;
+  // The process's NCCL: GRACE_NCCL_LIB (the Python binding points it at torch's
+  // bundled libnccl), else an already-loaded or system libnccl.so.2.  Only calls
+  // present in every NCCL >= 2.7 are used (the transposes are grouped send/recv).
   bool load() {
     if (h) return true;
     const char* env = getenv("GRACE_NCCL_LIB");
@@ -92,21 +94,22 @@ struct Nccl {
       if (!n) continue;
       h = dlopen(n, RTLD_NOW | RTLD_NOLOAD);
       if (!h) h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
-      if (h) break;
+      if (h && bind()) return true;
+      h = nullptr;
     }
-    if (!h) return false;
+    return false;
+  }
+  bool bind() {
     getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
     commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
     commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
-    allToAll = (decltype(allToAll))dlsym(h, "ncclAlltoAll");
     allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
     send = (decltype(send))dlsym(h, "ncclSend");
     recv = (decltype(recv))dlsym(h, "ncclRecv");
     groupStart = (decltype(groupStart))dlsym(h, "ncclGroupStart");
     groupEnd = (decltype(groupEnd))dlsym(h, "ncclGroupEnd");
     errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
-    return getUniqueId && commInitRank && commDestroy && allToAll && allReduce && send && recv && groupStart &&
-           groupEnd && errStr;
+    return getUniqueId && commInitRank && commDestroy && allReduce && send && recv && groupStart && groupEnd && errStr;
   }
 };
 Nccl g_nccl;
@@ -222,9 +225,16 @@ struct grace_ctx {
                              sizeof(float2) * blk, cudaMemcpyDeviceToDevice, s));
       return cudaSuccess;
     }
+    // grouped point-to-point: block q of the send buffer to rank q, block q of the
+    // receive buffer from rank q (what ncclAlltoAll does, without needing NCCL >= 2.28)
     Rank& rk = ranks[0];
-    const ncclResult_t r = g_nccl.allToAll(rk.*src, rk.*dst, (size_t)blk * 2, kNcclFloat32, comm, s);
-    return r == 0 ? cudaSuccess : cudaErrorUnknown;
+    bool bad = g_nccl.groupStart() != 0;
+    for (int q = 0; q < P && !bad; ++q) {
+      bad |= g_nccl.send(rk.*src + (size_t)q * blk, (size_t)blk * 2, kNcclFloat32, q, comm, s) != 0;
+      bad |= g_nccl.recv(rk.*dst + (size_t)q * blk, (size_t)blk * 2, kNcclFloat32, q, comm, s) != 0;
+    }
+    bad |= g_nccl.groupEnd() != 0;
+    return bad ? cudaErrorUnknown : cudaSuccess;
   }
   // halo: plane nzl-1 of rank r-1 -> Hlo of rank r; plane 0 of rank r+1 -> Hhi of rank r.
   cudaError_t halo(int c, cudaStream_t s) {
@@ -438,9 +448,10 @@ int make_geom(int nx, int ny, int nz, double dx, double dy, double dz, double Ms
 }
 
 // The slab of rank r of P.
-Geom rank_geom(const Geom& g0, int r, int P) {
+// dist: the distributed layouts (also with P = 1, GRACE_FORCE_NCCL)
+Geom rank_geom(const Geom& g0, int r, int P, bool dist) {
   Geom g = g0;
-  if (P == 1) return g;
+  if (!dist) return g;
   const int Kb = (int)round_up((g0.Kx + P - 1) / P, 2);  // even: 16-byte TMA row strides
   g.nzl = g0.nz / P;
   g.kb = Kb;
@@ -495,7 +506,8 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
   h->Ku = Ku;
   h->alpha = alpha;
   h->gamma0 = gamma;
-  h->fused = (P == 1) && fused_y_path(g0);
+  const bool dlay = mode != grace_ctx::kSingle;  // distributed layouts and transposes
+  h->fused = !dlay && fused_y_path(g0);
   auto bail = [&](int code) {
     h->release();
     delete h;
@@ -523,16 +535,16 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
   for (int i = 0; i < nranks_here; ++i) {
     Rank& rk = h->ranks[i];
     rk.r = first_rank + i;
-    rk.g = rank_geom(g0, rk.r, P);
+    rk.g = rank_geom(g0, rk.r, P, dlay);
     const Geom& g = rk.g;
     rk.Nl = (long long)g.nzl * ny * nx;
     const size_t mb = sizeof(float) * 3 * (size_t)rk.Nl;
-    const size_t ab = P == 1 ? sizeof(float2) * 3 * (size_t)nz * ny * g.Kxp : sizeof(float2) * (size_t)P * g.blk1;
+    const size_t ab = !dlay ? sizeof(float2) * 3 * (size_t)nz * ny * g.Kxp : sizeof(float2) * (size_t)P * g.blk1;
     const size_t x2 = h->fused ? 0 : sizeof(float2) * 3 * (size_t)nz * g.Py * g.pitch2;
     const size_t ks = sizeof(float) * 6 * (size_t)g.Kzh * g.Kyh * g.KSp;
     const size_t hb = sizeof(float) * 3 * (size_t)ny * nx;
     if ((rc = h->alloc((void**)&rk.M[0], mb)) || (rc = h->alloc((void**)&rk.M[1], mb)) ||
-        (rc = h->alloc((void**)&rk.A, ab)) || (P > 1 && (rc = h->alloc((void**)&rk.B, ab))) ||
+        (rc = h->alloc((void**)&rk.A, ab)) || (dlay && (rc = h->alloc((void**)&rk.B, ab))) ||
         (x2 && (rc = h->alloc((void**)&rk.X2, x2))) || (rc = h->alloc((void**)&rk.KS, ks)) ||
         (g.has_lo && (rc = h->alloc((void**)&rk.Hlo, hb))) || (g.has_hi && (rc = h->alloc((void**)&rk.Hhi, hb))) ||
         (rc = h->alloc((void**)&rk.prm, sizeof(StepParams))) ||
@@ -545,7 +557,7 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
   // TMA descriptors for the y-pencil kernels (K2 reads the x-row layout, K4 reads X2)
   if (!h->fused && !getenv("GRACE_NO_TMA"))
     for (auto& rk : h->ranks)
-      rk.tma = make_ky_tmaps(rk.g, P == 1 ? rk.A : rk.B, rk.X2, &rk.k2map, &rk.k4map) == cudaSuccess;
+      rk.tma = make_ky_tmaps(rk.g, dlay ? rk.B : rk.A, rk.X2, &rk.k2map, &rk.k4map) == cudaSuccess;
   cudaGetLastError();
   h->N = (mode == grace_ctx::kNccl) ? h->ranks[0].Nl : (long long)nx * ny * nz;
 
@@ -559,15 +571,15 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
   const size_t workb = sizeof(double2) * (size_t)g0.Px * g0.Py * g0.Pz;
   const size_t ksfb = sizeof(float) * 6 * (size_t)g0.Kzh * g0.Kyh * g0.KSp;
   if (cudaMalloc(&oct, octb) != cudaSuccess || cudaMalloc(&work, workb) != cudaSuccess ||
-      (P > 1 && cudaMalloc(&ksfull, ksfb) != cudaSuccess)) {
+      (dlay && cudaMalloc(&ksfull, ksfb) != cudaSuccess)) {
     cudaGetLastError();
     if (oct) cudaFree(oct);
     if (work) cudaFree(work);
     return bail(fail(GRACE_ENOMEM, "setup needs %zu bytes of fp64 scratch", octb + workb + ksfb));
   }
   cudaError_t e = tensor_octant_device(nx, ny, nz, dx, dy, dz, oct, s);
-  if (e == cudaSuccess) e = kernel_spectrum_device(g0, oct, work, P == 1 ? h->ranks[0].KS : ksfull, s);
-  if (e == cudaSuccess && P > 1) {
+  if (e == cudaSuccess) e = kernel_spectrum_device(g0, oct, work, !dlay ? h->ranks[0].KS : ksfull, s);
+  if (e == cudaSuccess && dlay) {
     for (auto& rk : h->ranks) {
       if (rk.g.Kc == 0) continue;
       const int kx0 = rk.r * rk.g.kb;
@@ -657,7 +669,11 @@ int grace_nccl_unique_id(void* out128) {
 int grace_create_dist(int nx, int ny, int nz, double dx, double dy, double dz, double Ms, double A, double Ku,
                       double alpha, double gamma, int rank, int nranks, const void* nccl_id, grace_ctx** out) {
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(GRACE_EINVAL, "bad rank %d of %d", rank, nranks);
-  if (nranks == 1) return grace_create(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma, out);
+  // One rank is the single-GPU context, unless GRACE_FORCE_NCCL is set: then the
+  // NCCL path runs with P = 1 (distributed layouts, ncclAllToAll / ncclAllReduce on
+  // a one-rank communicator) -- how its host and device plumbing is exercised on a
+  // one-GPU machine (tests/test_gpu_dist.py).
+  if (nranks == 1 && !getenv("GRACE_FORCE_NCCL")) return grace_create(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma, out);
   if (!nccl_id) return fail(GRACE_EINVAL, "NULL nccl id");
   return create_impl(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma, grace_ctx::kNccl, nranks, rank, 1, nccl_id,
                      out);

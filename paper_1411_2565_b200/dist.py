@@ -85,5 +85,6 @@ def create_context(w, rank, nranks, device_index):
 
         nid = broadcast_bytes(nid, 0, device=torch.device("cuda", device_index)
                               if dist.get_backend() == "nccl" else None)
+    force = bool(os.environ.get("GRACE_FORCE_NCCL"))  # one-rank NCCL path (plumbing tests)
     return pb.Grace(w.n, w.d, w.Ms, w.A, w.Ku, w.alpha, w.gamma0,
-                    dist=(rank, nranks, nid) if nranks > 1 else None)
+                    dist=(rank, nranks, nid) if (nranks > 1 or force) else None)

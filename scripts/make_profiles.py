@@ -129,7 +129,7 @@ def main(rnd, rep, launches, bench):
                          f"{bk.get('ms_per_launch', float('nan')):.3f} | {bk.get('share', float('nan')):.3f} |")
     lines += ["", f"Bench line: {b['ms_per_step']:.3f} ms/step, {b['value'] / 1e9:.2f} Gcell-updates/s, dominant kernel "
               f"{b['roofline']['kernel']} at {b['roofline']['achieved']:.0f} GB/s = {b['roofline']['frac']:.3f} of "
-              f"{b['roofline']['peak']} GB/s; step {b['roofline']['step_GBps']:.0f} GB/s = "
+              f"{b['roofline']['peak']} GB/s; step {b['roofline'].get('step_GBps_per_gpu', b['roofline'].get('step_GBps')):.0f} GB/s = "
               f"{b['roofline']['step_frac']:.3f} of the measured HBM copy peak."]
     open(os.path.join(PROF, f"{rnd}_ncu_summary.md"), "w").write("\n".join(lines) + "\n")
     text = open(launches).read().splitlines()

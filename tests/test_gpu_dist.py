@@ -100,3 +100,35 @@ def test_virtual_ranks_heun_matches_single():
         out.append(g.get_m())
         g.close()
     assert np.abs(out[0] - out[1]).max() <= 1e-6 * Ms
+
+
+def test_nccl_path_one_rank_matches_single(monkeypatch):
+    """The real NCCL path (dlopen'd libnccl, unique id, communicator, ncclAllToAll
+    for both transposes, ncclAllReduce for <M> and the diagnostics, destination-
+    blocked layouts) on a one-rank communicator (GRACE_FORCE_NCCL): same results
+    as the single-GPU context.  Multi-rank NCCL runs need more GPUs than this
+    machine gives; the P > 1 index logic is covered by the virtual ranks above."""
+    monkeypatch.setenv("GRACE_FORCE_NCCL", "1")
+    n, d, Ms = (48, 20, 6), (2e-9, 2e-9, 3e-9), 8e5
+    M = random_m(n, Ms, seed=53)
+    h = pb.grace_create_dist(*n, *d, Ms, 1.3e-11, 2e4, 0.3, GAMMA0, 0, 1, pb.grace_nccl_unique_id())
+    assert pb.grace_partition(h)["P"] == 1 and pb.grace_partition(h)["kx_block"] > 0  # distributed layouts, P = 1
+    ref = pb.Grace(n, d, Ms, 1.3e-11, 2e4, 0.3, GAMMA0)
+    for hh in (h, ref.h):
+        pb.grace_set_m(hh, M.ravel().copy())
+        pb.grace_set_hext(hh, 1e4, -3e3, 2e3)
+    out = []
+    for hh in (h, ref.h):
+        H = np.empty(3 * M[0].size)
+        pb.grace_heff(hh, H)
+        pb.grace_step(hh, 7, 2e-14)
+        Mo = np.empty(3 * M[0].size)
+        pb.grace_get_m(hh, Mo)
+        out.append((H, Mo, pb.grace_mavg(hh), pb.grace_energy(hh)))
+    (Ha, Ma, ma, ea), (Hb, Mb, mb, eb) = out
+    assert np.abs(Ha - Hb).max() <= 1e-6 * np.abs(Hb).max()
+    assert np.abs(Ma - Mb).max() <= 1e-6 * Ms
+    np.testing.assert_allclose(ma, mb, rtol=0, atol=1e-9)
+    np.testing.assert_allclose(ea, eb, rtol=1e-9, atol=0)
+    pb.grace_destroy(h)
+    ref.close()
