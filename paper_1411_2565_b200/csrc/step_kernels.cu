@@ -296,6 +296,89 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, GRACE_YT_MINB)
   }
 }
 
+// K2 for long pencils (L >= 4096), where two TMA tiles of >= 4 columns do not fit:
+// one work tile of 4 columns (full 32-byte row sectors on the store side) plus
+// one staging buffer for the forward input (rows < L/2).  Pass 0 reads the
+// staged rows into registers and writes the work tile; as soon as every thread
+// is past it, the next tile's TMA load goes into the staging buffer and overlaps
+// the remaining passes.  Twiddles from the global table (no room for smem ones).
+template <int L>
+struct YStage {
+  static constexpr int NCOL = 4;
+  using T = TileIdx<L, NCOL, true>;
+  static constexpr int WB = ((T::ELEMS * 8 + 1023) / 1024) * 1024;  // work tile bytes
+  static constexpr int SB = NCOL * (L / 2) * 8;                       // staging bytes
+  static constexpr size_t SMEM = (size_t)WB + SB + 64;
+  static constexpr int NT = NCOL * (L / 16);
+  static constexpr int BR = 256;
+};
+
+template <int L>
+__global__ void __launch_bounds__(YStage<L>::NT, 1)
+    k_y_stage(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, const float2* __restrict__ tw, Geom g,
+              int n_out) {
+  using Y = YStage<L>;
+  constexpr int NCOL = Y::NCOL, NT = Y::NT, ROWS = L / 2, NBOX = ROWS / Y::BR;
+  constexpr unsigned TX = NCOL * ROWS * 8;
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  float2* work = reinterpret_cast<float2*>(smraw);
+  float2* stage = reinterpret_cast<float2*>(smraw + Y::WB);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + Y::WB + Y::SB);
+  pdl_trigger();
+  const int ntx = (g.Kc + NCOL - 1) / NCOL;
+  const int ntiles = ntx * 3 * g.nz;
+  auto issue = [&](int t) {
+    const int slab = t / ntx, xt = t - slab * ntx;
+    const int c = slab / g.nz, z = slab - c * g.nz;
+    const int c4 = z / g.nzl, c2 = z - c4 * g.nzl;  // x-row layout [q][c][zl][y][kx]
+    mbar_expect_tx(bar, TX);
+#pragma unroll
+    for (int nb = 0; nb < NBOX; ++nb) tma_load_5d(stage + nb * Y::BR * NCOL, &tin, bar, xt * NCOL, nb * Y::BR, c2, c, c4);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  int t = blockIdx.x;
+  if (threadIdx.x == 0 && t < ntiles) issue(t);
+  struct StageLd {
+    __device__ static constexpr bool kSmem() { return false; }  // not the work tile: no in-place hazard
+    const float2* s;
+    __device__ float2 operator()(int b, int, int ib, int C) const { return s[(ib + C) * NCOL + b]; }
+  };
+  struct St {
+    __device__ static constexpr bool kSmem() { return false; }
+    float2* p;
+    int pitch, ncol_valid;
+    __device__ void operator()(int b, int, int ib, int C, float2 v) const {
+      if (b < ncol_valid) p[b + (ib + C) * pitch] = v;
+    }
+  };
+  using PL = Plan<L, false, 4>;
+  constexpr int IFACE0 = TileIdx<L, NCOL, true, PL::R(0)>::PAD ? kPad : kLin;
+  const ThreadMap<L, NCOL, NT, true> tm;
+  for (int k = 0; t < ntiles; ++k, t += gridDim.x) {
+    mbar_wait(bar, k & 1);
+    const int slab = t / ntx, xt = t - slab * ntx;
+    const int kx0 = xt * NCOL;
+    const St st{out + (size_t)slab * g.Py * g.pitch2 + kx0, g.pitch2, g.Kc - kx0};
+    // pass 0: staged rows (< L/2, the rest is the zero padding) -> work tile
+    fft_pass<L, 0, false, NCOL, NT, true, 1, false, true, false, kExt, IFACE0>(tm, StageLd{stage}, st, work, tw,
+                                                                              g.Lmax / L);
+    __syncthreads();  // the staging buffer is free
+    if (threadIdx.x == 0 && t + (int)gridDim.x < ntiles) {
+      fence_proxy_async();
+      issue(t + gridDim.x);
+    }
+    fft_passes<L, 1, false, NCOL, NT, true, 1, false, true, false, kExt, kExt>(tm, work, StageLd{stage}, st, tw,
+                                                                                g.Lmax / L);
+    __syncthreads();
+  }
+  (void)n_out;
+}
+
 // ---------------------------------------------------------------------------
 // k-space multiply with the CTA's folded KS slice staged in smem:
 // kss[c][kf][b], c = 0..5 (xx xy xz yy yz zz), kf the folded index of the
@@ -1313,8 +1396,26 @@ static cudaError_t ky_tma_launch(const Geom& g, float2* out, const float2* tw, c
   return cudaGetLastError();
 }
 
+template <int L>
+static cudaError_t ky_stage_launch(const Geom& g, float2* out, const float2* tw, cudaStream_t st,
+                                   const TmapBlob* tmap) {
+  using Y = YStage<L>;
+  auto kern = k_y_stage<L>;
+  cudaError_t e = prep(kern, Y::SMEM);
+  if (e != cudaSuccess) return e;
+  const int ntiles = ((g.Kc + Y::NCOL - 1) / Y::NCOL) * 3 * g.nz;
+  const int grid = ntiles < g.nsm ? ntiles : g.nsm;
+  CUtensorMap map;
+  memcpy(&map, tmap->b, sizeof map);
+  GRACE_TRY(launch_k(2, kern, grid, Y::NT, Y::SMEM, st, map, out, tw, g, g.Py));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_k2(const Geom& g, const float2* X1, float2* X2, const float2* tw, cudaStream_t st,
                       const TmapBlob* tmap) {
+#ifndef GRACE_NO_YSTAGE
+  if (tmap != nullptr && g.Py == 4096) return ky_stage_launch<4096>(g, X2, tw, st, tmap);
+#endif
   // The TMA tiles hold GRACE_YT_ELEMS / L columns; below 4 (L >= 4096) K2's row
   // stores are 16-byte half sectors and cost L2 read-modify-writes (block
   // 2048x2048x64: 22.3 ms, 4.6x the input read from DRAM), so K2 takes the
@@ -1375,7 +1476,13 @@ static cudaError_t ky_maps(const Geom& g, const float2* k2_in, const float2* x2,
   const unsigned long long d2[5] = {(unsigned long long)g.Kc, (unsigned long long)g.ny, (unsigned long long)g.nzl, 3,
                                     (unsigned long long)nq};
   const unsigned long long s2[4] = {p1, p1 * g.ny, p1 * g.ny * g.nzl, p1 * g.ny * g.nzl * 3};
-  cudaError_t e = encode5(k2map, k2_in, d2, s2, NCOL, Y::br(false));
+  // K2's map: 4-column boxes for the staged long-pencil kernel (k_y_stage)
+#ifndef GRACE_NO_YSTAGE
+  constexpr int NCOL2 = L == 4096 ? YStage<(L == 4096 ? L : 4096)>::NCOL : NCOL;
+#else
+  constexpr int NCOL2 = NCOL;
+#endif
+  cudaError_t e = encode5(k2map, k2_in, d2, s2, NCOL2, Y::br(false));
   if (e != cudaSuccess) return e;
   const unsigned long long d4[5] = {(unsigned long long)g.Kc, (unsigned long long)g.Py, (unsigned long long)g.nz, 3, 1};
   const unsigned long long s4[4] = {p2, p2 * g.Py, p2 * g.Py * g.nz, p2 * g.Py * g.nz * 3};

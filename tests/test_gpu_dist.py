@@ -25,6 +25,7 @@ CASES = [
     ((7, 5, 6), (1e-9, 2e-9, 1e-9), (2, 3, 6)),
     ((2, 3, 4), (1e-9, 1e-9, 1e-9), (4,)),       # Kx = 3 < 4 ranks: an empty kx block
     ((64, 48, 16), (2e-9, 2e-9, 2e-9), (2, 8)),
+    ((6, 2048, 4), (1e-9, 1e-9, 1e-9), (2,)),    # Py = 4096: staged K2 on the distributed layout
 ]
 
 

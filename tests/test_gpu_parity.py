@@ -98,6 +98,7 @@ HEFF_CASES = [
     ((4, 3, 100), (1e-9, 1e-9, 1e-9), 1e6, 1e-11, 0.0, (0, 0, 0)),     # Pz = 256: K3 4-column tiles
     ((3, 2, 200), (1e-9, 1e-9, 1e-9), 1e6, 1e-11, 0.0, (0, 0, 0)),     # Pz = 512: 8-column tiles
     ((2, 2, 300), (1e-9, 1e-9, 1e-9), 1e6, 1e-11, 0.0, (0, 0, 0)),     # Pz = 1024
+    ((4, 2048, 2), (1e-9, 1e-9, 1e-9), 1e6, 1e-11, 0.0, (0, 0, 0)),    # Py = 4096: staged K2, partial tile
 ]
 
 
