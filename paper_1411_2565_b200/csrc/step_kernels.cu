@@ -302,9 +302,15 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, GRACE_YT_MINB)
 // staged rows into registers and writes the work tile; as soon as every thread
 // is past it, the next tile's TMA load goes into the staging buffer and overlaps
 // the remaining passes.  Twiddles from the global table (no room for smem ones).
+#ifndef GRACE_YSTAGE_2048
+#define GRACE_YSTAGE_2048 8  // columns of the staged K2 at L = 2048 (0: the double-buffered TMA kernel; 0.68 -> 0.61 ms)
+#endif
+#ifndef GRACE_YSTAGE_MINB
+#define GRACE_YSTAGE_MINB 1
+#endif
 template <int L>
 struct YStage {
-  static constexpr int NCOL = 4;
+  static constexpr int NCOL = (L == 2048 && GRACE_YSTAGE_2048) ? GRACE_YSTAGE_2048 : 4;
   using T = TileIdx<L, NCOL, true>;
   static constexpr int WB = ((T::ELEMS * 8 + 1023) / 1024) * 1024;  // work tile bytes
   static constexpr int SB = NCOL * (L / 2) * 8;                       // staging bytes
@@ -314,7 +320,7 @@ struct YStage {
 };
 
 template <int L>
-__global__ void __launch_bounds__(YStage<L>::NT, 1)
+__global__ void __launch_bounds__(YStage<L>::NT, (L == 2048 ? GRACE_YSTAGE_MINB : 1))
     k_y_stage(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, const float2* __restrict__ tw, Geom g,
               int n_out) {
   using Y = YStage<L>;
@@ -1404,7 +1410,8 @@ static cudaError_t ky_stage_launch(const Geom& g, float2* out, const float2* tw,
   cudaError_t e = prep(kern, Y::SMEM);
   if (e != cudaSuccess) return e;
   const int ntiles = ((g.Kc + Y::NCOL - 1) / Y::NCOL) * 3 * g.nz;
-  const int grid = ntiles < g.nsm ? ntiles : g.nsm;
+  const int cap = g.nsm * (L == 2048 ? GRACE_YSTAGE_MINB : 1);
+  const int grid = ntiles < cap ? ntiles : cap;
   CUtensorMap map;
   memcpy(&map, tmap->b, sizeof map);
   GRACE_TRY(launch_k(2, kern, grid, Y::NT, Y::SMEM, st, map, out, tw, g, g.Py));
@@ -1415,6 +1422,7 @@ cudaError_t launch_k2(const Geom& g, const float2* X1, float2* X2, const float2*
                       const TmapBlob* tmap) {
 #ifndef GRACE_NO_YSTAGE
   if (tmap != nullptr && g.Py == 4096) return ky_stage_launch<4096>(g, X2, tw, st, tmap);
+  if (GRACE_YSTAGE_2048 && tmap != nullptr && g.Py == 2048) return ky_stage_launch<2048>(g, X2, tw, st, tmap);
 #endif
   // The TMA tiles hold GRACE_YT_ELEMS / L columns; below 4 (L >= 4096) K2's row
   // stores are 16-byte half sectors and cost L2 read-modify-writes (block
@@ -1478,7 +1486,7 @@ static cudaError_t ky_maps(const Geom& g, const float2* k2_in, const float2* x2,
   const unsigned long long s2[4] = {p1, p1 * g.ny, p1 * g.ny * g.nzl, p1 * g.ny * g.nzl * 3};
   // K2's map: 4-column boxes for the staged long-pencil kernel (k_y_stage)
 #ifndef GRACE_NO_YSTAGE
-  constexpr int NCOL2 = L == 4096 ? YStage<(L == 4096 ? L : 4096)>::NCOL : NCOL;
+  constexpr int NCOL2 = (L == 4096 || (L == 2048 && GRACE_YSTAGE_2048)) ? YStage<(L >= 2048 ? L : 2048)>::NCOL : NCOL;
 #else
   constexpr int NCOL2 = NCOL;
 #endif
