@@ -1,0 +1,54 @@
+"""Per-kernel SASS mnemonic counts of libgrace.so (TMA / bulk copies / async barriers /
+programmatic launch), the evidence table of profiles/r01_sass_evidence.md.
+
+python scripts/sass_evidence.py [libgrace.so] > profiles/rNN_sass_evidence.md
+"""
+import collections
+import re
+import subprocess
+import sys
+
+LIB = sys.argv[1] if len(sys.argv) > 1 else "paper_1411_2565_b200/libgrace.so"
+WATCH = ["UTMALDG", "UTMASTG", "UBLKCP", "SYNCS", "LDGSTS", "UTC", "HMMA", "LDS", "STS", "LDG", "STG", "FFMA",
+         "FADD", "FMUL", "ACQBULK", "PREEXIT"]
+# the instantiations the slab 1024x1024x32 step runs (K1..K6), then SP4's K2' and the setup
+KERNELS = [r"k_x_bulk<1024, true, false>", r"k_y_stage<2048>", r"k3_z<64, 16, 128, 4>", r"k_y_tma<2048, 4, true>",
+           r"k_x_bulk<1024, false, false>", r"k6_llg<true, false, 0>", r"k2f_y_fused<64, ", r"k_octant",
+           r"k_fft64", r"k_diag_partial<false>"]
+
+out = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
+funcs = collections.OrderedDict()
+cur = None
+for ln in out.splitlines():
+    m = re.match(r"\s+Function : (\S+)", ln)
+    if m:
+        dem = subprocess.run(["c++filt", m.group(1)], capture_output=True, text=True).stdout.strip()
+        cur = dem
+        funcs[cur] = collections.Counter()
+        continue
+    if cur is None:
+        continue
+    m = re.match(r"\s+/\*[0-9a-f]+\*/\s+(?:@!?U?P\w+\s+)?([A-Z][A-Z0-9_]*)", ln)
+    if m:
+        funcs[cur][m.group(1)] += 1
+
+print("# SASS evidence (`cuobjdump -sass paper_1411_2565_b200/libgrace.so`, static instruction counts)\n")
+print("sm_100a: TMA tensor loads are `UTMALDG`, 1-D bulk copies `UBLKCP`, mbarrier waits `SYNCS*`, "
+      "programmatic dependent launch `ACQBULK` (griddepcontrol.wait) / `PREEXIT` (launch_dependents); `LDGSTS` is "
+      "cp.async (K3's KS slice).  No tensor-core instructions by design (no dense contraction on this path).  "
+      "Rows: the slab step's kernels (K1 = k_x_bulk<1024, true>, K2 = k_y_stage<2048>, K3 = k3_z<64, ...>, "
+      "K4 = k_y_tma<2048, 4, true>, K5 = k_x_bulk<1024, false>, K6 = k6_llg), SP4's K2', the tensor setup and the "
+      "diagnostics reduction.\n")
+print("| kernel | " + " | ".join(WATCH) + " |")
+print("|---|" + "---|" * len(WATCH))
+seen = collections.Counter()
+for name, c in funcs.items():
+    short = re.sub(r"^void (grace::)?(\(anonymous namespace\)::)?", "", name)
+    key = next((k for k in KERNELS if short.startswith(k) or ("::" + k) in short), None)
+    if key is None or seen[key] >= 1:
+        continue
+    seen[key] += 1
+    row = []
+    for w in WATCH:
+        row.append(str(sum(v for k, v in c.items() if k.startswith(w))))
+    print(f"| `{short[:70]}` | " + " | ".join(row) + " |")
