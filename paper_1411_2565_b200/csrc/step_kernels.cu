@@ -201,13 +201,15 @@ __global__ void __launch_bounds__(NT, MINB) k_y(const float2* __restrict__ in, f
 // of the CTA's next tile lands in the other (mbarrier completion), so HBM reads
 // overlap the radix passes.  Box = {NCOL columns, <= 256 rows}; rows beyond ny
 // (forward) and columns beyond Kc are zero-filled by the TMA unit.
-template <int L, int NCOL>
+template <int L, int NCOL, int NB = 2>
 struct YTma {
   using T = TileIdx<L, NCOL, true>;
   static constexpr int TB = ((T::ELEMS * 8 + 1023) / 1024) * 1024;  // bytes per tile buffer
   using PL = Plan<L, false, 4>;
   static constexpr int TWE = PL::TW_ELEMS > 1 ? PL::TW_ELEMS : 1;
-  static constexpr size_t SMEM = 2 * (size_t)TB + (size_t)TWE * 8 + 64;  // 2 tiles, per-pass twiddles, barriers
+  // NB tile buffers (2: double-buffered; 1: single, latency hidden by 2 CTAs/SM),
+  // per-pass twiddles, barriers
+  static constexpr size_t SMEM = NB * (size_t)TB + (size_t)TWE * 8 + 64;
   static constexpr int NT = NCOL * (L / 16);
   __host__ __device__ static constexpr int rows_in(bool inv) { return inv ? L : L / 2; }
   __host__ __device__ static constexpr int br(bool inv) { return rows_in(inv) < 256 ? rows_in(inv) : 256; }
@@ -216,11 +218,14 @@ struct YTma {
 #ifndef GRACE_YT_MINB
 #define GRACE_YT_MINB 1
 #endif
-template <int L, int NCOL, bool INV>
-__global__ void __launch_bounds__(YTma<L, NCOL>::NT, GRACE_YT_MINB)
+#ifndef GRACE_YT_NB_INV
+#define GRACE_YT_NB_INV 1  // K4 tile buffers per CTA (1: two single-buffered CTAs per SM, 0.596 -> 0.585 ms; 2: double-buffered)
+#endif
+template <int L, int NCOL, bool INV, int NB = 2>
+__global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? 2 : GRACE_YT_MINB)
     k_y_tma(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, const float2* __restrict__ tw, Geom g,
             int n_out) {
-  using Y = YTma<L, NCOL>;
+  using Y = YTma<L, NCOL, NB>;
   constexpr int NT = Y::NT;
   constexpr int ROWS = Y::rows_in(INV);
   constexpr int BR = Y::br(INV);
@@ -229,8 +234,8 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, GRACE_YT_MINB)
   extern __shared__ __align__(1024) unsigned char smraw[];
   // tile buffer k & 1 at smraw + (k & 1) * TB (pointer arithmetic on the shared
   // array keeps every access in the shared address space: LDS/STS, not LD/ST)
-  float2* tws = reinterpret_cast<float2*>(smraw + 2 * Y::TB);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + 2 * Y::TB + Y::TWE * 8);
+  float2* tws = reinterpret_cast<float2*>(smraw + NB * Y::TB);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + NB * Y::TB + Y::TWE * 8);
 #ifdef GRACE_PDL_EARLY
   pdl_trigger();
 #endif
@@ -257,7 +262,7 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, GRACE_YT_MINB)
   __syncthreads();
   pdl_wait();
   int t = blockIdx.x;
-  if (threadIdx.x == 0 && t < ntiles) issue(t, reinterpret_cast<float2*>(smraw), bar);
+  if (NB == 2 && threadIdx.x == 0 && t < ntiles) issue(t, reinterpret_cast<float2*>(smraw), bar);
   struct St {
     __device__ static constexpr bool kSmem() { return false; }
     float2* p;
@@ -275,13 +280,21 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, GRACE_YT_MINB)
   };
   if (t + (int)gridDim.x >= ntiles) pdl_trigger();  // no tile or one tile left
   for (int k = 0; t < ntiles; ++k, t += gridDim.x) {
-    float2* cur = reinterpret_cast<float2*>(smraw + (k & 1) * Y::TB);
+    float2* cur = reinterpret_cast<float2*>(smraw + (NB == 2 ? (k & 1) * Y::TB : 0));
     if (t + (int)gridDim.x < ntiles && t + 2 * (int)gridDim.x >= ntiles) pdl_trigger();  // last tile next
-    if (threadIdx.x == 0 && t + (int)gridDim.x < ntiles) {
-      fence_proxy_async();
-      issue(t + gridDim.x, reinterpret_cast<float2*>(smraw + ((k + 1) & 1) * Y::TB), bar + ((k + 1) & 1));
+    if constexpr (NB == 2) {
+      if (threadIdx.x == 0 && t + (int)gridDim.x < ntiles) {
+        fence_proxy_async();
+        issue(t + gridDim.x, reinterpret_cast<float2*>(smraw + ((k + 1) & 1) * Y::TB), bar + ((k + 1) & 1));
+      }
+      mbar_wait(bar + (k & 1), (k >> 1) & 1);
+    } else {
+      if (threadIdx.x == 0) {
+        fence_proxy_async();
+        issue(t, cur, bar);
+      }
+      mbar_wait(bar, k & 1);
     }
-    mbar_wait(bar + (k & 1), (k >> 1) & 1);
     const int slab = t / ntx, xt = t - slab * ntx;
     const int kx0 = xt * NCOL;
     float2* o = out + (INV ? xrow_slab(g, slab) : (size_t)slab * g.Py * g.pitch2) + kx0;
@@ -1387,12 +1400,14 @@ template <int L, bool INV>
 static cudaError_t ky_tma_launch(const Geom& g, float2* out, const float2* tw, cudaStream_t st, int n_out,
                                  const TmapBlob* tmap) {
   constexpr int NCOL = ytma_ncol<L>();
-  using Y = YTma<L, NCOL>;
-  auto kern = k_y_tma<L, NCOL, INV>;
+  constexpr int NB = (INV && L == 2048) ? GRACE_YT_NB_INV : 2;  // single-buffered slower elsewhere (block K4 27.6 vs 8.0 ms)
+  using Y = YTma<L, NCOL, NB>;
+  auto kern = k_y_tma<L, NCOL, INV, NB>;
   cudaError_t e = prep(kern, Y::SMEM);
   if (e != cudaSuccess) return e;
   const int ntiles = ((g.Kc + NCOL - 1) / NCOL) * 3 * g.nz;
-  const int per_sm = (int)(220 * 1024 / Y::SMEM) < GRACE_YT_MINB ? (int)(220 * 1024 / Y::SMEM) : GRACE_YT_MINB;
+  const int want = NB == 1 ? 2 : GRACE_YT_MINB;
+  const int per_sm = (int)(220 * 1024 / Y::SMEM) < want ? (int)(220 * 1024 / Y::SMEM) : want;
   const int cap = g.nsm * (per_sm > 0 ? per_sm : 1);
   const int grid = ntiles < cap ? ntiles : cap;
   CUtensorMap map;
