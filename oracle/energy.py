@@ -16,17 +16,21 @@ import numpy as np
 from . import MU0
 
 
-def energy(M, demag_op, A, Ms, Ku, d, hext):
+def energy(M, demag_op, A, Ms, Ku, d, hext, mask=None):
+    """mask (reading Q26): sums over magnetic cells and bonds between two of them
+    (M = 0 in empty cells; a bond to an empty cell is dropped)."""
     V = (d[0] * d[1]) * d[2]
     m = M / Ms
+    w = np.ones(M.shape[1:]) if mask is None else (np.asarray(mask) != 0).astype(np.float64)
     e_ex = 0.0
     for arr_axis, delta in ((3, d[0]), (2, d[1]), (1, d[2])):
         n = M.shape[arr_axis]
         if n < 2:
             continue
         diff = np.diff(m, axis=arr_axis)
-        e_ex += A * (diff * diff).sum() / (delta * delta)
-    e_an = Ku * (1.0 - m[0] * m[0]).sum()
+        bond = w.take(range(1, n), axis=arr_axis - 1) * w.take(range(0, n - 1), axis=arr_axis - 1)
+        e_ex += A * ((diff * diff) * bond).sum() / (delta * delta)
+    e_an = Ku * ((1.0 - m[0] * m[0]) * w).sum()
     Hd = demag_op(M)
     e_d = -0.5 * MU0 * (Hd * M).sum()
     e_z = -MU0 * sum(hext[a] * M[a].sum() for a in range(3))

@@ -10,14 +10,20 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
   direction"; field H_an = (2Ku/(mu0 Ms^2)) Mx x (reading Q4).
 * Zeeman: uniform H_ext (reading Q19).
 * H_eff = H_exch + H_anis + H_demag + H_extern, Eq. (2) (1/mu0 per Q3).
+* Geometry mask (the paper's future work "non-regular
+  geometry"; reading Q26): ``mask`` [nz,ny,nx] of 0/1, M = 0 in empty
+  cells.  An exchange bond exists only between two magnetic cells (an empty
+  neighbour is a free surface, like the outer boundary); H_eff is reported as 0
+  in empty cells.
 """
 import numpy as np
 
 from . import MU0
 
 
-def exchange(M, A, Ms, d):
-    """Six-neighbour exchange field with Neumann boundaries. M: [3,nz,ny,nx]."""
+def exchange(M, A, Ms, d, mask=None):
+    """Six-neighbour exchange field with Neumann boundaries. M: [3,nz,ny,nx].
+    mask: bonds only between two cells with mask 1 (Q26)."""
     H = np.zeros_like(M, dtype=np.float64)
     # axis of the [3,nz,ny,nx] array for x, y, z and the matching cell size
     for arr_axis, delta in ((3, d[0]), (2, d[1]), (1, d[2])):
@@ -31,6 +37,8 @@ def exchange(M, A, Ms, d):
         lo, hi = tuple(lo), tuple(hi)
         c = 2.0 * A / (MU0 * Ms * Ms) / (delta * delta)
         diff = M[hi] - M[lo]  # M(r+e) - M(r) on the lower cell of each bond
+        if mask is not None:
+            diff = diff * (mask[hi[1:]] * mask[lo[1:]])  # no bond to an empty cell
         H[lo] += c * diff
         H[hi] -= c * diff
     return H
@@ -50,9 +58,10 @@ def zeeman(M, hext):
     return H
 
 
-def heff(M, demag_op, A, Ms, Ku, d, hext):
-    """Eq. (2): H_eff = H_exch + H_anis + H_demag + H_extern."""
-    return exchange(M, A, Ms, d) + anisotropy(M, Ku, Ms) + demag_op(M) + zeeman(M, hext)
+def heff(M, demag_op, A, Ms, Ku, d, hext, mask=None):
+    """Eq. (2): H_eff = H_exch + H_anis + H_demag + H_extern (0 in empty cells, Q26)."""
+    H = exchange(M, A, Ms, d, mask) + anisotropy(M, Ku, Ms) + demag_op(M) + zeeman(M, hext)
+    return H if mask is None else H * mask
 
 
 def schedule_amplitude(k, start, decay, stop):

@@ -12,6 +12,8 @@ used as written (no small-alpha expansion).
 (P:L55): M* = M + dt dM/dt(M, H_eff(M)), with H_eff evaluated once at the
 pre-step M (reading Q17), then M <- Ms M*/|M*| (reading Q16).
 A non-finite result aborts with the step index and cell.
+With a geometry mask (reading Q26) only magnetic cells are stepped and
+renormalised; empty cells keep M = 0, and <m> averages over magnetic cells.
 """
 import numpy as np
 
@@ -34,17 +36,23 @@ def llg_rhs(M, H, alpha, gamma0, Ms):
     return -a * MxH - (alpha * a / Ms) * MxMxH
 
 
-def renormalize(M, Ms):
-    """Scale every cell to |M| = Ms."""
+def renormalize(M, Ms, mask=None):
+    """Scale every cell to |M| = Ms; empty cells (mask 0) stay 0 (Q26)."""
     n = np.sqrt(M[0] * M[0] + M[1] * M[1] + M[2] * M[2])
-    return Ms * M / n
+    if mask is None:
+        return Ms * M / n
+    return np.where(mask > 0, Ms * M / np.where(mask > 0, n, 1.0), 0.0)
 
 
 class Sim:
     """State + parameters of one fp64 run (the oracle twin of a grace context)."""
 
-    def __init__(self, M, demag_op, Ms, A, Ku, alpha, gamma0, d, hext=(0.0, 0.0, 0.0), schedule=None):
+    def __init__(self, M, demag_op, Ms, A, Ku, alpha, gamma0, d, hext=(0.0, 0.0, 0.0), schedule=None, mask=None):
+        # geometry mask [nz,ny,nx] of 0/1 (Q26): M = 0 in empty cells
+        self.mask = None if mask is None else (np.asarray(mask) != 0).astype(np.float64)
         self.M = np.array(M, dtype=np.float64)
+        if self.mask is not None:
+            self.M = self.M * self.mask
         self.demag = demag_op
         self.Ms, self.A, self.Ku = Ms, A, Ku
         self.alpha, self.gamma0 = alpha, gamma0
@@ -65,12 +73,12 @@ class Sim:
 
     def heff(self, M=None):
         M = self.M if M is None else M
-        return _heff(M, self.demag, self.A, self.Ms, self.Ku, self.d, self.field())
+        return _heff(M, self.demag, self.A, self.Ms, self.Ku, self.d, self.field(), self.mask)
 
     def euler_step(self, dt):
         H = self.heff()
         Mstar = self.M + dt * llg_rhs(self.M, H, self.alpha, self.gamma0, self.Ms)
-        Mn = renormalize(Mstar, self.Ms)
+        Mn = renormalize(Mstar, self.Ms, self.mask)
         bad = ~np.isfinite(Mn).all(axis=0)
         if bad.any():
             raise NonFinite(self.step_count, int(np.flatnonzero(bad.ravel())[0]))
@@ -84,13 +92,13 @@ class Sim:
             f0 = rhs(M, H(M, t_k));  M* = renorm(M + dt f0)
             f1 = rhs(M*, H(M*, t_{k+1}));  M' = renorm(M + dt (f0 + f1) / 2)."""
         f0 = llg_rhs(self.M, self.heff(), self.alpha, self.gamma0, self.Ms)
-        Mstar = renormalize(self.M + dt * f0, self.Ms)
+        Mstar = renormalize(self.M + dt * f0, self.Ms, self.mask)
         k = self.step_count
         self.step_count = k + 1  # the corrector's field is the next timestep's
         H1 = self.heff(Mstar)
         self.step_count = k
         f1 = llg_rhs(Mstar, H1, self.alpha, self.gamma0, self.Ms)
-        Mn = renormalize(self.M + (0.5 * dt) * (f0 + f1), self.Ms)
+        Mn = renormalize(self.M + (0.5 * dt) * (f0 + f1), self.Ms, self.mask)
         bad = ~np.isfinite(Mn).all(axis=0)
         if bad.any():
             raise NonFinite(self.step_count, int(np.flatnonzero(bad.ravel())[0]))
@@ -103,5 +111,6 @@ class Sim:
             step(dt)
 
     def mavg(self):
-        """<M>/Ms, summed in fixed (C) order (S:L94)."""
-        return np.array([self.M[a].sum() for a in range(3)]) / (self.M[0].size * self.Ms)
+        """<M>/Ms, summed in fixed (C) order, over the magnetic cells (Q26)."""
+        ncell = self.M[0].size if self.mask is None else self.mask.sum()
+        return np.array([self.M[a].sum() for a in range(3)]) / (ncell * self.Ms)

@@ -91,3 +91,27 @@ def uniform_m(n, Ms, direction):
     for a in range(3):
         M[a] = Ms * u[a]
     return M
+
+
+def ellipse_mask(n, hole=True):
+    """Non-regular geometry: an elliptical disc
+    inscribed in the nx x ny plane, extruded through z, optionally with an
+    off-centre circular hole (antidot).  uint8 [nz, ny, nx]."""
+    nx, ny, nz = n
+    y, x = np.mgrid[0:ny, 0:nx]
+    u = (x + 0.5 - nx / 2) / (nx / 2)
+    v = (y + 0.5 - ny / 2) / (ny / 2)
+    m = (u * u + v * v) <= 1.0
+    if hole:
+        hu = (x + 0.5 - 0.6 * nx) / (0.12 * nx)
+        hv = (y + 0.5 - 0.45 * ny) / (0.12 * nx)
+        m &= (hu * hu + hv * hv) > 1.0
+    return np.broadcast_to(m, (nz, ny, nx)).astype(np.uint8).copy()
+
+
+def box_mask(n, lo, size):
+    """uint8 [nz, ny, nx] mask of the box of `size` (sx, sy, sz) cells at corner `lo`."""
+    nx, ny, nz = n
+    m = np.zeros((nz, ny, nx), dtype=np.uint8)
+    m[lo[2]:lo[2] + size[2], lo[1]:lo[1] + size[1], lo[0]:lo[0] + size[0]] = 1
+    return m
