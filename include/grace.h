@@ -141,6 +141,19 @@ int grace_set_field_schedule(grace_ctx *h, double h0x, double h0y, double h0z, l
  * GRACE_EUNSUPPORTED with GRACE_K5_FUSED=1 or in profiling mode. */
 int grace_set_integrator(grace_ctx *h, int kind);
 
+/* Geometry mask (the paper's "non-regular geometry", P:L121;
+ * DESIGN.md reading Q26).  mask: host uint8 [nz][ny][nx] (the rank-local slab
+ * [nz/P][ny][nx] for grace_create_dist), nonzero = magnetic cell, copied before
+ * return; NULL removes the mask.  Empty cells hold M = 0 (they carry no magnetic
+ * charge in the demag sum); an exchange bond exists only between two magnetic
+ * cells (an empty neighbour is a free surface, like the outer boundary);
+ * grace_heff reports 0 in empty cells; grace_step leaves them at 0; grace_mavg and
+ * grace_energy sum over magnetic cells.  The current M is zeroed in empty cells;
+ * grace_set_m afterwards ignores the input there (cells newly made magnetic need
+ * a grace_set_m).  GRACE_EINVAL if no cell is magnetic, GRACE_EUNSUPPORTED with
+ * GRACE_K5_FUSED=1.  Costs Nl bytes of device memory per rank. */
+int grace_set_geometry(grace_ctx *h, const unsigned char *mask);
+
 /* Steps taken so far (t = steps * dt). */
 int grace_step_count(grace_ctx *h, long long *steps);
 

@@ -63,6 +63,7 @@ SIGNATURES = [
     ("grace_nccl_unique_id", _I, [_P]),
     ("grace_create_dist", _I, [_I, _I, _I, _D, _D, _D, _D, _D, _D, _D, _D, _I, _I, _P, ctypes.POINTER(_P)]),
     ("grace_partition", _I, [_P, _PLL]),
+    ("grace_set_geometry", _I, [_P, _P]),
 ]
 
 _lib = None
@@ -190,6 +191,10 @@ def grace_last_error():
 
 def grace_set_alpha(h, alpha):
     _check(load().grace_set_alpha(h, alpha))
+
+
+def grace_set_geometry(h, mask_ptr):
+    _check(load().grace_set_geometry(h, _P(mask_ptr) if mask_ptr else None))
 
 
 def grace_set_stream(h, stream_ptr):
@@ -359,6 +364,16 @@ class Grace:
     def set_field_schedule(self, h0, start, decay, stop):
         """Paper/SPEC field schedule: + a(k) h0 (A/m) on top of set_hext's field."""
         grace_set_field_schedule(self.h, h0, start, decay, stop)
+
+    def set_geometry(self, mask):
+        """Geometry mask uint8/bool [nz, ny, nx] (nonzero = magnetic; None removes it)."""
+        if mask is None:
+            grace_set_geometry(self.h, None)
+            return
+        m = np.ascontiguousarray(np.asarray(mask) != 0, dtype=np.uint8)
+        if m.size != int(np.prod(self.shape[1:])):
+            raise ValueError(f"mask of {m.size} cells for a grid of {int(np.prod(self.shape[1:]))}")
+        grace_set_geometry(self.h, m.ctypes.data)
 
     def set_integrator(self, kind):
         """'euler' (the paper's, default) or 'heun' (second order, two H_eff per step)."""

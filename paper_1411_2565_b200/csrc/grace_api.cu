@@ -136,6 +136,7 @@ struct Rank {
   float* Hbuf = nullptr;
   float* Hd = nullptr;                 // H_demag [3][nzl][ny][nx] (split K5/K6 step)
   float* F = nullptr;                  // Heun: dM/dt of the predictor stage
+  unsigned char* mask = nullptr;       // geometry mask [nzl][ny][nx] (grace_set_geometry; null: none)
   bool tma = false;                    // TMA descriptors of the K2 / K4 inputs built
   TmapBlob k2map{}, k4map{};
 };
@@ -153,6 +154,7 @@ struct grace_ctx {
   long long steps = 0;
   long long nf_step = -1, nf_cell = -1;
   long long N = 0;  // cells addressed by set_m/get_m/heff (whole grid, or the local slab in nccl mode)
+  double nmag = 0;  // magnetic cells of the whole grid under the geometry mask (0: no mask)
   int cur = 0;
   bool fused = false;
   Geom g0{};  // global geometry
@@ -389,7 +391,7 @@ struct grace_ctx {
     for (auto e : ev) cudaEventDestroy(e);
     for (auto& rk : ranks) {
       void* ptrs[] = {rk.M[0], rk.M[1], rk.A,   rk.B,    rk.X2,  rk.KS,   rk.Hlo,
-                      rk.Hhi,  rk.prm,  rk.flag, rk.red, rk.Hbuf, rk.Hd,  rk.dred, rk.F};
+                      rk.Hhi,  rk.prm,  rk.flag, rk.red, rk.Hbuf, rk.Hd,  rk.dred, rk.F, rk.mask};
       for (void* p : ptrs)
         if (p) cudaFree(p);
     }
@@ -712,7 +714,7 @@ int grace_set_m(grace_ctx* h, const double* m) {
     for (int c = 0; c < 3; ++c)
       CUDA_OR(cudaMemcpyAsync(stage + c * rk.Nl, m + c * h->N + off, sizeof(double) * rk.Nl, cudaMemcpyHostToDevice,
                               h->stream));
-    CUDA_OR(launch_set_m_f64(stage, rk.M[target], rk.Nl, h->Ms, rk.flag + 1, h->stream));
+    CUDA_OR(launch_set_m_f64(stage, rk.M[target], rk.Nl, h->Ms, rk.mask, rk.flag + 1, h->stream));
   }
   return finish_set_m(h, target);
 }
@@ -722,14 +724,14 @@ int grace_set_m_device(grace_ctx* h, const float* d_m) {
   const int target = 1 - h->cur;
   for (auto& rk : h->ranks) {
     if (h->mode != grace_ctx::kVirtual) {
-      CUDA_OR(launch_set_m_f32(d_m, rk.M[target], rk.Nl, (float)h->Ms, rk.flag + 1, h->stream));
+      CUDA_OR(launch_set_m_f32(d_m, rk.M[target], rk.Nl, (float)h->Ms, rk.mask, rk.flag + 1, h->stream));
     } else {
       float* stage = reinterpret_cast<float*>(rk.A);
       const size_t off = slab_offset(h, rk);
       for (int c = 0; c < 3; ++c)
         CUDA_OR(cudaMemcpyAsync(stage + c * rk.Nl, d_m + c * h->N + off, sizeof(float) * rk.Nl,
                                 cudaMemcpyDeviceToDevice, h->stream));
-      CUDA_OR(launch_set_m_f32(stage, rk.M[target], rk.Nl, (float)h->Ms, rk.flag + 1, h->stream));
+      CUDA_OR(launch_set_m_f32(stage, rk.M[target], rk.Nl, (float)h->Ms, rk.mask, rk.flag + 1, h->stream));
     }
   }
   return finish_set_m(h, target);
@@ -805,6 +807,59 @@ int grace_set_integrator(grace_ctx* h, int kind) {
     h->g1[c] = h->gc[c] = nullptr;
   }
   h->integrator = kind;
+  return GRACE_OK;
+}
+
+int grace_set_geometry(grace_ctx* h, const unsigned char* mask) {
+  if (!h) return fail(GRACE_EINVAL, "NULL context");
+  if (mask && !h->g0.split_llg)
+    return fail(GRACE_EUNSUPPORTED, "a geometry mask needs the split K5/K6 step (GRACE_K5_FUSED unset)");
+  double local = 0;
+  if (mask) {
+    for (auto& rk : h->ranks) {
+      const size_t off = slab_offset(h, rk);
+      for (long long i = 0; i < rk.Nl; ++i) local += mask[off + i] ? 1.0 : 0.0;
+    }
+    double total = local;
+    if (h->mode == grace_ctx::kNccl) {  // magnetic cells of the whole grid
+      Rank& rk = h->ranks[0];
+      double* d = rk.red + kMavgPartials;
+      CUDA_OR(cudaMemcpyAsync(d, &local, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+      const ncclResult_t r = g_nccl.allReduce(d, d, 1, kNcclFloat64, kNcclSum, h->comm, h->stream);
+      if (r != 0) return fail(GRACE_ECUDA, "ncclAllReduce: %s", g_nccl.errStr(r));
+      CUDA_OR(cudaMemcpyAsync(&total, d, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+      CUDA_OR(cudaStreamSynchronize(h->stream));
+    }
+    if (!(total > 0)) return fail(GRACE_EINVAL, "geometry mask selects no cell");
+    for (auto& rk : h->ranks) {
+      if (!rk.mask) {
+        int rc = h->alloc((void**)&rk.mask, (size_t)rk.Nl);
+        if (rc) return rc;
+      }
+      CUDA_OR(cudaMemcpyAsync(rk.mask, mask + slab_offset(h, rk), (size_t)rk.Nl, cudaMemcpyHostToDevice, h->stream));
+      // empty cells of the current M become 0 (magnetic cells keep their value)
+      CUDA_OR(launch_apply_mask(rk.M[h->cur], rk.Nl, rk.mask, h->stream));
+      rk.g.masked = 1;
+    }
+    h->nmag = total;
+  } else {
+    for (auto& rk : h->ranks) {
+      if (rk.mask) {
+        cudaFree(rk.mask);
+        h->bytes -= (size_t)rk.Nl;
+      }
+      rk.mask = nullptr;
+      rk.g.masked = 0;
+    }
+    h->nmag = 0;
+  }
+  CUDA_OR(cudaStreamSynchronize(h->stream));
+  h->g0.masked = mask ? 1 : 0;
+  for (int c = 0; c < 2; ++c) {  // captured step graphs carry the old K6 instantiation
+    if (h->g1[c]) cudaGraphExecDestroy(h->g1[c]);
+    if (h->gc[c]) cudaGraphExecDestroy(h->gc[c]);
+    h->g1[c] = h->gc[c] = nullptr;
+  }
   return GRACE_OK;
 }
 
@@ -933,7 +988,9 @@ int grace_mavg(grace_ctx* h, double* out3) {
     std::memcpy(part, h->pin->red, sizeof part);
     for (int q = 0; q < 3; ++q) acc[q] += part[q];
   }
-  for (int q = 0; q < 3; ++q) out3[q] = acc[q] / h->P;  // equal slabs: mean of the slab means
+  // equal slabs: mean of the slab means; with a geometry mask, over magnetic cells (reading Q26)
+  const double scale = h->nmag > 0 ? (double)h->g0.nx * h->g0.ny * h->g0.nz / h->nmag : 1.0;
+  for (int q = 0; q < 3; ++q) out3[q] = acc[q] / h->P * scale;
   return GRACE_OK;
 }
 

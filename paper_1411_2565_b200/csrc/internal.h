@@ -54,6 +54,7 @@ struct Geom {
   int has_lo, has_hi;  // z-1 / z+1 halo planes present
   int nsm;             // SMs of the device (persistent grids)
   int split_llg;       // 1: K5 stores H_demag and K6 does the local terms + update (streaming)
+  int masked;          // geometry mask set (grace_set_geometry): M = 0 marks an empty cell (reading Q26)
   float cx, cy, cz; // exchange 2A/(mu0 Ms^2 d^2) per axis (0 for a singleton axis)
   float ck;         // anisotropy 2Ku/(mu0 Ms^2)
   float Ms;
@@ -93,9 +94,12 @@ int kernel_count(const Geom& g);   // kernels per step
 
 // Utilities (step_kernels.cu).
 cudaError_t launch_twiddles(float2* tw, int Lmax, cudaStream_t st);
-cudaError_t launch_set_m_f64(const double* src, float* M, long long n, double Ms, unsigned long long* flag,
+cudaError_t launch_set_m_f64(const double* src, float* M, long long n, double Ms, const unsigned char* mask,
+                             unsigned long long* flag,
                              cudaStream_t st);
-cudaError_t launch_set_m_f32(const float* src, float* M, long long n, float Ms, unsigned long long* flag,
+cudaError_t launch_apply_mask(float* M, long long n, const unsigned char* mask, cudaStream_t st);
+cudaError_t launch_set_m_f32(const float* src, float* M, long long n, float Ms, const unsigned char* mask,
+                             unsigned long long* flag,
                              cudaStream_t st);
 cudaError_t launch_mavg(const float* M, long long n, double Ms, double* partial, double* out, cudaStream_t st);
 constexpr int kMavgPartials = 3 * 296;

@@ -1084,7 +1084,10 @@ __global__ void __launch_bounds__(XBulk<L>::NT, 1)
 // HEUN = 3: predictor (also stores f = dM/dt into Hout); HEUN = 4: corrector,
 // M' = renorm(M0 + dt (f0 + f(M*)) / 2) with M0 = Mn (updated in place), f0 = Hout,
 // M* = M; the applied field of the next timestep.  HEUN = 0: modes 0 / 1.
-template <bool VEC, bool DIST, int HEUN = 0>
+// MASK (geometry mask, reading Q26): a cell with M = 0 is empty; an empty
+// neighbour is a free surface (replaced by the centre, like a missing one), an
+// empty centre stays 0 (H_eff 0, f 0).
+template <bool VEC, bool DIST, int HEUN = 0, bool MASK = false>
 __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __restrict__ Hd, const float* __restrict__ M,
                                               float* __restrict__ Mn, float* __restrict__ Hout, Geom g,
                                               const StepParams* __restrict__ prm, unsigned long long* __restrict__ flag,
@@ -1135,12 +1138,35 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
     xl[c] = __ldg(mc + ixl);
     xr[c] = __ldg(mc + ixr);
   }
+  bool ea[W], exl = false, exr = false;
+  if constexpr (MASK) {
+    auto empty = [](float u, float v, float w) { return u == 0.f && v == 0.f && w == 0.f; };
+    exl = empty(xl[0], xl[1], xl[2]);
+    exr = empty(xr[0], xr[1], xr[2]);
+#pragma unroll
+    for (int s = 0; s < W; ++s) {
+      ea[s] = empty(a[0][s], a[1][s], a[2][s]);
+      const bool e0 = empty(ym[0][s], ym[1][s], ym[2][s]), e1 = empty(yp[0][s], yp[1][s], yp[2][s]);
+      const bool e2 = empty(zm[0][s], zm[1][s], zm[2][s]), e3 = empty(zp[0][s], zp[1][s], zp[2][s]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if (e0) ym[c][s] = a[c][s];
+        if (e1) yp[c][s] = a[c][s];
+        if (e2) zm[c][s] = a[c][s];
+        if (e3) zp[c][s] = a[c][s];
+      }
+    }
+  }
   float m[3][W], h[3][W];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
 #pragma unroll
     for (int s = 0; s < W; ++s) {
-      const float l = s > 0 ? a[c][s - 1] : xl[c], r = s + 1 < W ? a[c][s + 1] : xr[c];
+      float l = s > 0 ? a[c][s - 1] : xl[c], r = s + 1 < W ? a[c][s + 1] : xr[c];
+      if constexpr (MASK) {
+        if (s > 0 ? ea[s - 1] : exl) l = a[c][s];
+        if (s + 1 < W ? ea[s + 1] : exr) r = a[c][s];
+      }
       // Eq. (2): H_demag + six-neighbour exchange (difference form, Q11) + Zeeman (+ x anisotropy)
       float e = 0.f;
       e += cxyz[0] * (l - a[c][s]);
@@ -1165,6 +1191,16 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
   }
 #pragma unroll
   for (int s = 0; s < W; ++s) {
+    if constexpr (MASK) {
+      if (ea[s]) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          o[c][s] = 0.f;
+          if constexpr (HEUN == 3) f[c][s] = 0.f;
+        }
+        continue;
+      }
+    }
     if (HEUN == 0 && mode == 1) {
       for (int c = 0; c < 3; ++c) o[c][s] = h[c][s];
       continue;
@@ -1544,7 +1580,7 @@ cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* 
 bool fused_y_path(const Geom& g) { return g.Pz == 1 && g.Py <= 512; }
 int kernel_count(const Geom& g) { return (fused_y_path(g) ? 3 : 5) + (g.split_llg ? 1 : 0); }
 
-template <int HEUN>
+template <int HEUN, bool MASK>
 static cudaError_t k6_launch(const Geom& g, int mode, const float* Hd, const float* M, float* Mn, float* Hout,
                              const StepParams* prm, unsigned long long* flag, cudaStream_t st, const float* Hlo,
                              const float* Hhi) {
@@ -1553,11 +1589,11 @@ static cudaError_t k6_launch(const Geom& g, int mode, const float* Hd, const flo
   const long long threads = vec ? N / 4 : N;
   const unsigned grid = (unsigned)((threads + 255) / 256);
   if (vec) {
-    if (g.kb) GRACE_TRY(launch_k(32, k6_llg<true, true, HEUN>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
-    else GRACE_TRY(launch_k(32, k6_llg<true, false, HEUN>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
+    if (g.kb) GRACE_TRY(launch_k(32, k6_llg<true, true, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
+    else GRACE_TRY(launch_k(32, k6_llg<true, false, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
   } else {
-    if (g.kb) GRACE_TRY(launch_k(32, k6_llg<false, true, HEUN>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
-    else GRACE_TRY(launch_k(32, k6_llg<false, false, HEUN>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
+    if (g.kb) GRACE_TRY(launch_k(32, k6_llg<false, true, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
+    else GRACE_TRY(launch_k(32, k6_llg<false, false, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
   }
   return cudaGetLastError();
 }
@@ -1567,9 +1603,14 @@ static cudaError_t k6_launch(const Geom& g, int mode, const float* Hd, const flo
 cudaError_t launch_k6(const Geom& g, int mode, const float* Hd, const float* M, float* Mn, float* Hout,
                       const StepParams* prm, unsigned long long* flag, cudaStream_t st, const float* Hlo,
                       const float* Hhi) {
-  if (mode == 3) return k6_launch<3>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
-  if (mode == 4) return k6_launch<4>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
-  return k6_launch<0>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
+  if (g.masked) {  // geometry mask (reading Q26)
+    if (mode == 3) return k6_launch<3, true>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
+    if (mode == 4) return k6_launch<4, true>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
+    return k6_launch<0, true>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
+  }
+  if (mode == 3) return k6_launch<3, false>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
+  if (mode == 4) return k6_launch<4, false>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
+  return k6_launch<0, false>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
 }
 
 template <int L>
@@ -1645,10 +1686,15 @@ cudaError_t launch_twiddles(float2* tw, int Lmax, cudaStream_t st) {
 }
 
 // grace_set_m: M <- Ms M/|M| per cell (fp64 input, fp32 output); a zero or
-// non-finite cell records its index.
+// non-finite cell records its index.  With a geometry mask, empty
+// cells (mask 0) get M = 0 whatever the input (reading Q26).
 __global__ void k_set_m_f64(const double* __restrict__ src, float* __restrict__ M, long long n, double Ms,
-                            unsigned long long* flag) {
+                            const unsigned char* __restrict__ mask, unsigned long long* flag) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    if (mask && !mask[i]) {
+      M[i] = M[n + i] = M[2 * n + i] = 0.f;
+      continue;
+    }
     const double x = src[i], y = src[n + i], z = src[2 * n + i];
     const double r = sqrt(x * x + y * y + z * z);
     if (!(r > 0.0) || !isfinite(r)) {
@@ -1663,8 +1709,12 @@ __global__ void k_set_m_f64(const double* __restrict__ src, float* __restrict__ 
 }
 
 __global__ void k_set_m_f32(const float* __restrict__ src, float* __restrict__ M, long long n, float Ms,
-                            unsigned long long* flag) {
+                            const unsigned char* __restrict__ mask, unsigned long long* flag) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    if (mask && !mask[i]) {
+      M[i] = M[n + i] = M[2 * n + i] = 0.f;
+      continue;
+    }
     const float x = src[i], y = src[n + i], z = src[2 * n + i];
     const float r = sqrtf(x * x + y * y + z * z);
     if (!(r > 0.f) || !isfinite(r)) {
@@ -1678,14 +1728,24 @@ __global__ void k_set_m_f32(const float* __restrict__ src, float* __restrict__ M
   }
 }
 
-cudaError_t launch_set_m_f64(const double* src, float* M, long long n, double Ms, unsigned long long* flag,
-                             cudaStream_t st) {
-  k_set_m_f64<<<148 * 8, 256, 0, st>>>(src, M, n, Ms, flag);
+cudaError_t launch_set_m_f64(const double* src, float* M, long long n, double Ms, const unsigned char* mask,
+                             unsigned long long* flag, cudaStream_t st) {
+  k_set_m_f64<<<148 * 8, 256, 0, st>>>(src, M, n, Ms, mask, flag);
   return cudaGetLastError();
 }
-cudaError_t launch_set_m_f32(const float* src, float* M, long long n, float Ms, unsigned long long* flag,
-                             cudaStream_t st) {
-  k_set_m_f32<<<148 * 8, 256, 0, st>>>(src, M, n, Ms, flag);
+cudaError_t launch_set_m_f32(const float* src, float* M, long long n, float Ms, const unsigned char* mask,
+                             unsigned long long* flag, cudaStream_t st) {
+  k_set_m_f32<<<148 * 8, 256, 0, st>>>(src, M, n, Ms, mask, flag);
+  return cudaGetLastError();
+}
+
+// grace_set_geometry: M <- 0 in the empty cells of the mask (reading Q26).
+__global__ void k_apply_mask(float* __restrict__ M, long long n, const unsigned char* __restrict__ mask) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    if (!mask[i]) M[i] = M[n + i] = M[2 * n + i] = 0.f;
+}
+cudaError_t launch_apply_mask(float* M, long long n, const unsigned char* mask, cudaStream_t st) {
+  k_apply_mask<<<148 * 8, 256, 0, st>>>(M, n, mask);
   return cudaGetLastError();
 }
 
@@ -1760,6 +1820,12 @@ __global__ void k_diag_partial(const float* __restrict__ M, const float* __restr
       nb[3][c] = y + 1 < g.ny ? M[c * n + i + g.nx] : a[c];
       nb[4][c] = zl > 0 ? M[c * n + i - plane] : ((DIST && g.has_lo) ? Hlo[c * plane + ip] : a[c]);
       nb[5][c] = zl + 1 < g.nzl ? M[c * n + i + plane] : ((DIST && g.has_hi) ? Hhi[c * plane + ip] : a[c]);
+    }
+    if (g.masked) {  // reading Q26: skip empty cells; an empty neighbour is a free surface
+      if (a[0] == 0.f && a[1] == 0.f && a[2] == 0.f) continue;
+      for (int k = 0; k < 6; ++k)
+        if (nb[k][0] == 0.f && nb[k][1] == 0.f && nb[k][2] == 0.f)
+          for (int c = 0; c < 3; ++c) nb[k][c] = a[c];
     }
     // bonds to the +x, +y, +z neighbours (a missing neighbour adds nothing)
     const double w[3] = {idx2, idy2, idz2};
