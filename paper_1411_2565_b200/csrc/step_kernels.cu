@@ -927,9 +927,15 @@ struct XbSt {
   }
 };
 
+#ifndef GRACE_XB_ELEMS
+#define GRACE_XB_ELEMS 8192  // complex values per x tile (8192: 512 threads at 16 elements each)
+#endif
+#ifndef GRACE_XB_MINB
+#define GRACE_XB_MINB 1  // resident x-kernel CTAs per SM
+#endif
 template <int L>
 struct XBulk {
-  static constexpr int RB = 8192 / L;  // rows per tile: 512 threads at 16 elements each
+  static constexpr int RB = GRACE_XB_ELEMS / L > 0 ? GRACE_XB_ELEMS / L : 1;  // rows per tile
   static constexpr int NT = RB * (L / 16);
   using T = TileIdx<L, RB, false>;
   static constexpr int TB = ((T::ELEMS * 8 + 1023) / 1024) * 1024;
@@ -941,7 +947,7 @@ struct XBulk {
 constexpr int kXBulkMinL = 64, kXBulkMaxL = 4096;
 
 template <int L, bool FWD, bool DIST>
-__global__ void __launch_bounds__(XBulk<L>::NT, 1)
+__global__ void __launch_bounds__(XBulk<L>::NT, GRACE_XB_MINB)
     k_x_bulk(const void* __restrict__ in, void* __restrict__ out, const float2* __restrict__ tw, Geom g,
              StepParams* bump) {
   using X = XBulk<L>;
@@ -1370,7 +1376,8 @@ static cudaError_t xbulk_launch(const Geom& g, const void* in, void* out, const 
   cudaError_t e = prep(kern, X::SMEM);
   if (e != cudaSuccess) return e;
   const int ntiles = (3 * g.nzl * g.ny + X::RB - 1) / X::RB;
-  const int grid = ntiles < g.nsm ? ntiles : g.nsm;
+  const int cap = g.nsm * GRACE_XB_MINB;
+  const int grid = ntiles < cap ? ntiles : cap;
   GRACE_TRY(launch_k(FWD ? 1 : 16, kern, grid, X::NT, X::SMEM, st, in, out, tw, g, bump));
   return cudaGetLastError();
 }
