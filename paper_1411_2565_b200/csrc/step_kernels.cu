@@ -928,10 +928,10 @@ struct XbSt {
 };
 
 #ifndef GRACE_XB_ELEMS
-#define GRACE_XB_ELEMS 8192  // complex values per x tile (8192: 512 threads at 16 elements each)
+#define GRACE_XB_ELEMS 2048  // complex values per x tile (L = 1024: 2 rows, 128 threads at 16 elements each)
 #endif
 #ifndef GRACE_XB_MINB
-#define GRACE_XB_MINB 1  // resident x-kernel CTAs per SM
+#define GRACE_XB_MINB 4  // resident x-kernel CTAs per SM (scripts/sweep_x2.sh: 8192 x 1 -> 2048 x 4: slab K1 0.348 -> 0.288, K5 0.296 -> 0.275 ms; SP4 19.3 -> 11.3 us/step)
 #endif
 template <int L>
 struct XBulk {
@@ -1376,7 +1376,9 @@ static cudaError_t xbulk_launch(const Geom& g, const void* in, void* out, const 
   cudaError_t e = prep(kern, X::SMEM);
   if (e != cudaSuccess) return e;
   const int ntiles = (3 * g.nzl * g.ny + X::RB - 1) / X::RB;
-  const int cap = g.nsm * GRACE_XB_MINB;
+  int per_sm = 0;  // resident CTAs per SM (shared memory may allow fewer than GRACE_XB_MINB)
+  GRACE_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, X::NT, X::SMEM));
+  const int cap = g.nsm * (per_sm < 1 ? 1 : (per_sm < GRACE_XB_MINB ? per_sm : GRACE_XB_MINB));
   const int grid = ntiles < cap ? ntiles : cap;
   GRACE_TRY(launch_k(FWD ? 1 : 16, kern, grid, X::NT, X::SMEM, st, in, out, tw, g, bump));
   return cudaGetLastError();

@@ -133,3 +133,31 @@ def test_nccl_path_one_rank_matches_single(monkeypatch):
     np.testing.assert_allclose(ea, eb, rtol=1e-9, atol=0)
     pb.grace_destroy(h)
     ref.close()
+
+
+def test_nccl_path_one_rank_masked_matches_single(monkeypatch):
+    """Geometry mask (reading Q26) on the NCCL path: the magnetic-cell count is
+    all-reduced over the communicator for <m>; one rank = the single context."""
+    from workloads import ellipse_mask
+
+    monkeypatch.setenv("GRACE_FORCE_NCCL", "1")
+    n, d, Ms = (48, 20, 6), (2e-9, 2e-9, 3e-9), 8e5
+    M = random_m(n, Ms, seed=54)
+    mask = ellipse_mask(n)
+    h = pb.grace_create_dist(*n, *d, Ms, 1.3e-11, 2e4, 0.3, GAMMA0, 0, 1, pb.grace_nccl_unique_id())
+    ref = pb.Grace(n, d, Ms, 1.3e-11, 2e4, 0.3, GAMMA0)
+    out = []
+    for hh in (h, ref.h):
+        pb.grace_set_geometry(hh, mask.ctypes.data)
+        pb.grace_set_m(hh, M.ravel().copy())
+        pb.grace_step(hh, 5, 2e-14)
+        Mo = np.empty(3 * M[0].size)
+        pb.grace_get_m(hh, Mo)
+        out.append((Mo, pb.grace_mavg(hh), pb.grace_energy(hh)))
+    (Ma, ma, ea), (Mb, mb, eb) = out
+    assert np.abs(Ma - Mb).max() <= 1e-6 * Ms
+    assert np.all(Ma.reshape(3, -1)[:, mask.ravel() == 0] == 0.0)
+    np.testing.assert_allclose(ma, mb, rtol=0, atol=1e-9)
+    np.testing.assert_allclose(ea, eb, rtol=1e-9, atol=0)
+    pb.grace_destroy(h)
+    ref.close()
