@@ -1280,15 +1280,28 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
 __host__ __device__ constexpr int tpc_of(int L, int ept) { return L >= ept ? L / ept : 1; }
 __host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
-template <int L, int EPT, int MINB256>
+template <int L, int EPT, int MINB256, int NTT = 256>
 struct XCfgT {  // K1 / K5: B spatial rows x 3 components per CTA
   static constexpr int TPC = tpc_of(L, EPT);
-  static constexpr int B = (L == 0) ? 64 : cmax(1, 256 / TPC);
+  static constexpr int B = (L == 0) ? 64 : cmax(1, NTT / TPC);
   static constexpr int NT = (L == 0) ? 64 : B * TPC;
   static constexpr int MINB = NT <= 256 ? MINB256 : (NT <= 512 ? 2 : 1);
 };
+// Short rows (L <= 32: cubes up to 32^3, 8^3 .. 32^3 of Table 1) have few rows
+// in all: fewer elements per thread and smaller CTAs spread them over more SMs
+// (16^3: K5 was one 256-thread CTA).  GRACE_EPT_SMALL = 0 keeps the large-row
+// configuration everywhere.
+#ifndef GRACE_EPT_SMALL
+#define GRACE_EPT_SMALL 4
+#endif
+#ifndef GRACE_NT_SMALL
+#define GRACE_NT_SMALL 64
+#endif
 template <int L>
-using X1Cfg = XCfgT<L, GRACE_EPT_K1, GRACE_MINB_K1>;
+constexpr bool x_small() { return GRACE_EPT_SMALL > 0 && L > 0 && L <= 32; }
+template <int L>
+using X1Cfg = XCfgT<L, x_small<L>() ? GRACE_EPT_SMALL : GRACE_EPT_K1, GRACE_MINB_K1,
+                    x_small<L>() ? GRACE_NT_SMALL : 256>;
 template <int L>
 using X5Cfg = XCfgT<L, GRACE_EPT_K5, GRACE_MINB_K5>;
 #ifndef GRACE_EPT_K5S
@@ -1298,7 +1311,8 @@ using X5Cfg = XCfgT<L, GRACE_EPT_K5, GRACE_MINB_K5>;
 #define GRACE_MINB_K5S 2
 #endif
 template <int L>
-using X5SCfg = XCfgT<L, GRACE_EPT_K5S, GRACE_MINB_K5S>;  // K5 of the split step (no LLG epilogue)
+using X5SCfg = XCfgT<L, x_small<L>() ? GRACE_EPT_SMALL : GRACE_EPT_K5S, GRACE_MINB_K5S,
+                     x_small<L>() ? GRACE_NT_SMALL : 256>;  // K5 of the split step (no LLG epilogue)
 template <int L>
 struct YCfg {  // K2/K4 columns
   static constexpr int NCOL = cmax(2, cmin(32, GRACE_Y_ELEMS / L));
