@@ -1271,6 +1271,15 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
 #ifndef GRACE_MINB_Z
 #define GRACE_MINB_Z 4
 #endif
+#ifndef GRACE_MINB_Z256
+#define GRACE_MINB_Z256 8  // scripts/sweep_zlong.sh: 256^3 K3 1.46 -> 1.34 ms
+#endif
+#ifndef GRACE_MINB_Z512
+#define GRACE_MINB_Z512 1  // 2: 64 registers with spills
+#endif
+#ifndef GRACE_MINB_Z1024
+#define GRACE_MINB_Z1024 1  // 512^3 K3 20.7 -> 15.6 ms (2: 648 B of spills)
+#endif
 #ifndef GRACE_MINB_Z16
 #define GRACE_MINB_Z16 3  // scripts/sweep_z16.sh: film K3 0.084 -> 0.074 ms (4: 128 registers with spills; 2: 0.086 ms)
 #endif
@@ -1327,7 +1336,11 @@ struct ZCfg {  // K3 and K2'
   static constexpr int B = ZPlan<L>::B;
   static constexpr int NT = ZPlan<L>::NT;
   // L = 16 (film Pz, 8^3 cubes): one thread holds a radix-16 pencil of 3 components
-  static constexpr int MINB = (L == 16 ? GRACE_MINB_Z16 : (NT <= 256 ? GRACE_MINB_Z : (NT <= 512 ? 2 : 1)));
+  static constexpr int MINB = (L == 16 ? GRACE_MINB_Z16
+                                : L == 256 ? GRACE_MINB_Z256
+                                : L == 512 ? GRACE_MINB_Z512
+                                : L == 1024 ? GRACE_MINB_Z1024
+                                : (NT <= 256 ? GRACE_MINB_Z : (NT <= 512 ? 2 : 1)));
   static constexpr size_t SMEM = (size_t)3 * TileIdx<L, B, true>::ELEMS * 8 + (size_t)6 * (L / 2 + 1) * B * 4;
 };
 
