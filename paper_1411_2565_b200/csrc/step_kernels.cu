@@ -1271,6 +1271,9 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
 #ifndef GRACE_MINB_Z
 #define GRACE_MINB_Z 4
 #endif
+#ifndef GRACE_MINB_Z128
+#define GRACE_MINB_Z128 GRACE_MINB_Z
+#endif
 #ifndef GRACE_MINB_Z256
 #define GRACE_MINB_Z256 8  // scripts/sweep_zlong.sh: 256^3 K3 1.46 -> 1.34 ms
 #endif
@@ -1337,6 +1340,7 @@ struct ZCfg {  // K3 and K2'
   static constexpr int NT = ZPlan<L>::NT;
   // L = 16 (film Pz, 8^3 cubes): one thread holds a radix-16 pencil of 3 components
   static constexpr int MINB = (L == 16 ? GRACE_MINB_Z16
+                                : L == 128 ? GRACE_MINB_Z128
                                 : L == 256 ? GRACE_MINB_Z256
                                 : L == 512 ? GRACE_MINB_Z512
                                 : L == 1024 ? GRACE_MINB_Z1024
