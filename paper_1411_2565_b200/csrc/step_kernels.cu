@@ -1272,7 +1272,7 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
 #define GRACE_MINB_Z 4
 #endif
 #ifndef GRACE_MINB_Z128
-#define GRACE_MINB_Z128 GRACE_MINB_Z
+#define GRACE_MINB_Z128 3  // scripts/sweep_z128.sh: block K3 12.15 -> 11.76 ms (4: 128 registers; 2: 15.1 ms)
 #endif
 #ifndef GRACE_MINB_Z256
 #define GRACE_MINB_Z256 8  // scripts/sweep_zlong.sh: 256^3 K3 1.46 -> 1.34 ms
