@@ -43,24 +43,33 @@ UNIT = "cell-updates/s"
 # ------------------------------------------------------------------ helpers
 
 def algorithmic_bytes(geo, names):
-    """Compulsory HBM bytes per launch of each kernel, unpadded Kx."""
+    """Compulsory HBM bytes per launch of each kernel, unpadded Kx.
+    K5 writes H_demag (12 B/cell) and K6 reads it back: the split step moves
+    24 B/cell more than SURVEY §8(d)'s design (C2R + LLG in one pass)."""
     nx, ny, nz = geo["nx"], geo["ny"], geo["nz"]
     Py, Kx, Kyh, Kzh = geo["Py"], geo["Kx"], geo["Kyh"], geo["Kzh"]
     N = nx * ny * nz
     x1 = 3 * nz * ny * Kx * 8
     x2 = 3 * nz * Py * Kx * 8
     m = 12 * N
-    split = "K6" in names
     ks = 6 * Kzh * Kyh * Kx * 4 if geo["Pz"] > 1 else 4 * Kyh * Kx * 4
     b = {"K1": m + x1, "K2f": 2 * x1 + ks, "K2": x1 + x2, "K3": 2 * x2 + ks, "K4": x2 + x1,
-         "K5": x1 + (m if split else 2 * m), "K6": 3 * m}
+         "K5": x1 + m, "K6": 3 * m}
     return {k: b[k] for k in names}
 
 
+def design_step_bytes(geo):
+    """SURVEY §8(d)'s per-step compulsory bytes (349 B/cell at the slab): the
+    same FFT stages with the C2R and the LLG update in one pass (x1 + 2m)."""
+    nx, ny, nz = geo["nx"], geo["ny"], geo["nz"]
+    names = KERNEL_NAMES[geo["kernels"]]
+    ab = algorithmic_bytes(geo, names)
+    return sum(ab.values()) - 2 * 12 * nx * ny * nz
+
+
 STEP_DESC = {"K1": "K1 x-R2C", "K2": "K2 y-FFT (TMA)", "K2f": "K2' y-FFT*N*iFFT", "K3": "K3 z-FFT*N*iFFT",
-             "K4": "K4 y-iFFT (TMA)", "K5": "K5 x-C2R (+LLG if fused)", "K6": "K6 exch+anis+Zeeman+LLG+Euler stencil"}
-KERNEL_NAMES = {3: ["K1", "K2f", "K5"], 4: ["K1", "K2f", "K5", "K6"], 5: ["K1", "K2", "K3", "K4", "K5"],
-                6: ["K1", "K2", "K3", "K4", "K5", "K6"]}
+             "K4": "K4 y-iFFT (TMA)", "K5": "K5 x-C2R -> H_demag", "K6": "K6 exch+anis+Zeeman+LLG+Euler stencil"}
+KERNEL_NAMES = {4: ["K1", "K2f", "K5", "K6"], 6: ["K1", "K2", "K3", "K4", "K5", "K6"]}
 
 
 def read_peaks():
@@ -144,27 +153,49 @@ REF_EST_S = {(256, 256, 32): 4.6, (128, 128, 32): 1.1, (64, 64, 32): 0.25, (64, 
              (32, 32, 16): 0.03, (32, 32, 8): 0.015}
 
 
-def oracle_sim(w, n):
+def oracle_sim(w, n, workers=None, oct_=None):
     from oracle.demag import DemagFFT
     from oracle.llg import Sim
     from oracle.tensor import tensor_octant
 
-    op = DemagFFT(tensor_octant(*n, *w.d))
+    if oct_ is None:
+        oct_ = tensor_octant(*n, *w.d)
+    op = DemagFFT(oct_, workers=workers)
     return Sim(random_m(n, w.Ms), op, w.Ms, w.A, w.Ku, w.alpha, w.gamma0, w.d, w.hext)
 
 
 def cpu_baseline(w, steps=3):
+    """The oracle as it stands on this host's cores, on a bounded sample of the
+    workload: tensor setup timed separately, then Euler steps with numpy's
+    single-thread FFT and with scipy.fft on all cores."""
+    from oracle.tensor import tensor_octant
+
     n = (min(256, w.n[0]), min(256, w.n[1]), w.n[2])
-    sim = oracle_sim(w, n)
+    cells = n[0] * n[1] * n[2]
+    ncores = host_cores()
+    t = time.perf_counter()
+    oct_ = tensor_octant(*n, *w.d)
+    t_oct = time.perf_counter() - t
+    t = time.perf_counter()
+    sim = oracle_sim(w, n, oct_=oct_)
+    t_spec = time.perf_counter() - t
     sim.euler_step(w.dt)
     t = time.perf_counter()
     sim.run(steps, w.dt)
-    el = time.perf_counter() - t
-    cells = n[0] * n[1] * n[2]
-    return {"value": cells * steps / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+    el1 = time.perf_counter() - t
+    simk = oracle_sim(w, n, workers=ncores, oct_=oct_)
+    simk.euler_step(w.dt)
+    t = time.perf_counter()
+    simk.run(steps, w.dt)
+    elk = time.perf_counter() - t
+    return {"value": cells * steps / el1, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "value_all_cores": cells * steps / elk, "cores_all": ncores,
+            "setup_s": {"tensor_octant": t_oct, "kernel_spectrum": t_spec},
             "sample": f"{n[0]}x{n[1]}x{n[2]} cells of the {w.name} workload (same material, cell, dt), "
-                      f"1 warm-up + {steps} timed fp64 oracle Euler steps, numpy pocketfft single thread; "
-                      f"{el / steps:.2f} s/step; host has {host_cores()} cores"}
+                      f"1 warm-up + {steps} timed fp64 oracle Euler steps per mode; value: numpy pocketfft "
+                      f"single thread ({el1 / steps:.2f} s/step); value_all_cores: scipy.fft workers={ncores} "
+                      f"({elk / steps:.2f} s/step); tensor setup (octant + spectrum) {t_oct + t_spec:.1f} s, "
+                      f"not in the per-step values"}
 
 
 def run_reference(args, w):
@@ -286,13 +317,17 @@ def run_own(args, w):
     # dominant kernel: the longest measured launch (profiling mode), else the most bytes
     dom = max(kern, key=lambda k: kern[k]["ms_per_launch"] if profile else kern[k]["bytes_per_launch"])
     ach = kern[dom]["GBps"] if profile else None
-    step_bytes = sum(ab.values())
-    gpu_bytes = step_bytes / world if distributed else step_bytes  # per GPU per step
+    step_bytes = sum(ab.values())  # moved by this build's kernels (373 B/cell at the slab)
+    design_bytes = design_step_bytes(geo)  # SURVEY §8(d) (349 B/cell at the slab)
+    div = world if distributed else 1  # per GPU per step
     roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": ach / peak if ach else None,
                 "traffic": ncu_traffic(w.name, dom), "peak_source": peak_src,
-                "step_bytes": step_bytes, "step_GBps_per_gpu": gpu_bytes / (ms_step / 1e3) / 1e9,
-                "step_frac": gpu_bytes / (ms_step / 1e3) / 1e9 / peak}
+                "step_bytes_design": design_bytes, "step_bytes_moved": step_bytes,
+                "step_frac": design_bytes / div / (ms_step / 1e3) / 1e9 / peak,
+                "step_frac_moved": step_bytes / div / (ms_step / 1e3) / 1e9 / peak,
+                "step_frac_note": "step_frac: SURVEY 8(d) design bytes (349 B/cell at the slab) / ms_step / peak; "
+                                  "step_frac_moved: the bytes this build's kernels move (K5/K6 split: +24 B/cell)"}
 
     # e2e through the public API with pinned host buffers
     e2e = None
@@ -340,9 +375,10 @@ def run_own(args, w):
                     else f"{world} independent replicas (nz not divisible by {world})"),
                    "step": " | ".join(STEP_DESC[k] for k in names),
                    "timing": "timed region 1 (value, ms_per_step): K steps of CUDA-graph replay with programmatic "
-                             "dependent launch, CUDA events on the library stream; timed region 2 (kernels, roofline): "
-                             "the same K steps in libgrace profiling mode, eager launches with a CUDA event pair per "
-                             "kernel",
+                             "dependent launch (the step graphs are instantiated in grace_create, none is captured "
+                             "inside the region), CUDA events on the library stream; timed region 2 (kernels, "
+                             "roofline): the same K steps in libgrace profiling mode, eager launches with a CUDA "
+                             "event pair per kernel",
                    "ms_per_step_profiling_mode": ms_prof},
         "roofline": roofline,
         "kernels": kern,

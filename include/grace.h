@@ -137,8 +137,8 @@ int grace_set_field_schedule(grace_ctx *h, double h0x, double h0y, double h0z, l
  * renormalisation (the paper's; default), 1 = Heun (explicit trapezoid,
  * second order) with the same renormalisation: f0 = dM/dt(M_k, t_k),
  * M* = renorm(M_k + dt f0), M_{k+1} = renorm(M_k + dt (f0 + dM/dt(M*, t_{k+1}))/2);
- * two H_eff evaluations per step.  GRACE_EINVAL for another kind,
- * GRACE_EUNSUPPORTED with GRACE_K5_FUSED=1 or in profiling mode. */
+ * two H_eff evaluations per step.  GRACE_EINVAL for another kind; grace_step
+ * returns GRACE_EUNSUPPORTED for Heun in profiling mode. */
 int grace_set_integrator(grace_ctx *h, int kind);
 
 /* Geometry mask (the paper's "non-regular geometry", P:L121;
@@ -150,8 +150,8 @@ int grace_set_integrator(grace_ctx *h, int kind);
  * grace_heff reports 0 in empty cells; grace_step leaves them at 0; grace_mavg and
  * grace_energy sum over magnetic cells.  The current M is zeroed in empty cells;
  * grace_set_m afterwards ignores the input there (cells newly made magnetic need
- * a grace_set_m).  GRACE_EINVAL if no cell is magnetic, GRACE_EUNSUPPORTED with
- * GRACE_K5_FUSED=1.  Costs Nl bytes of device memory per rank. */
+ * a grace_set_m).  GRACE_EINVAL if no cell is magnetic.  Costs Nl bytes of
+ * device memory per rank. */
 int grace_set_geometry(grace_ctx *h, const unsigned char *mask);
 
 /* Steps taken so far (t = steps * dt). */

@@ -98,21 +98,33 @@ def demag_fft(M, oct_, P=None):
 
 
 class DemagFFT:
-    """The same FFT convolution with the kernel spectrum computed once (P:L55 precompute)."""
+    """The same FFT convolution with the kernel spectrum computed once (P:L55 precompute).
 
-    def __init__(self, oct_, P=None):
+    workers: None = numpy.fft (single thread); an int = scipy.fft with that many
+    threads (the all-core CPU baseline).  The same rfftn /
+    irfftn either way.
+    """
+
+    def __init__(self, oct_, P=None, workers=None):
         _, nz, ny, nx = oct_.shape
         self.shape = (nz, ny, nx)
         self.P = P if P is not None else (_pad(nz), _pad(ny), _pad(nx))
         self.Ns = kernel_spectrum(oct_, self.P)
+        if workers is None:
+            self._rfftn, self._irfftn = np.fft.rfftn, np.fft.irfftn
+        else:
+            import scipy.fft as sf
+
+            self._rfftn = lambda a, s, axes: sf.rfftn(a, s=s, axes=axes, workers=workers)
+            self._irfftn = lambda a, s, axes: sf.irfftn(a, s=s, axes=axes, workers=workers)
 
     def __call__(self, M):
         nz, ny, nx = self.shape
-        Mh = [np.fft.rfftn(M[b], s=self.P, axes=(0, 1, 2)) for b in range(3)]
+        Mh = [self._rfftn(M[b], s=self.P, axes=(0, 1, 2)) for b in range(3)]
         H = np.empty((3, nz, ny, nx), dtype=np.float64)
         for a in range(3):
             acc = np.zeros_like(Mh[0])
             for b in range(3):
                 acc = acc + self.Ns[_PAIRS[a][b]] * Mh[b]
-            H[a] = np.fft.irfftn(-acc, s=self.P, axes=(0, 1, 2))[:nz, :ny, :nx]
+            H[a] = self._irfftn(-acc, s=self.P, axes=(0, 1, 2))[:nz, :ny, :nx]
         return H

@@ -71,12 +71,13 @@ typedef int ncclResult_t;
 struct ncclUniqueId {
   char internal[128];
 };
-enum { kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0, kNcclMax = 2 };
+enum { kNcclUint64 = 5, kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0, kNcclMax = 2, kNcclMin = 3 };
 struct Nccl {
   void* h = nullptr;
   ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*commSplit)(ncclComm_t, int, int, ncclComm_t*, void*) = nullptr;  // optional (NCCL >= 2.18)
   ncclResult_t (*allReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -85,7 +86,9 @@ struct Nccl {
   const char* (*errStr)(ncclResult_t) = nullptr;
   // The process's NCCL: GRACE_NCCL_LIB (the Python binding points it at torch's
   // bundled libnccl), else an already-loaded or system libnccl.so.2.  Only calls
-  // present in every NCCL >= 2.7 are used (the transposes are grouped send/recv).
+  // present in every NCCL >= 2.7 are required (the transposes are grouped
+  // send/recv); ncclCommSplit, when present, gives the halo exchange its own
+  // communicator.
   bool load() {
     if (h) return true;
     const char* env = getenv("GRACE_NCCL_LIB");
@@ -103,6 +106,7 @@ struct Nccl {
     getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
     commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
     commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    commSplit = (decltype(commSplit))dlsym(h, "ncclCommSplit");
     allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
     send = (decltype(send))dlsym(h, "ncclSend");
     recv = (decltype(recv))dlsym(h, "ncclRecv");
@@ -130,7 +134,7 @@ struct Rank {
   float* Hlo = nullptr;  // halo planes [3][ny][nx]
   float* Hhi = nullptr;
   StepParams* prm = nullptr;
-  unsigned long long* flag = nullptr;  // [0] step non-finite, [1] set_m zero cell
+  unsigned long long* flag = nullptr;  // [0] step non-finite, [1] set_m zero cell, [2] NCCL reduction slot
   double* red = nullptr;               // mavg partials + 3 outputs
   double* dred = nullptr;              // diagnostics partials + 5 outputs (allocated on first use)
   float* Hbuf = nullptr;
@@ -166,6 +170,7 @@ struct grace_ctx {
   cudaEvent_t evM = nullptr, evH = nullptr;   // fork (M[c] ready) / join (halos landed)
   cudaGraphExec_t g1[2] = {nullptr, nullptr}, gc[2] = {nullptr, nullptr};
   ncclComm_t comm = nullptr;
+  ncclComm_t comm_halo = nullptr;  // C3's own communicator (NCCL orders work per communicator)
   bool profiling = false;
   std::vector<double> kms;
   std::vector<long long> klaunch;
@@ -257,15 +262,16 @@ struct grace_ctx {
     }
     Rank& rk = ranks[0];
     const int r = myrank;
+    ncclComm_t hc = comm_halo ? comm_halo : comm;
     bool bad = g_nccl.groupStart() != 0;
     for (int q = 0; q < 3 && !bad; ++q) {
       if (r > 0) {
-        bad |= g_nccl.send(rk.M[c] + q * Nl, plane, kNcclFloat32, r - 1, comm, s) != 0;
-        bad |= g_nccl.recv(rk.Hlo + q * plane, plane, kNcclFloat32, r - 1, comm, s) != 0;
+        bad |= g_nccl.send(rk.M[c] + q * Nl, plane, kNcclFloat32, r - 1, hc, s) != 0;
+        bad |= g_nccl.recv(rk.Hlo + q * plane, plane, kNcclFloat32, r - 1, hc, s) != 0;
       }
       if (r + 1 < P) {
-        bad |= g_nccl.send(rk.M[c] + q * Nl + (size_t)(nzl - 1) * plane, plane, kNcclFloat32, r + 1, comm, s) != 0;
-        bad |= g_nccl.recv(rk.Hhi + q * plane, plane, kNcclFloat32, r + 1, comm, s) != 0;
+        bad |= g_nccl.send(rk.M[c] + q * Nl + (size_t)(nzl - 1) * plane, plane, kNcclFloat32, r + 1, hc, s) != 0;
+        bad |= g_nccl.recv(rk.Hhi + q * plane, plane, kNcclFloat32, r + 1, hc, s) != 0;
       }
     }
     bad |= g_nccl.groupEnd() != 0;
@@ -274,13 +280,19 @@ struct grace_ctx {
 
   // C3 on the side stream: it needs only M[c], so it runs under K1..K4 and the
   // transposes; the stencil kernel joins it (halo_join) before reading Hlo/Hhi.
+  // On the NCCL path the side stream is used only with the halo's own
+  // communicator (ncclCommSplit): on the transposes' communicator NCCL would
+  // run it in issue order anyway, so it then goes on the step stream.
   cudaError_t halo_start(int c, cudaStream_t s) {
+    if (mode == kNccl && !comm_halo) return halo(c, s);
     CE(cudaEventRecord(evM, s));
     CE(cudaStreamWaitEvent(hs, evM, 0));
     CE(halo(c, hs));
     return cudaEventRecord(evH, hs);
   }
-  cudaError_t halo_join(cudaStream_t s) { return mode == kSingle ? cudaSuccess : cudaStreamWaitEvent(s, evH, 0); }
+  cudaError_t halo_join(cudaStream_t s) {
+    return (mode == kSingle || (mode == kNccl && !comm_halo)) ? cudaSuccess : cudaStreamWaitEvent(s, evH, 0);
+  }
 
   // H~ for every rank: K1 .. K4 plus the transposes.  M[c] is the input.
   cudaError_t demag_stages(int c, cudaStream_t s, bool bump, cudaEvent_t* ev = nullptr) {
@@ -329,13 +341,13 @@ struct grace_ctx {
     CE(demag_stages(c, s, true));
     CE(halo_join(s));
     for (auto& rk : ranks) {
-      CE(launch_k5(rk.g, 2, rk.A, rk.M[c], nullptr, rk.Hd, tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+      CE(launch_k5(rk.g, rk.A, rk.Hd, tw, s));
       CE(launch_k6(rk.g, 3, rk.Hd, rk.M[c], rk.M[1 - c], rk.F, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
     }
     CE(demag_stages(1 - c, s, false));
     CE(halo_join(s));
     for (auto& rk : ranks) {
-      CE(launch_k5(rk.g, 2, rk.A, rk.M[1 - c], nullptr, rk.Hd, tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+      CE(launch_k5(rk.g, rk.A, rk.Hd, tw, s));
       CE(launch_k6(rk.g, 4, rk.Hd, rk.M[1 - c], rk.M[c], rk.F, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
     }
     return cudaSuccess;
@@ -348,22 +360,15 @@ struct grace_ctx {
     if (integrator == 1) return enqueue_heun(c, s);
     CE(demag_stages(c, s, true, ev));
     const int nk = kernel_count(g0);
-    const int k5 = 2 * (nk - (g0.split_llg ? 2 : 1));
+    const int k5 = 2 * (nk - 2);
     if (ev) cudaEventRecord(ev[k5], s);
     CE(halo_join(s));
-    for (auto& rk : ranks) {
-      if (g0.split_llg)
-        CE(launch_k5(rk.g, 2, rk.A, rk.M[c], nullptr, rk.Hd, tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
-      else
-        CE(launch_k5(rk.g, 0, rk.A, rk.M[c], rk.M[1 - c], nullptr, tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
-    }
+    for (auto& rk : ranks) CE(launch_k5(rk.g, rk.A, rk.Hd, tw, s));
     if (ev) cudaEventRecord(ev[k5 + 1], s);
-    if (g0.split_llg) {
-      if (ev) cudaEventRecord(ev[k5 + 2], s);
-      for (auto& rk : ranks)
-        CE(launch_k6(rk.g, 0, rk.Hd, rk.M[c], rk.M[1 - c], nullptr, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
-      if (ev) cudaEventRecord(ev[k5 + 3], s);
-    }
+    if (ev) cudaEventRecord(ev[k5 + 2], s);
+    for (auto& rk : ranks)
+      CE(launch_k6(rk.g, 0, rk.Hd, rk.M[c], rk.M[1 - c], nullptr, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+    if (ev) cudaEventRecord(ev[k5 + 3], s);
     return cudaSuccess;
   }
 
@@ -383,6 +388,26 @@ struct grace_ctx {
     return e;
   }
 
+  // Capture and instantiate every single-GPU step graph the loop can use (16-step
+  // chunks and single steps, from either M buffer) ahead of time, so no
+  // grace_step call pays a capture: done at create and after anything that
+  // invalidates them (integrator, geometry mask).
+  cudaError_t prepare_graphs() {
+    if (mode != kSingle) return cudaSuccess;
+    for (int c = 0; c < 2; ++c) {
+      if (!gc[c]) CE(build_graph(c, kChunk, &gc[c]));
+      if (!g1[c]) CE(build_graph(c, 1, &g1[c]));
+    }
+    return cudaSuccess;
+  }
+  void drop_graphs() {
+    for (int c = 0; c < 2; ++c) {
+      if (g1[c]) cudaGraphExecDestroy(g1[c]);
+      if (gc[c]) cudaGraphExecDestroy(gc[c]);
+      g1[c] = gc[c] = nullptr;
+    }
+  }
+
   void release() {
     for (int c = 0; c < 2; ++c) {
       if (g1[c]) cudaGraphExecDestroy(g1[c]);
@@ -396,6 +421,7 @@ struct grace_ctx {
         if (p) cudaFree(p);
     }
     if (tw) cudaFree(tw);
+    if (comm_halo) g_nccl.commDestroy(comm_halo);
     if (comm) g_nccl.commDestroy(comm);
     if (own) cudaStreamDestroy(own);
     if (cap) cudaStreamDestroy(cap);
@@ -439,8 +465,6 @@ int make_geom(int nx, int ny, int nz, double dx, double dy, double dz, double Ms
   g.Kc = g.Kx;
   g.pitch2 = g.Kxp;
   g.has_lo = g.has_hi = 0;
-  const char* fz = getenv("GRACE_K5_FUSED");
-  g.split_llg = (fz && fz[0] == '1') ? 0 : 1;
   int dev = 0, nsm = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   cudaGetLastError();
@@ -532,6 +556,9 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
     std::memcpy(&id, nccl_id, sizeof id);
     const ncclResult_t r = g_nccl.commInitRank(&h->comm, P, id, first_rank);
     if (r != 0) return bail(fail(GRACE_ECUDA, "ncclCommInitRank: %s", g_nccl.errStr(r)));
+    if (g_nccl.commSplit && !getenv("GRACE_NO_HALO_COMM")) {  // collective over the ranks: all or none
+      if (g_nccl.commSplit(h->comm, 0, first_rank, &h->comm_halo, nullptr) != 0) h->comm_halo = nullptr;
+    }
   }
   h->ranks.resize(nranks_here);
   for (int i = 0; i < nranks_here; ++i) {
@@ -550,9 +577,9 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
         (x2 && (rc = h->alloc((void**)&rk.X2, x2))) || (rc = h->alloc((void**)&rk.KS, ks)) ||
         (g.has_lo && (rc = h->alloc((void**)&rk.Hlo, hb))) || (g.has_hi && (rc = h->alloc((void**)&rk.Hhi, hb))) ||
         (rc = h->alloc((void**)&rk.prm, sizeof(StepParams))) ||
-        (rc = h->alloc((void**)&rk.flag, 2 * sizeof(unsigned long long))) ||
+        (rc = h->alloc((void**)&rk.flag, 3 * sizeof(unsigned long long))) ||
         (rc = h->alloc((void**)&rk.red, sizeof(double) * (kMavgPartials + 3))) ||
-        (g.split_llg && (rc = h->alloc((void**)&rk.Hd, mb))))
+        (rc = h->alloc((void**)&rk.Hd, mb)))
       return bail(rc);
   }
   if ((rc = h->alloc((void**)&h->tw, sizeof(float2) * g0.Lmax))) return bail(rc);
@@ -563,33 +590,26 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
   cudaGetLastError();
   h->N = (mode == grace_ctx::kNccl) ? h->ranks[0].Nl : (long long)nx * ny * nz;
 
-  // setup: fp64 octant -> fp64 padded spectrum -> fp32 folded KS (S1..S5), once,
-  // then each rank keeps its kx columns
+  // setup: fp64 octant -> fp64 padded spectrum -> fp32 folded KS (S1..S5), once;
+  // each rank's table receives only its kx columns (no full-width copy).  The
+  // transient scratch is the fp64 octant (48 B/cell) plus one component's padded
+  // complex grid (16 B per padded point), for the whole grid on every rank.
   const long long Ng = (long long)nx * ny * nz;
   double* oct = nullptr;
   double2* work = nullptr;
-  float* ksfull = nullptr;
   const size_t octb = sizeof(double) * 6 * (size_t)Ng;
   const size_t workb = sizeof(double2) * (size_t)g0.Px * g0.Py * g0.Pz;
-  const size_t ksfb = sizeof(float) * 6 * (size_t)g0.Kzh * g0.Kyh * g0.KSp;
-  if (cudaMalloc(&oct, octb) != cudaSuccess || cudaMalloc(&work, workb) != cudaSuccess ||
-      (dlay && cudaMalloc(&ksfull, ksfb) != cudaSuccess)) {
+  if (cudaMalloc(&oct, octb) != cudaSuccess || cudaMalloc(&work, workb) != cudaSuccess) {
     cudaGetLastError();
     if (oct) cudaFree(oct);
     if (work) cudaFree(work);
-    return bail(fail(GRACE_ENOMEM, "setup needs %zu bytes of fp64 scratch", octb + workb + ksfb));
+    return bail(fail(GRACE_ENOMEM, "setup needs %zu bytes of fp64 scratch", octb + workb));
   }
+  std::vector<KsOut> kso;
+  for (auto& rk : h->ranks)
+    if (rk.g.Kc > 0 || !dlay) kso.push_back(KsOut{rk.KS, dlay ? rk.r * rk.g.kb : 0, rk.g.Kc, rk.g.KSp});
   cudaError_t e = tensor_octant_device(nx, ny, nz, dx, dy, dz, oct, s);
-  if (e == cudaSuccess) e = kernel_spectrum_device(g0, oct, work, !dlay ? h->ranks[0].KS : ksfull, s);
-  if (e == cudaSuccess && dlay) {
-    for (auto& rk : h->ranks) {
-      if (rk.g.Kc == 0) continue;
-      const int kx0 = rk.r * rk.g.kb;
-      e = cudaMemcpy2DAsync(rk.KS, sizeof(float) * rk.g.KSp, ksfull + kx0, sizeof(float) * g0.KSp,
-                            sizeof(float) * rk.g.Kc, (size_t)6 * g0.Kzh * g0.Kyh, cudaMemcpyDeviceToDevice, s);
-      if (e != cudaSuccess) break;
-    }
-  }
+  if (e == cudaSuccess) e = kernel_spectrum_device(g0, oct, work, (int)kso.size(), kso.data(), s);
   if (e == cudaSuccess) e = launch_twiddles(h->tw, g0.Lmax, s);
   for (auto& rk : h->ranks) {
     if (e == cudaSuccess) e = launch_fill_uniform_x(rk.M[0], rk.Nl, (float)Ms, s);
@@ -599,7 +619,6 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   cudaFree(oct);
   cudaFree(work);
-  if (ksfull) cudaFree(ksfull);
   if (e != cudaSuccess) return bail(fail(GRACE_ECUDA, "tensor setup: %s", cudaGetErrorString(e)));
   // Dry run of one step (M[0] -> M[1], the spare buffer) so every kernel's
   // shared-memory attribute is set before any graph capture; then restore the
@@ -609,29 +628,43 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
     if (e == cudaSuccess) e = cudaMemsetAsync(rk.flag, 0xff, 2 * sizeof(unsigned long long), s);
   if (e == cudaSuccess) e = h->upload_params(1e-15);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = h->prepare_graphs();
   if (e != cudaSuccess) return bail(fail(GRACE_ECUDA, "first step: %s", cudaGetErrorString(e)));
   *out = h;
   return GRACE_OK;
 }
 
 // First set flag over the ranks (0: step non-finite, packed step<<36|cell; 1: set_m
-// zero cell), translated to the caller's cell numbering, and reset on the device.
+// zero cell), translated to the global cell numbering (z-slab offset added), and
+// reset on the device.  On the NCCL path the ranks agree: the translated flags
+// are min-reduced over the communicator, so every rank returns the same status
+// (a rank that alone returned an error would leave the others waiting in the
+// next collective).
 int check_flags(grace_ctx* h, int which, unsigned long long* first) {
   *first = kNoFlag;
+  const unsigned long long mask = (1ULL << 36) - 1;
   for (auto& rk : h->ranks) {
     unsigned long long f = kNoFlag;
     CUDA_OR(cudaMemcpyAsync(&h->pin->flag, rk.flag + which, sizeof f, cudaMemcpyDeviceToHost, h->stream));
     CUDA_OR(cudaStreamSynchronize(h->stream));
     f = h->pin->flag;
-    if (f == kNoFlag) continue;
-    CUDA_OR(cudaMemsetAsync(rk.flag + which, 0xff, sizeof f, h->stream));
-    CUDA_OR(cudaStreamSynchronize(h->stream));
-    const unsigned long long off =
-        (h->mode == grace_ctx::kVirtual) ? (unsigned long long)rk.r * rk.g.nzl * h->g0.ny * h->g0.nx : 0;
-    const unsigned long long mask = (1ULL << 36) - 1;
-    const unsigned long long packed = (which == 0) ? ((f & ~mask) | ((f & mask) + off)) : f + off;
-    if (packed < *first) *first = packed;
+    if (f != kNoFlag) {
+      CUDA_OR(cudaMemsetAsync(rk.flag + which, 0xff, sizeof f, h->stream));
+      const unsigned long long off = (unsigned long long)rk.r * rk.g.nzl * h->g0.ny * h->g0.nx;
+      f = (which == 0) ? ((f & ~mask) | ((f & mask) + off)) : f + off;
+    }
+    if (h->mode == grace_ctx::kNccl) {
+      h->pin->flag = f;
+      CUDA_OR(cudaMemcpyAsync(rk.flag + 2, &h->pin->flag, sizeof f, cudaMemcpyHostToDevice, h->stream));
+      const ncclResult_t r = g_nccl.allReduce(rk.flag + 2, rk.flag + 2, 1, kNcclUint64, kNcclMin, h->comm, h->stream);
+      if (r != 0) return fail(GRACE_ECUDA, "ncclAllReduce: %s", g_nccl.errStr(r));
+      CUDA_OR(cudaMemcpyAsync(&h->pin->flag, rk.flag + 2, sizeof f, cudaMemcpyDeviceToHost, h->stream));
+      CUDA_OR(cudaStreamSynchronize(h->stream));
+      f = h->pin->flag;
+    }
+    if (f < *first) *first = f;
   }
+  CUDA_OR(cudaStreamSynchronize(h->stream));
   return GRACE_OK;
 }
 
@@ -794,26 +827,20 @@ int grace_set_integrator(grace_ctx* h, int kind) {
   if (kind != 0 && kind != 1) return fail(GRACE_EINVAL, "integrator must be 0 (Euler) or 1 (Heun)");
   if (kind == h->integrator) return GRACE_OK;
   if (kind == 1) {
-    if (!h->g0.split_llg) return fail(GRACE_EUNSUPPORTED, "Heun needs the split K5/K6 step (GRACE_K5_FUSED unset)");
     for (auto& rk : h->ranks)
       if (!rk.F) {
         int rc = h->alloc((void**)&rk.F, sizeof(float) * 3 * (size_t)rk.Nl);
         if (rc) return rc;
       }
   }
-  for (int c = 0; c < 2; ++c) {  // captured step graphs belong to the old integrator
-    if (h->g1[c]) cudaGraphExecDestroy(h->g1[c]);
-    if (h->gc[c]) cudaGraphExecDestroy(h->gc[c]);
-    h->g1[c] = h->gc[c] = nullptr;
-  }
+  h->drop_graphs();  // captured step graphs belong to the old integrator
   h->integrator = kind;
+  CUDA_OR(h->prepare_graphs());
   return GRACE_OK;
 }
 
 int grace_set_geometry(grace_ctx* h, const unsigned char* mask) {
   if (!h) return fail(GRACE_EINVAL, "NULL context");
-  if (mask && !h->g0.split_llg)
-    return fail(GRACE_EUNSUPPORTED, "a geometry mask needs the split K5/K6 step (GRACE_K5_FUSED unset)");
   double local = 0;
   if (mask) {
     for (auto& rk : h->ranks) {
@@ -855,11 +882,8 @@ int grace_set_geometry(grace_ctx* h, const unsigned char* mask) {
   }
   CUDA_OR(cudaStreamSynchronize(h->stream));
   h->g0.masked = mask ? 1 : 0;
-  for (int c = 0; c < 2; ++c) {  // captured step graphs carry the old K6 instantiation
-    if (h->g1[c]) cudaGraphExecDestroy(h->g1[c]);
-    if (h->gc[c]) cudaGraphExecDestroy(h->gc[c]);
-    h->g1[c] = h->gc[c] = nullptr;
-  }
+  h->drop_graphs();  // captured step graphs carry the old K6 instantiation
+  CUDA_OR(h->prepare_graphs());
   return GRACE_OK;
 }
 
@@ -882,12 +906,8 @@ int grace_heff(grace_ctx* h, double* out) {
   CUDA_OR(h->demag_stages(h->cur, s, false));
   CUDA_OR(h->halo_join(s));
   for (auto& rk : h->ranks) {
-    if (rk.g.split_llg) {
-      CUDA_OR(launch_k5(rk.g, 2, rk.A, rk.M[h->cur], nullptr, rk.Hd, h->tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
-      CUDA_OR(launch_k6(rk.g, 1, rk.Hd, rk.M[h->cur], nullptr, rk.Hbuf, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
-    } else {
-      CUDA_OR(launch_k5(rk.g, 1, rk.A, rk.M[h->cur], nullptr, rk.Hbuf, h->tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
-    }
+    CUDA_OR(launch_k5(rk.g, rk.A, rk.Hd, h->tw, s));
+    CUDA_OR(launch_k6(rk.g, 1, rk.Hd, rk.M[h->cur], nullptr, rk.Hbuf, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
   }
   for (auto& rk : h->ranks) {
     double* stage = reinterpret_cast<double*>(rk.A);
@@ -1011,7 +1031,7 @@ static int diagnostics(grace_ctx* h, double S[5]) {
   CUDA_OR(h->demag_stages(h->cur, s, false));
   CUDA_OR(h->halo_join(s));
   for (auto& rk : h->ranks)
-    CUDA_OR(launch_k5(rk.g, 2, rk.A, rk.M[h->cur], nullptr, rk.Hd, h->tw, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+    CUDA_OR(launch_k5(rk.g, rk.A, rk.Hd, h->tw, s));
   for (int q = 0; q < 4; ++q) S[q] = 0.0;
   S[4] = 0.0;
   for (auto& rk : h->ranks) {

@@ -53,7 +53,6 @@ struct Geom {
   int pitch2;       // row pitch of X2
   int has_lo, has_hi;  // z-1 / z+1 halo planes present
   int nsm;             // SMs of the device (persistent grids)
-  int split_llg;       // 1: K5 stores H_demag and K6 does the local terms + update (streaming)
   int masked;          // geometry mask set (grace_set_geometry): M = 0 marks an empty cell (reading Q26)
   float cx, cy, cz; // exchange 2A/(mu0 Ms^2 d^2) per axis (0 for a singleton axis)
   float ck;         // anisotropy 2Ku/(mu0 Ms^2)
@@ -80,12 +79,10 @@ cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* 
 cudaError_t launch_k4(const Geom& g, const float2* X2, float2* X1, const float2* tw, cudaStream_t st,
                       const TmapBlob* tmap = nullptr);
 cudaError_t launch_k2f(const Geom& g, float2* X1, const float* KS, const float2* tw, cudaStream_t st);
-// mode 0: LLG Euler step M -> Mn; mode 1: store H_eff into Hout; mode 2: store H_demag into Hout.
+// K5: inverse x C2R of X1 -> H_demag Hd [3][nzl][ny][nx].
+cudaError_t launch_k5(const Geom& g, const float2* X1, float* Hd, const float2* tw, cudaStream_t st);
+// K6: local terms + LLG + Euler from H_demag (mode 0: M -> Mn; mode 1: H_eff -> Hout).
 // Hlo / Hhi: halo planes [3][ny][nx] of z-1 / z+1 (used when g.has_lo / g.has_hi).
-cudaError_t launch_k5(const Geom& g, int mode, const float2* X1, const float* M, float* Mn, float* Hout,
-                      const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st,
-                      const float* Hlo = nullptr, const float* Hhi = nullptr);
-// K6 (split step): local terms + LLG + Euler from H_demag (mode 0: M -> Mn; mode 1: H_eff -> Hout).
 cudaError_t launch_k6(const Geom& g, int mode, const float* Hd, const float* M, float* Mn, float* Hout,
                       const StepParams* prm, unsigned long long* flag, cudaStream_t st, const float* Hlo,
                       const float* Hhi);
@@ -116,8 +113,14 @@ cudaError_t launch_widen(const float* src, double* dst, long long n, cudaStream_
 // Real-space octant [6][nz][ny][nx] into device memory `oct` (bit-exact with the oracle).
 cudaError_t tensor_octant_device(int nx, int ny, int nz, double dx, double dy, double dz, double* oct,
                                  cudaStream_t st);
-// Spectral table KS [6][Kzh][Kyh][KSp] fp32 = -Re(FFT(circulant N))/(Px Py Pz), from the octant.
-// `work` must hold Px*Py*Pz double2.
-cudaError_t kernel_spectrum_device(const Geom& g, const double* oct, double2* work, float* KS, cudaStream_t st);
+// Spectral table KS [6][Kzh][Kyh][KSp] fp32 = -Re(FFT(circulant N))/(Px Py Pz), from the octant,
+// written for each output's kx columns [kx0, kx0 + ncol) (a rank's kx block; the
+// single-GPU table is kx0 = 0, ncol = Kx).  `work` must hold Px*Py*Pz double2.
+struct KsOut {
+  float* KS;
+  int kx0, ncol, KSp;
+};
+cudaError_t kernel_spectrum_device(const Geom& g, const double* oct, double2* work, int nout, const KsOut* out,
+                                   cudaStream_t st);
 
 }  // namespace grace

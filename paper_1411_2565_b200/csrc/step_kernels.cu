@@ -5,10 +5,11 @@
 //   K2  y-FFT (pruned: ny of Py inputs nonzero)  X1 -> X2 [3][nz][Py][Kxp]
 //   K3  z-FFT, H~ = KS . M~ (6 real folded comps), inverse z, keep z < nz   X2 -> X2
 //   K4  inverse y, keep y < ny                   X2 -> X1
-//   K5  inverse x C2R (keep x < nx) = H_demag, + six-neighbour exchange + x anisotropy
-//       + Zeeman (Eq. (2)), Eq. (3) LLG, Euler + renormalise   X1, M -> M'
+//   K5  inverse x C2R (keep x < nx) = H_demag                X1 -> Hd
+//   K6  six-neighbour exchange + x anisotropy + Zeeman (Eq. (2)), Eq. (3) LLG,
+//       Euler + renormalise                                 Hd, M -> M'
 // nz == 1 (thin films, SP4): K2' fuses y-FFT, multiply and inverse y in one
-// CTA (the z axis is unpadded), so the step is K1, K2', K5.
+// CTA (the z axis is unpadded), so the step is K1, K2', K5, K6.
 // The 1/(Px Py Pz) normalisation and the minus sign of H = -N*M live in KS.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -419,20 +420,26 @@ __device__ __forceinline__ void kmul_s(float2& a, float2& b, float2& c, const fl
 
 // Stage KS[c][k1][k2][kx0 .. kx0+B) for c = 0..5 into kss[c][k][b] with cp.async,
 // where the staged axis k runs over KH entries at stride kstride (floats) from `base`.
+// Columns at or beyond `avail` (= KSp - kx0: past the end of the KS row) are
+// zero-filled instead of read, so the last CTA never reads past the table.
 template <int B, int NT>
 __device__ __forceinline__ void stage_ks(float* kss, const float* __restrict__ base, size_t cstride, size_t kstride,
-                                         int KH) {
+                                         int KH, int avail) {
   if constexpr (B % 4 == 0) {
     for (int t = threadIdx.x; t < 6 * KH * (B / 4); t += NT) {
       const int ch = t % (B / 4), r = t / (B / 4);
       const int comp = r / KH, k = r - comp * KH;
-      cp_async16(kss + r * B + 4 * ch, base + comp * cstride + k * kstride + 4 * ch);
+      if (4 * ch < avail)  // KSp is a multiple of 32: a 4-float chunk is all in or all out
+        cp_async16(kss + r * B + 4 * ch, base + comp * cstride + k * kstride + 4 * ch);
+      else
+        *reinterpret_cast<float4*>(kss + r * B + 4 * ch) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   } else {
     for (int t = threadIdx.x; t < 6 * KH * B; t += NT) {
       const int bb = t % B, r = t / B;
       const int comp = r / KH, k = r - comp * KH;
-      cp_async4(kss + r * B + bb, base + comp * cstride + k * kstride + bb);
+      if (bb < avail) cp_async4(kss + r * B + bb, base + comp * cstride + k * kstride + bb);
+      else kss[r * B + bb] = 0.f;
     }
   }
 }
@@ -558,7 +565,8 @@ __global__ void __launch_bounds__(NT, MINB) k3_z(float2* __restrict__ X2, const 
   const int nky = (kyf == 0 || 2 * kyf == g.Py) ? 1 : 2;
   float* kss = reinterpret_cast<float*>(smem + 3 * TileIdx<L, B, true>::ELEMS);
   pdl_trigger();
-  stage_ks<B, NT>(kss, KS + (size_t)kyf * g.KSp + kx0, (size_t)g.Kzh * g.Kyh * g.KSp, (size_t)g.Kyh * g.KSp, KZH);
+  stage_ks<B, NT>(kss, KS + (size_t)kyf * g.KSp + kx0, (size_t)g.Kzh * g.Kyh * g.KSp, (size_t)g.Kyh * g.KSp, KZH,
+                  g.KSp - kx0);
   pdl_wait();  // the KS slice is constant; X2 comes from K2
   for (int rep = 0; rep < nky; ++rep) {
     const int ky = rep == 0 ? kyf : g.Py - kyf;
@@ -634,7 +642,7 @@ __global__ void __launch_bounds__(NT, MINB) k2f_y_fused(float2* __restrict__ X1,
   const size_t cstride = (size_t)g.ny * g.pitch1;
   float2* base = X1 + kx0;
   float* kss = reinterpret_cast<float*>(smem + 3 * TileIdx<L, B, true>::ELEMS);
-  stage_ks<B, NT>(kss, KS + kx0, (size_t)g.Kzh * g.Kyh * g.KSp, (size_t)g.KSp, KYH);
+  stage_ks<B, NT>(kss, KS + kx0, (size_t)g.Kzh * g.Kyh * g.KSp, (size_t)g.KSp, KYH, g.KSp - kx0);
   struct Ld {
     __device__ static constexpr bool kSmem() { return false; }
     const float2* p;
@@ -659,135 +667,15 @@ __global__ void __launch_bounds__(NT, MINB) k2f_y_fused(float2* __restrict__ X1,
 }
 
 // ---------------------------------------------------------------------------
-// K5: inverse x C2R of the three H~ rows, then the local terms and the update.
-// C2R of length Px = 2L from the half spectrum X[0..L]:
+// K5: inverse x C2R of the three H~ rows -> H_demag (K6 then applies the local
+// terms and the update).  C2R of length Px = 2L from the half spectrum X[0..L]:
 //   Z[k] = (X[k] + conj X[L-k]) + i w^-k (X[k] - conj X[L-k]),  k < L,
 //   z = IFFT_L(Z) (unnormalised; 1/P is in KS),  x[2n] = Re z[n], x[2n+1] = Im z[n].
-// The last inverse pass leaves H_demag of cells x = 2n, 2n+1 (all three
-// components) in the registers of one thread, which applies Eq. (2), Eq. (3)
-// and the Euler update to that cell pair directly.
-struct CellCtx {
-  const float* M;
-  float* Mn;
-  float* Hout;
-  const float* Hlo;
-  const float* Hhi;
-  unsigned long long* flag;
-  size_t N, plane;
-  int mode;
-};
-
-__device__ __forceinline__ float2 ld2(const float* p, bool pair_ok, bool vec) {
-  // (p[0], p[1]); p[1] only if pair_ok.  vec: one 8-byte load (nx even, x0 even: aligned).
-  if (vec) return __ldg(reinterpret_cast<const float2*>(p));
-  return pair_ok ? make_float2(__ldg(p), __ldg(p + 1)) : make_float2(__ldg(p), 0.f);
-}
-
-// Update cells (x0, zl, y) and (x0+1, zl, y) (the second only if hasB) with
-// H_demag hA / hB.  Missing neighbours (Neumann) use the centre value.
-template <bool DIST>
-__device__ __forceinline__ void cell_pair(const CellCtx& cc, const Geom& g, const StepParams& p, int row, int x0,
-                                          bool hasB, const float hA[3], const float hB[3]) {
-  const int zl = row / g.ny, y = row - zl * g.ny;
-  const size_t i = (size_t)row * g.nx + x0;
-  const size_t iy0 = y > 0 ? i - g.nx : i, iy1 = y + 1 < g.ny ? i + g.nx : i;
-  const float* zlo;  // pointers to the z-1 / z+1 cell of x0 (component 0), and component strides
-  const float* zhi;
-  size_t czlo = cc.N, czhi = cc.N;
-  if (zl > 0) zlo = cc.M + (i - cc.plane);
-  else if (DIST && g.has_lo) { zlo = cc.Hlo + (size_t)y * g.nx + x0; czlo = cc.plane; }
-  else zlo = cc.M + i;
-  if (zl + 1 < g.nzl) zhi = cc.M + (i + cc.plane);
-  else if (DIST && g.has_hi) { zhi = cc.Hhi + (size_t)y * g.nx + x0; czhi = cc.plane; }
-  else zhi = cc.M + i;
-  const bool xm = x0 > 0, xp = x0 + 2 < g.nx;
-  const bool vec = hasB && ((g.nx & 1) == 0);
-  float m[3][2], nx0[3], nx1[3], ny0[3][2], ny1[3][2], nz0[3][2], nz1[3][2];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const float* mc = cc.M + c * cc.N;
-    const float2 mm = ld2(mc + i, hasB, vec);
-    m[c][0] = mm.x;
-    m[c][1] = mm.y;
-    nx0[c] = xm ? __ldg(mc + i - 1) : mm.x;
-    nx1[c] = xp ? __ldg(mc + i + 2) : (hasB ? mm.y : mm.x);
-    const float2 a = ld2(mc + iy0, hasB, vec), b = ld2(mc + iy1, hasB, vec);
-    const float2 d = ld2(zlo + c * czlo, hasB, vec), e = ld2(zhi + c * czhi, hasB, vec);
-    ny0[c][0] = a.x; ny0[c][1] = a.y;
-    ny1[c][0] = b.x; ny1[c][1] = b.y;
-    nz0[c][0] = d.x; nz0[c][1] = d.y;
-    nz1[c][0] = e.x; nz1[c][1] = e.y;
-  }
-  float out[2][3];
-  float ha[3];
-  applied_field(p, ha);
-#pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    const float* hd = s ? hB : hA;
-    const float mx = m[0][s], my = m[1][s], mz = m[2][s];
-    // Eq. (2): H_eff = H_demag + H_exch + H_anis + H_ext
-    float hx = hd[0] + ha[0] + g.ck * mx;
-    float hy = hd[1] + ha[1];
-    float hz = hd[2] + ha[2];
-    // six-neighbour exchange (difference form: uniform M gives exactly 0; reading Q11)
-    float e3[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const float mc = m[c][s];
-      const float xl = s ? m[c][0] : nx0[c];                    // x-1
-      const float xr = s ? nx1[c] : (hasB ? m[c][1] : nx1[c]);  // x+1
-      float e = 0.f;
-      e += g.cx * (xl - mc);
-      e += g.cx * (xr - mc);
-      e += g.cy * (ny0[c][s] - mc);
-      e += g.cy * (ny1[c][s] - mc);
-      e += g.cz * (nz0[c][s] - mc);
-      e += g.cz * (nz1[c][s] - mc);
-      e3[c] = e;
-    }
-    hx += e3[0];
-    hy += e3[1];
-    hz += e3[2];
-    if (cc.mode == 1) {
-      out[s][0] = hx;
-      out[s][1] = hy;
-      out[s][2] = hz;
-      continue;
-    }
-    // Eq. (3): dM/dt = c_prec (M x H) + c_damp M x (M x H); Euler; renormalise (Q16)
-    const float ax = my * hz - mz * hy, ay = mz * hx - mx * hz, az = mx * hy - my * hx;
-    const float bx = my * az - mz * ay, by = mz * ax - mx * az, bz = mx * ay - my * ax;
-    const float sx = mx + p.dt * (p.c_prec * ax + p.c_damp * bx);
-    const float sy = my + p.dt * (p.c_prec * ay + p.c_damp * by);
-    const float sz = mz + p.dt * (p.c_prec * az + p.c_damp * bz);
-    const float sc = g.Ms / sqrtf(sx * sx + sy * sy + sz * sz);
-    out[s][0] = sx * sc;
-    out[s][1] = sy * sc;
-    out[s][2] = sz * sc;
-    if (!(isfinite(out[s][0]) && isfinite(out[s][1]) && isfinite(out[s][2])) && (s == 0 || hasB))
-      atomicMin(cc.flag, ((unsigned long long)(p.step - 1) << 36) | (unsigned long long)(i + s));
-  }
-  float* dst = cc.mode == 1 ? cc.Hout : cc.Mn;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    float* q = dst + c * cc.N + i;
-    if (vec) {
-      *reinterpret_cast<float2*>(q) = make_float2(out[0][c], out[1][c]);
-    } else {
-      q[0] = out[0][c];
-      if (hasB) q[1] = out[1][c];
-    }
-  }
-}
-
-template <int L, int B, int NT, int MINB, bool DIST, bool EPI>
-__global__ void __launch_bounds__(NT, MINB) k5_inv_x_llg(const float2* __restrict__ X1, const float* __restrict__ M,
-                                                         float* __restrict__ Mn, float* __restrict__ Hout,
-                                                         const float2* __restrict__ tw, Geom g,
-                                                         const StepParams* __restrict__ prm,
-                                                         unsigned long long* __restrict__ flag, int mode,
-                                                         const float* __restrict__ Hlo,
-                                                         const float* __restrict__ Hhi) {
+// This non-persistent kernel covers the rows the bulk-copy kernel (k_x_bulk)
+// does not take: nx % 4 != 0, L < 64, nx == 1.
+template <int L, int B, int NT, int MINB, bool DIST>
+__global__ void __launch_bounds__(NT, MINB) k5_inv_x(const float2* __restrict__ X1, float* __restrict__ Hout,
+                                                     const float2* __restrict__ tw, Geom g) {
   pdl_trigger();
   pdl_wait();
   extern __shared__ float2 smem[];
@@ -795,21 +683,12 @@ __global__ void __launch_bounds__(NT, MINB) k5_inv_x_llg(const float2* __restric
   const int row0 = blockIdx.x * B;
   const size_t N = (size_t)nrows * g.nx;
   const size_t cstrideX = (size_t)nrows * g.pitch1;  // X1 component stride
-  const StepParams p = *prm;
-  const CellCtx cc{M, Mn, Hout, Hlo, Hhi, flag, N, (size_t)g.nx * g.ny, mode};
   if constexpr (L == 0) {  // nx == 1: H_demag = Re X[0]
     for (int b = threadIdx.x; b < B; b += NT) {
       const int row = row0 + b;
       if (row >= nrows) continue;
-      float h[3];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) h[c] = __ldg(X1 + c * cstrideX + (size_t)row * g.pitch1).x;
-      if (!EPI || mode == 2) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) Hout[c * N + row] = h[c];
-        continue;
-      }
-      if constexpr (EPI) cell_pair<DIST>(cc, g, p, row, 0, false, h, h);
+      for (int c = 0; c < 3; ++c) Hout[c * N + row] = __ldg(X1 + c * cstrideX + (size_t)row * g.pitch1).x;
     }
   } else {
     const int twpx = g.Lmax / (2 * L);
@@ -846,53 +725,37 @@ __global__ void __launch_bounds__(NT, MINB) k5_inv_x_llg(const float2* __restric
     PS ps;
     fft_to_regs<L, B, NT, false, 3, true, false, true, false>(tm, smem, ld, tw, g.Lmax / L, ps);
     const int row = row0 + tm.b;
-    if (!EPI || mode == 2) {  // split step: store H_demag, K6 applies the local terms and the update
-      if (PS::active(tm) && row < nrows) {
-        const bool vec = (g.nx & 1) == 0;
-#pragma unroll
-        for (int q = 0; q < PS::UPT; ++q)
-#pragma unroll
-          for (int r = 0; r < PS::R / 2; ++r) {
-            const int x0 = 2 * (PS::sb(tm) + PS::C2(q, r));
-            if (x0 >= g.nx) continue;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              float* h = Hout + c * N + (size_t)row * g.nx + x0;
-              if (vec) *reinterpret_cast<float2*>(h) = ps.v[q][c][r];
-              else {
-                h[0] = ps.v[q][c][r].x;
-                if (x0 + 1 < g.nx) h[1] = ps.v[q][c][r].y;
-              }
-            }
-          }
-      }
-      return;
-    }
     if (PS::active(tm) && row < nrows) {
+      const bool vec = (g.nx & 1) == 0;
 #pragma unroll
       for (int q = 0; q < PS::UPT; ++q)
 #pragma unroll
         for (int r = 0; r < PS::R / 2; ++r) {
-          const int n = PS::sb(tm) + PS::C2(q, r);
-          const int x0 = 2 * n;
+          const int x0 = 2 * (PS::sb(tm) + PS::C2(q, r));
           if (x0 >= g.nx) continue;
-          const float hA[3] = {ps.v[q][0][r].x, ps.v[q][1][r].x, ps.v[q][2][r].x};
-          const float hB[3] = {ps.v[q][0][r].y, ps.v[q][1][r].y, ps.v[q][2][r].y};
-          if constexpr (EPI) cell_pair<DIST>(cc, g, p, row, x0, x0 + 1 < g.nx, hA, hB);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            float* h = Hout + c * N + (size_t)row * g.nx + x0;
+            if (vec) *reinterpret_cast<float2*>(h) = ps.v[q][c][r];
+            else {
+              h[0] = ps.v[q][c][r].x;
+              if (x0 + 1 < g.nx) h[1] = ps.v[q][c][r].y;
+            }
+          }
         }
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// K1 / K5 (split step) as persistent bulk-copy kernels.  One tile = RB rows of
+// K1 / K5 as persistent bulk-copy kernels.  One tile = RB rows of
 // the flattened (component, z, y) row index (each row transformed on its own,
 // V = 1), 512 threads, two tile buffers: while the FFT of tile t runs in place
 // in one buffer, one-dimensional bulk copies (cp.async.bulk, mbarrier
 // completion) bring the CTA's next tile into the other, so the row reads of
 // HBM overlap the radix passes instead of stalling the first one.
 //   FWD (K1): rows of M (nx floats) -> R2C post-process -> X1 rows
-//   !FWD (K5, mode 2): X1 rows (Kx = L + 1 complex; DIST: P blocks of kb)
+//   !FWD (K5): X1 rows (Kx = L + 1 complex; DIST: P blocks of kb)
 //              -> C2R pre-process -> H_demag rows (nx floats)
 // Requires nx % 4 == 0 (16-byte row copies); the launchers fall back to the
 // non-persistent kernels otherwise.
@@ -1080,7 +943,7 @@ __global__ void __launch_bounds__(XBulk<L>::NT, GRACE_XB_MINB)
 }
 
 // ---------------------------------------------------------------------------
-// K6 (split step): Eq. (2) local terms + Eq. (3) + Euler from H_demag in HBM.
+// K6: Eq. (2) local terms + Eq. (3) + Euler from H_demag in HBM.
 // A streaming stencil: each thread owns 4 consecutive cells of a row (16-byte
 // loads), components are processed one after another to keep registers low.
 // mode 0: M -> Mn; mode 1: store H_eff into Hout.
@@ -1259,14 +1122,8 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
 #ifndef GRACE_EPT_K1
 #define GRACE_EPT_K1 8
 #endif
-#ifndef GRACE_EPT_K5
-#define GRACE_EPT_K5 16
-#endif
 #ifndef GRACE_MINB_K1
 #define GRACE_MINB_K1 3  // CTAs/SM the register budget of K1 (256 threads) is sized for
-#endif
-#ifndef GRACE_MINB_K5
-#define GRACE_MINB_K5 2
 #endif
 #ifndef GRACE_MINB_Z
 #define GRACE_MINB_Z 4
@@ -1317,8 +1174,6 @@ constexpr bool x_small() { return GRACE_EPT_SMALL > 0 && L > 0 && L <= 32; }
 template <int L>
 using X1Cfg = XCfgT<L, x_small<L>() ? GRACE_EPT_SMALL : GRACE_EPT_K1, GRACE_MINB_K1,
                     x_small<L>() ? GRACE_NT_SMALL : 256>;
-template <int L>
-using X5Cfg = XCfgT<L, GRACE_EPT_K5, GRACE_MINB_K5>;
 #ifndef GRACE_EPT_K5S
 #define GRACE_EPT_K5S 16
 #endif
@@ -1327,7 +1182,7 @@ using X5Cfg = XCfgT<L, GRACE_EPT_K5, GRACE_MINB_K5>;
 #endif
 template <int L>
 using X5SCfg = XCfgT<L, x_small<L>() ? GRACE_EPT_SMALL : GRACE_EPT_K5S, GRACE_MINB_K5S,
-                     x_small<L>() ? GRACE_NT_SMALL : 256>;  // K5 of the split step (no LLG epilogue)
+                     x_small<L>() ? GRACE_NT_SMALL : 256>;  // K5 (C2R -> H_demag)
 template <int L>
 struct YCfg {  // K2/K4 columns
   static constexpr int NCOL = cmax(2, cmin(32, GRACE_Y_ELEMS / L));
@@ -1622,7 +1477,7 @@ cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* 
 }
 
 bool fused_y_path(const Geom& g) { return g.Pz == 1 && g.Py <= 512; }
-int kernel_count(const Geom& g) { return (fused_y_path(g) ? 3 : 5) + (g.split_llg ? 1 : 0); }
+int kernel_count(const Geom& g) { return (fused_y_path(g) ? 3 : 5) + 1; }
 
 template <int HEUN, bool MASK>
 static cudaError_t k6_launch(const Geom& g, int mode, const float* Hd, const float* M, float* Mn, float* Hout,
@@ -1673,43 +1528,29 @@ cudaError_t launch_k2f(const Geom& g, float2* X1, const float* KS, const float2*
 #undef CASE
 }
 
-template <int L, bool DIST, bool EPI>
-static cudaError_t k5_launch(const Geom& g, int mode, const float2* X1, const float* M, float* Mn, float* Hout,
-                             const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st,
-                             const float* Hlo, const float* Hhi) {
-  using C = std::conditional_t<EPI, X5Cfg<L>, X5SCfg<L>>;
+template <int L, bool DIST>
+static cudaError_t k5_launch(const Geom& g, const float2* X1, float* Hd, const float2* tw, cudaStream_t st) {
+  if constexpr (L >= kXBulkMinL && L <= kXBulkMaxL) {
+    if (xbulk_ok<L>(g, false)) return xbulk_launch<L, false, DIST>(g, X1, Hd, tw, nullptr, st);
+  }
+  using C = X5SCfg<L>;
   const size_t smem = (L == 0) ? 0 : (size_t)3 * TileIdx<(L > 0 ? L : 1), C::B, false>::ELEMS * sizeof(float2);
-  auto kern = k5_inv_x_llg<L, C::B, C::NT, C::MINB, DIST, EPI>;
+  auto kern = k5_inv_x<L, C::B, C::NT, C::MINB, DIST>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
   const int nrows = g.nzl * g.ny;
-  GRACE_TRY(launch_k(16, kern, (nrows + C::B - 1) / C::B, C::NT, smem, st, X1, M, Mn, Hout, tw, g, prm, flag, mode, Hlo, Hhi));
+  GRACE_TRY(launch_k(16, kern, (nrows + C::B - 1) / C::B, C::NT, smem, st, X1, Hd, tw, g));
   return cudaGetLastError();
 }
 
-template <int L, bool DIST>
-static cudaError_t k5_launch2(const Geom& g, int mode, const float2* X1, const float* M, float* Mn, float* Hout,
-                              const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st,
-                              const float* Hlo, const float* Hhi) {
-  if constexpr (L >= kXBulkMinL && L <= kXBulkMaxL) {
-    if (mode == 2 && xbulk_ok<L>(g, false)) return xbulk_launch<L, false, DIST>(g, X1, Hout, tw, nullptr, st);
-  }
-  if (mode == 2) return k5_launch<L, DIST, false>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi);
-  return k5_launch<L, DIST, true>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi);
-}
-
-cudaError_t launch_k5(const Geom& g, int mode, const float2* X1, const float* M, float* Mn, float* Hout,
-                      const float2* tw, const StepParams* prm, unsigned long long* flag, cudaStream_t st,
-                      const float* Hlo, const float* Hhi) {
-  if (g.Px == 1)
-    return g.kb ? k5_launch2<0, true>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi)
-                : k5_launch2<0, false>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi);
+cudaError_t launch_k5(const Geom& g, const float2* X1, float* Hd, const float2* tw, cudaStream_t st) {
+  if (g.Px == 1) return g.kb ? k5_launch<0, true>(g, X1, Hd, tw, st) : k5_launch<0, false>(g, X1, Hd, tw, st);
   const int L = g.Px / 2;
-#define CASE(v)                                                                                               \
-  case v:                                                                                                     \
-    return (v < 2) ? cudaErrorInvalidValue                                                                    \
-           : g.kb  ? k5_launch2<(v >= 2 ? v : 2), true>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi) \
-                   : k5_launch2<(v >= 2 ? v : 2), false>(g, mode, X1, M, Mn, Hout, tw, prm, flag, st, Hlo, Hhi);
+#define CASE(v)                                                          \
+  case v:                                                                \
+    return (v < 2) ? cudaErrorInvalidValue                               \
+           : g.kb  ? k5_launch<(v >= 2 ? v : 2), true>(g, X1, Hd, tw, st) \
+                   : k5_launch<(v >= 2 ? v : 2), false>(g, X1, Hd, tw, st);
   GRACE_L_SWITCH(L, CASE)
 #undef CASE
 }

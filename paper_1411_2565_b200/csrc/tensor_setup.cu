@@ -312,16 +312,19 @@ __global__ void k_fft64(double2* A, int L, int logL, long long nlines, long long
   }
 }
 
-// S5: KS[c][kz'][ky'][kx] = -Re A[kz'][ky'][kx] / (Px Py Pz), rounded to fp32.
-__global__ void k_fold(float* KSc, const double2* A, Geom g) {
-  const long long tot = (long long)g.Kzh * g.Kyh * g.KSp;
+// S5: KS[c][kz'][ky'][kx - kx0] = -Re A[kz'][ky'][kx] / (Px Py Pz), rounded to fp32,
+// for the columns kx0 .. kx0 + ncol - 1 (one rank's kx block; pitch KSp, the
+// padding columns zero).
+__global__ void k_fold(float* KSc, const double2* A, Geom g, int kx0, int ncol, int KSp) {
+  const long long tot = (long long)g.Kzh * g.Kyh * KSp;
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= tot) return;
-  const int kx = (int)(idx % g.KSp);
-  const int ky = (int)((idx / g.KSp) % g.Kyh);
-  const int kz = (int)(idx / ((long long)g.KSp * g.Kyh));
+  const int col = (int)(idx % KSp);
+  const int ky = (int)((idx / KSp) % g.Kyh);
+  const int kz = (int)(idx / ((long long)KSp * g.Kyh));
+  const int kx = kx0 + col;
   float v = 0.f;
-  if (kx < g.Kx) {
+  if (col < ncol && kx < g.Kx) {
     const double P = (double)g.Px * (double)g.Py * (double)g.Pz;
     v = (float)(-A[((long long)kz * g.Py + ky) * g.Px + kx].x / P);
   }
@@ -372,10 +375,10 @@ static cudaError_t fft64_axis(double2* A, int L, long long nlines, long long inn
   return cudaGetLastError();
 }
 
-cudaError_t kernel_spectrum_device(const Geom& g, const double* oct, double2* work, float* KS, cudaStream_t st) {
+cudaError_t kernel_spectrum_device(const Geom& g, const double* oct, double2* work, int nout, const KsOut* out,
+                                   cudaStream_t st) {
   const long long tot = (long long)g.Px * g.Py * g.Pz;
   const long long N = (long long)g.nx * g.ny * g.nz;
-  const long long kslen = (long long)g.Kzh * g.Kyh * g.KSp;
   for (int c = 0; c < 6; ++c) {
     k_embed<<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(work, oct + c * N, c, g.nx, g.ny, g.nz, g.Px, g.Py, g.Pz);
     cudaError_t e = cudaGetLastError();
@@ -387,8 +390,12 @@ cudaError_t kernel_spectrum_device(const Geom& g, const double* oct, double2* wo
       return e;
     if ((e = fft64_axis(work, g.Pz, (long long)g.Py * kx, kx, g.Px, (long long)g.Px * g.Py, st)) != cudaSuccess)
       return e;
-    k_fold<<<(unsigned)cdiv(kslen, 256), 256, 0, st>>>(KS + c * kslen, work, g);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    for (int o = 0; o < nout; ++o) {
+      const long long kslen = (long long)g.Kzh * g.Kyh * out[o].KSp;
+      k_fold<<<(unsigned)cdiv(kslen, 256), 256, 0, st>>>(out[o].KS + c * kslen, work, g, out[o].kx0, out[o].ncol,
+                                                         out[o].KSp);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
   }
   return cudaSuccess;
 }

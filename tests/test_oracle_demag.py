@@ -87,3 +87,19 @@ def test_linearity_reciprocity_energy():
     for _ in range(5):
         M = RNG.standard_normal((3, nz, ny, nx))
         assert -0.5 * (M * op(M)).sum() >= 0.0
+
+
+def test_demagfft_workers_same_result():
+    """The all-core CPU baseline (scipy.fft, workers=k) computes the same convolution."""
+    import numpy as np
+
+    from oracle.demag import DemagFFT
+    from oracle.tensor import tensor_octant
+    from workloads import random_m
+
+    n, d = (12, 10, 6), (1e-9, 2e-9, 3e-9)
+    oct_ = tensor_octant(*n, *d)
+    M = random_m(n, 8e5, seed=4)
+    a = DemagFFT(oct_)(M)
+    b = DemagFFT(oct_, workers=4)(M)
+    assert np.abs(a - b).max() <= 1e-9 * np.abs(a).max()
