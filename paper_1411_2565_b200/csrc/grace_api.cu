@@ -143,6 +143,8 @@ struct Rank {
   unsigned char* mask = nullptr;       // geometry mask [nzl][ny][nx] (grace_set_geometry; null: none)
   bool tma = false;                    // TMA descriptors of the K2 / K4 inputs built
   TmapBlob k2map{}, k4map{};
+  bool tma3 = false;                   // TMA descriptors of the K3 pencils and KS slices built
+  TmapBlob k3x{}, k3k{};
 };
 
 struct grace_ctx {
@@ -313,7 +315,7 @@ struct grace_ctx {
         CE(launch_k2(rk.g, rk.A, rk.X2, tw, s, rk.tma ? &rk.k2map : nullptr));
         rec(3);
         rec(4);
-        CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s));
+        CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s, rk.tma3 ? &rk.k3x : nullptr, rk.tma3 ? &rk.k3k : nullptr));
         rec(5);
         rec(6);
         CE(launch_k4(rk.g, rk.X2, rk.A, tw, s, rk.tma ? &rk.k4map : nullptr));
@@ -327,7 +329,7 @@ struct grace_ctx {
     for (auto& rk : ranks) {
       if (rk.g.Kc > 0) {
         CE(launch_k2(rk.g, rk.B, rk.X2, tw, s, rk.tma ? &rk.k2map : nullptr));
-        CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s));
+        CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s, rk.tma3 ? &rk.k3x : nullptr, rk.tma3 ? &rk.k3k : nullptr));
         CE(launch_k4(rk.g, rk.X2, rk.B, tw, s, rk.tma ? &rk.k4map : nullptr));
       }
     }
@@ -585,8 +587,10 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
   if ((rc = h->alloc((void**)&h->tw, sizeof(float2) * g0.Lmax))) return bail(rc);
   // TMA descriptors for the y-pencil kernels (K2 reads the x-row layout, K4 reads X2)
   if (!h->fused && !getenv("GRACE_NO_TMA"))
-    for (auto& rk : h->ranks)
+    for (auto& rk : h->ranks) {
       rk.tma = make_ky_tmaps(rk.g, dlay ? rk.B : rk.A, rk.X2, &rk.k2map, &rk.k4map) == cudaSuccess;
+      rk.tma3 = rk.X2 && make_k3_tmaps(rk.g, rk.X2, rk.KS, &rk.k3x, &rk.k3k) == cudaSuccess;
+    }
   cudaGetLastError();
   h->N = (mode == grace_ctx::kNccl) ? h->ranks[0].Nl : (long long)nx * ny * nz;
 

@@ -75,7 +75,11 @@ struct alignas(64) TmapBlob {
 cudaError_t make_ky_tmaps(const Geom& g, const float2* k2_in, const float2* x2, TmapBlob* k2map, TmapBlob* k4map);
 cudaError_t launch_k2(const Geom& g, const float2* X1, float2* X2, const float2* tw, cudaStream_t st,
                       const TmapBlob* tmap = nullptr);
-cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* tw, cudaStream_t st);
+// K3 tensor maps (X2 pencils, KS slices) for the TMA-fed kernel; cudaErrorNotSupported
+// where K3 takes the LDG kernel (unfused long pencils, short L, nz == 1).
+cudaError_t make_k3_tmaps(const Geom& g, const float2* X2, const float* KS, TmapBlob* xmap, TmapBlob* kmap);
+cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* tw, cudaStream_t st,
+                      const TmapBlob* xmap = nullptr, const TmapBlob* kmap = nullptr);
 cudaError_t launch_k4(const Geom& g, const float2* X2, float2* X1, const float2* tw, cudaStream_t st,
                       const TmapBlob* tmap = nullptr);
 cudaError_t launch_k2f(const Geom& g, float2* X1, const float* KS, const float2* tw, cudaStream_t st);

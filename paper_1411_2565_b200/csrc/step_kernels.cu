@@ -78,6 +78,15 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // K1: x R2C.  A real row of Px (nx nonzero) is packed as z[n] = x[2n] + i x[2n+1],
 // a length-L = Px/2 complex FFT gives Z, and
@@ -485,10 +494,12 @@ struct ZPlan {
   static constexpr int NT = B * TPC < 32 ? 32 : B * TPC;
 };
 
-template <int L, int B, int NT, class LD, class ST>
+// kw(): called before the multiply's barrier -- waits for this thread's part of
+// the KS slice (cp.async group or TMA mbarrier).
+template <int L, int B, int NT, class LD, class ST, class KW>
 __device__ __forceinline__ void pencil_conv(float2* smem, const LD& ld, const ST& st, const float* kss, int KH,
                                             const float2* __restrict__ tw, int twstride, int P_other, int k_other,
-                                            bool fold_is_y, bool wait_ks) {
+                                            bool fold_is_y, const KW& kw) {
   // k along the pencil axis (length L = P_axis); the other folded axis index is
   // fixed for the CTA.  fold_is_y: the pencil axis is y (K2'), else z (K3).
   auto flags = [&](int k, bool& fy, bool& fz, int& kf) {
@@ -510,7 +521,7 @@ __device__ __forceinline__ void pencil_conv(float2* smem, const LD& ld, const ST
     static_assert(PF::R == PI::R && PF::UPT == 1 && PI::UPT == 1, "fused plan");
     PF pf;
     fft_to_regs<L, B, NT, true, 3, false, true, false, false>(tm, smem, ld, tw, twstride, pf);
-    if (wait_ks) cp_async_wait_all();
+    kw();
     __syncthreads();
     PI pi;
 #pragma unroll
@@ -529,7 +540,7 @@ __device__ __forceinline__ void pencil_conv(float2* smem, const LD& ld, const ST
   } else {
     using T = TileIdx<L, B, true>;
     fft_tile<L, B, NT, true, false, (L > 1), false, 3>(smem, ld, SmemSt<L, B, true>{smem}, tw, twstride);
-    if (wait_ks) cp_async_wait_all();
+    kw();
     __syncthreads();
     for (int u = threadIdx.x; u < L * B; u += NT) {
       const int k = u / B, b = u - k * B;
@@ -594,7 +605,116 @@ __global__ void __launch_bounds__(NT, MINB) k3_z(float2* __restrict__ X2, const 
       }
     } st{base, zstride, cstride, g.nz, nvalid};
     if (rep) __syncthreads();
-    pencil_conv<L, B, NT>(smem, ld, st, kss, KZH, tw, g.Lmax / L, g.Py, ky, false, rep == 0);
+    pencil_conv<L, B, NT>(smem, ld, st, kss, KZH, tw, g.Lmax / L, g.Py, ky, false, [&] {
+      if (rep == 0) cp_async_wait_all();
+    });
+  }
+}
+
+// K3 fed by TMA (fused short pencils, L <= 64).  The same pencil convolution as
+// k3_z, but every global read is a tensor-map copy issued by one thread, so the
+// HBM latency overlaps this and the other resident CTAs' work and no thread
+// spends instructions on address arithmetic, bounds checks or LDGs:
+//   * the KS slice [6][Kzh][B] (box {B, 1, Kzh, 6} of KS) before the PDL wait
+//     (it is constant), landing in the kss layout kmul_s reads;
+//   * the ky pencils of the three components (boxes {B, 1, L/2, 1} of X2, rows
+//     z >= nz and columns kx >= Kc zero-filled by the TMA unit) straight into
+//     the work tile, where the forward first pass runs in place;
+//   * with PRE, the mirror ky' = Py - ky pencils at the same time into a staging
+//     buffer, so the second pencil set never waits on HBM.
+// Outputs (z < nz) are stored from the inverse last pass as in k3_z.
+template <int L>
+struct Z3Tma {
+  static constexpr int B = ZPlan<L>::B;
+  static constexpr int NT = ZPlan<L>::NT;
+  using T = TileIdx<L, B, true>;
+  static_assert(!T::PAD, "TMA boxes land in the linear tile layout");
+  static constexpr int H = L / 2;  // rows per pencil box (nz <= L/2)
+  static constexpr int KZH = L / 2 + 1;
+  static constexpr size_t WORK = 3 * (size_t)T::ELEMS * 8;
+  static constexpr size_t STAGE = 3 * (size_t)H * B * 8;
+  static constexpr size_t KSB = 6 * (size_t)KZH * B * 4;
+  static constexpr size_t KSB16 = (KSB + 15) / 16 * 16;
+  static constexpr bool PRE = (WORK + STAGE + KSB16 + 64) * 4 <= 220 * 1024;
+  static constexpr size_t KSOFF = WORK + (PRE ? STAGE : 0);
+  static constexpr size_t SMEM = KSOFF + KSB16 + 64;
+};
+
+template <int L, int MINB>
+__global__ void __launch_bounds__(Z3Tma<L>::NT, MINB)
+    k3_z_tma(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
+             float2* __restrict__ X2, const float2* __restrict__ tw, Geom g) {
+  using Z = Z3Tma<L>;
+  constexpr int B = Z::B, NT = Z::NT, H = Z::H;
+  constexpr unsigned TXP = 3u * H * B * 8;  // bytes of one pencil set
+  extern __shared__ __align__(128) unsigned char smraw[];
+  float2* work = reinterpret_cast<float2*>(smraw);
+  float2* stage = reinterpret_cast<float2*>(smraw + Z::WORK);
+  float* kss = reinterpret_cast<float*>(smraw + Z::KSOFF);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + Z::KSOFF + Z::KSB16);  // KS, work, stage
+  const int kx0 = blockIdx.x * B;
+  const int kyf = blockIdx.y;
+  const int nky = (kyf == 0 || 2 * kyf == g.Py) ? 1 : 2;
+  const size_t zstride = (size_t)g.Py * g.pitch2;
+  const size_t cstride = (size_t)g.nz * zstride;
+  const int nvalid = g.Kc - kx0;
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    mbar_init(bar + 2, 1);
+    mbar_fence_init();
+    mbar_expect_tx(bar, (unsigned)Z::KSB);
+    tma_load_4d(kss, &kmap, bar, kx0, kyf, 0, 0);
+  }
+  __syncthreads();
+  pdl_wait();  // X2 comes from K2
+  auto issue = [&](float2* dst, int ky, uint64_t* b, int cstep) {
+    mbar_expect_tx(b, TXP);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) tma_load_4d(dst + c * cstep, &xmap, b, kx0, ky, 0, c);
+  };
+  if (threadIdx.x == 0) {
+    issue(work, kyf, bar + 1, Z::T::ELEMS);
+    if (Z::PRE && nky == 2) issue(stage, g.Py - kyf, bar + 2, H * B);
+  }
+  struct StageLd {  // staged mirror pencils [c][z][b] (a different buffer: no in-place hazard)
+    __device__ static constexpr bool kSmem() { return false; }
+    const float2* s;
+    __device__ float2 operator()(int b, int c, int ib, int C) const { return s[(c * H + ib + C) * B + b]; }
+  };
+  struct St {
+    __device__ static constexpr bool kSmem() { return false; }
+    float2* p;
+    size_t zs, cs;
+    int nz, nvalid;
+    __device__ void operator()(int b, int c, int ib, int C, float2 v) const {
+      const int i = ib + C;
+      if (i < nz && b < nvalid) p[c * cs + (b + i * zs)] = v;
+    }
+  };
+  for (int rep = 0; rep < nky; ++rep) {
+    const int ky = rep == 0 ? kyf : g.Py - kyf;
+    const St st{X2 + (size_t)ky * g.pitch2 + kx0, zstride, cstride, g.nz, nvalid};
+    auto kw = [&] {
+      if (rep == 0) mbar_wait(bar, 0);
+    };
+    if (rep == 0) {
+      mbar_wait(bar + 1, 0);
+      pencil_conv<L, B, NT>(work, SmemLd<L, B, true>{work}, st, kss, Z::KZH, tw, g.Lmax / L, g.Py, ky, false, kw);
+    } else if constexpr (Z::PRE) {
+      __syncthreads();  // the work tile is free
+      mbar_wait(bar + 2, 0);
+      pencil_conv<L, B, NT>(work, StageLd{stage}, st, kss, Z::KZH, tw, g.Lmax / L, g.Py, ky, false, kw);
+    } else {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        fence_proxy_async();
+        issue(work, ky, bar + 1, Z::T::ELEMS);
+      }
+      mbar_wait(bar + 1, 1);
+      pencil_conv<L, B, NT>(work, SmemLd<L, B, true>{work}, st, kss, Z::KZH, tw, g.Lmax / L, g.Py, ky, false, kw);
+    }
   }
 }
 
@@ -663,7 +783,7 @@ __global__ void __launch_bounds__(NT, MINB) k2f_y_fused(float2* __restrict__ X1,
       if (i < ny && b < nvalid) p[c * cs + (b + i * pitch)] = v;
     }
   } st{base, cstride, g.pitch1, g.ny, nvalid};
-  pencil_conv<L, B, NT>(smem, ld, st, kss, KYH, tw, g.Lmax / L, 1, 0, true, true);
+  pencil_conv<L, B, NT>(smem, ld, st, kss, KYH, tw, g.Lmax / L, 1, 0, true, [] { cp_async_wait_all(); });
 }
 
 // ---------------------------------------------------------------------------
@@ -1425,6 +1545,32 @@ static cudaError_t encode5(TmapBlob* out, const void* base, const unsigned long 
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// Host: N-D tensor map (rank 1..5) over `dtype` elements, box `box`, no swizzle.
+static cudaError_t encode_map(TmapBlob* out, CUtensorMapDataType dtype, int rank, const void* base,
+                              const unsigned long long* dims, const unsigned long long* strides,
+                              const unsigned* box) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+    enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  cuuint64_t gd[5], gs[4];
+  cuuint32_t bx[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    gd[i] = dims[i];
+    bx[i] = box[i];
+    es[i] = 1;
+  }
+  for (int i = 0; i + 1 < rank; ++i) gs[i] = strides[i];
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(out->b), dtype, rank, const_cast<void*>(base), gd, gs, bx, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, GRACE_TMA_PROMO,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <int L>
 static cudaError_t ky_maps(const Geom& g, const float2* k2_in, const float2* x2, TmapBlob* k2map, TmapBlob* k4map) {
   constexpr int NCOL = ytma_ncol<L>();
@@ -1454,9 +1600,63 @@ cudaError_t make_ky_tmaps(const Geom& g, const float2* k2_in, const float2* x2, 
 #undef CASE
 }
 
+#ifndef GRACE_K3_TMA_MINL
+#define GRACE_K3_TMA_MINL 32  // shortest z pencil fed by TMA (L = 16 keeps k3_z: 2 CTAs/SM of 77 KB either way)
+#endif
 template <int L>
-static cudaError_t k3_launch(const Geom& g, float2* X2, const float* KS, const float2* tw, cudaStream_t st) {
+constexpr bool k3_tma_ok() {
+  return ZPlan<L>::FUSE && L >= GRACE_K3_TMA_MINL && L >= 16;
+}
+
+// K3 tensor maps: X2 [3][nz][Py][pitch2] complex as 4-D {kx < Kc, ky, z, c}, box
+// {B, 1, Pz/2, 1}; KS [6][Kzh][Kyh][KSp] fp32 as 4-D {kx, ky', kz', c}, box
+// {B, 1, Kzh, 6}.
+template <int L>
+static cudaError_t k3_maps(const Geom& g, const float2* X2, const float* KS, TmapBlob* xmap, TmapBlob* kmap) {
+  if constexpr (!k3_tma_ok<L>()) {
+    return cudaErrorNotSupported;
+  } else {
+    using Z = Z3Tma<L>;
+    const unsigned long long p2 = 8ull * g.pitch2;
+    const unsigned long long xd[4] = {(unsigned long long)g.Kc, (unsigned long long)g.Py, (unsigned long long)g.nz, 3};
+    const unsigned long long xs[3] = {p2, p2 * g.Py, p2 * g.Py * g.nz};
+    const unsigned xb[4] = {(unsigned)Z::B, 1, (unsigned)Z::H, 1};
+    cudaError_t e = encode_map(xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, X2, xd, xs, xb);
+    if (e != cudaSuccess) return e;
+    const unsigned long long pk = 4ull * g.KSp;
+    const unsigned long long kd[4] = {(unsigned long long)g.KSp, (unsigned long long)g.Kyh, (unsigned long long)g.Kzh,
+                                      6};
+    const unsigned long long ks[3] = {pk, pk * g.Kyh, pk * g.Kyh * g.Kzh};
+    const unsigned kbx[4] = {(unsigned)Z::B, 1, (unsigned)Z::KZH, 6};
+    return encode_map(kmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, KS, kd, ks, kbx);
+  }
+}
+
+cudaError_t make_k3_tmaps(const Geom& g, const float2* X2, const float* KS, TmapBlob* xmap, TmapBlob* kmap) {
+  if (g.Pz < 2 || g.Kc < 1 || fused_y_path(g)) return cudaErrorNotSupported;
+#define CASE(v) case v: return (v >= 2 && v <= 1024) ? k3_maps<(v >= 2 && v <= 1024 ? v : 2)>(g, X2, KS, xmap, kmap) : cudaErrorNotSupported;
+  GRACE_L_SWITCH(g.Pz, CASE)
+#undef CASE
+}
+
+template <int L>
+static cudaError_t k3_launch(const Geom& g, float2* X2, const float* KS, const float2* tw, cudaStream_t st,
+                             const TmapBlob* xmap, const TmapBlob* kmap) {
   using C = ZCfg<L>;
+  if constexpr (k3_tma_ok<L>()) {
+    if (xmap != nullptr && kmap != nullptr && !getenv("GRACE_NO_K3_TMA")) {
+      using Z = Z3Tma<L>;
+      auto kern = k3_z_tma<L, C::MINB>;
+      cudaError_t e = prep(kern, Z::SMEM);
+      if (e != cudaSuccess) return e;
+      CUtensorMap xm, km;
+      memcpy(&xm, xmap->b, sizeof xm);
+      memcpy(&km, kmap->b, sizeof km);
+      dim3 grid((g.Kc + Z::B - 1) / Z::B, g.Kyh);
+      GRACE_TRY(launch_k(4, kern, grid, Z::NT, Z::SMEM, st, xm, km, X2, tw, g));
+      return cudaGetLastError();
+    }
+  }
   auto kern = k3_z<L, C::B, C::NT, C::MINB>;
   cudaError_t e = prep(kern, C::SMEM);
   if (e != cudaSuccess) return e;
@@ -1465,13 +1665,14 @@ static cudaError_t k3_launch(const Geom& g, float2* X2, const float* KS, const f
   return cudaGetLastError();
 }
 
-cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* tw, cudaStream_t st) {
+cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* tw, cudaStream_t st,
+                      const TmapBlob* xmap, const TmapBlob* kmap) {
   if (g.Pz == 1) {
     dim3 grid((g.Kc + 127) / 128, g.Py);
     GRACE_TRY(launch_k(4, k_mul_plane, grid, 128, 0, st, X2, KS, g));
     return cudaGetLastError();
   }
-#define CASE(v) case v: return (v >= 2 && v <= 1024) ? k3_launch<(v >= 2 && v <= 1024 ? v : 2)>(g, X2, KS, tw, st) : cudaErrorInvalidValue;
+#define CASE(v) case v: return (v >= 2 && v <= 1024) ? k3_launch<(v >= 2 && v <= 1024 ? v : 2)>(g, X2, KS, tw, st, xmap, kmap) : cudaErrorInvalidValue;
   GRACE_L_SWITCH(g.Pz, CASE)
 #undef CASE
 }
