@@ -37,7 +37,7 @@ def label(name):
         return "K3"
     if "k2f_y_fused" in name:
         return "K2f"
-    if "k5_inv_x_llg" in name:
+    if "k5_inv_x" in name:
         return "K5"
     if "k6_llg" in name:
         return "K6"
