@@ -187,9 +187,21 @@ int grace_kernel_times(grace_ctx *h, double *ms, long long *launches, int *nk, i
 /* ---- distributed z-slab path ------------------------------------
  * The grid is split into P slabs of nz/P planes (nz % P == 0).  One step: K1 on
  * each slab, all-to-all to kx blocks of ceil(Kx/P) columns (C1), K2..K4 on the
- * block (all z), all-to-all back (C2), one-plane halo exchange of M (C3), K5 on
- * each slab.  Results are identical to the single-GPU path (same per-pencil
- * arithmetic). */
+ * block (all z), all-to-all back (C2), one-plane halo exchange of M (C3), K5 + K6
+ * on each slab.  When K1 and K5 run as the bulk-copy kernels (nx % 4 == 0,
+ * 128 <= Px <= 8192) the transposes are pipelined per magnetisation component:
+ * C1 of component q runs on a communication stream while K1 computes q + 1 and
+ * K2 starts on q once it has landed; likewise C2 against K4 / K5 (GRACE_NO_PIPE
+ * turns this off).  C3 runs on its own stream and, on the NCCL path, its own
+ * communicator (ncclCommSplit).  The step is captured into CUDA graphs like the
+ * single-GPU step (GRACE_DIST_EAGER: eager launches).  Results are identical to
+ * the single-GPU path (same per-pencil arithmetic).
+ *
+ * Collective calls on the NCCL path (call them on every rank, in the same order):
+ * grace_create_dist, grace_step, grace_heff, grace_mavg, grace_energy,
+ * grace_max_torque, grace_relax, grace_set_geometry, grace_set_m,
+ * grace_set_m_device (their status is agreed over the ranks: a non-finite value
+ * or zero cell anywhere is reported by every rank, with the global cell index). */
 
 /* P ranks of one grid in this context on the current GPU; the exchanges are
  * device-to-device copies.  Same interface as grace_create (whole-grid arrays);
@@ -203,12 +215,14 @@ int grace_nccl_unique_id(void *out128);
 
 /* This process's rank of an nranks-way NCCL partition on the current GPU.
  * set_m/get_m/heff then address the local slab [3][nz/nranks][ny][nx] (z offset
- * rank*nz/nranks); grace_step and grace_mavg are collective (call on every rank). */
+ * rank*nz/nranks); see the collective calls above. */
 int grace_create_dist(int nx, int ny, int nz, double dx, double dy, double dz, double Ms, double A, double Ku,
                       double alpha, double gamma, int rank, int nranks, const void *nccl_id, grace_ctx **out);
 
-/* out[0..7] = P, rank, nz_local, z_offset, kx_block, kx_columns_here, pitch1, pitch2. */
-int grace_partition(grace_ctx *h, long long *out8);
+/* out[0..10] = P, rank, nz_local, z_offset, kx_block, kx_columns_here, pitch1, pitch2,
+ * transposes pipelined per component (0/1), step captured into graphs (0/1), halo on
+ * its own NCCL communicator (0/1). */
+int grace_partition(grace_ctx *h, long long *out11);
 
 #ifdef __cplusplus
 }

@@ -442,29 +442,30 @@ __device__ __forceinline__ void fft_passes(const ThreadMap<L, NCOL, NT, COLMODE>
 }
 
 // Passes P .. NH-1 of a transform, each writing the smem tile (pass 0 reads `ld`).
-template <int L, int P, int NH, bool REV, int NCOL, int NT, bool COLMODE, int V, bool INV, bool HIN, class LD,
-          class ST>
+template <int L, int P, int NH, bool REV, int NCOL, int NT, bool COLMODE, int V, bool INV, bool HIN, bool TWS,
+          class LD, class ST>
 __device__ __forceinline__ void fft_head(const ThreadMap<L, NCOL, NT, COLMODE>& tm, float2* s, const LD& ld,
                                          const ST& none, const float2* __restrict__ tw, int twstride) {
   if constexpr (P < NH) {
     constexpr int RB = rb_for(COLMODE, V);
     constexpr int IFACE0 = TileIdx<L, NCOL, COLMODE, Plan<L, REV, RB>::R(0)>::PAD ? kPad : kLin;
     if constexpr (P == 0) {
-      fft_pass<L, 0, REV, NCOL, NT, COLMODE, V, INV, HIN, false, kExt, IFACE0>(tm, ld, none, s, tw, twstride);
+      fft_pass<L, 0, REV, NCOL, NT, COLMODE, V, INV, HIN, false, kExt, IFACE0, TWS>(tm, ld, none, s, tw, twstride);
     } else {
       __syncthreads();
-      fft_pass<L, P, REV, NCOL, NT, COLMODE, V, INV, false, false, (P == 1 ? IFACE0 : kLin), kLin>(tm, ld, none, s,
-                                                                                                 tw, twstride);
+      fft_pass<L, P, REV, NCOL, NT, COLMODE, V, INV, false, false, (P == 1 ? IFACE0 : kLin), kLin, TWS>(
+          tm, ld, none, s, tw, twstride);
     }
-    fft_head<L, P + 1, NH, REV, NCOL, NT, COLMODE, V, INV, HIN>(tm, s, ld, none, tw, twstride);
+    fft_head<L, P + 1, NH, REV, NCOL, NT, COLMODE, V, INV, HIN, TWS>(tm, s, ld, none, tw, twstride);
   }
 }
 
 // Passes 0 .. NP-2 of a transform (the first from `ld`, writing the smem tile),
 // then the last pass is loaded and computed into `ps` and left in registers:
 // output element i = PS::sb(tm) + PS::C2(q, r) of component w is ps.v[q][w][r].
-template <int L, int NCOL, int NT, bool COLMODE, int V, bool INV, bool HIN, bool HOUT, bool REV, class LD,
-          class PS>
+// TWS: `tw` is the per-pass shared twiddle table of Plan<L, REV> (fill_pass_twiddles), else the global table.
+template <int L, int NCOL, int NT, bool COLMODE, int V, bool INV, bool HIN, bool HOUT, bool REV, bool TWS = false,
+          class LD, class PS>
 __device__ __forceinline__ void fft_to_regs(const ThreadMap<L, NCOL, NT, COLMODE>& tm, float2* s, const LD& ld,
                                             const float2* __restrict__ tw, int twstride, PS& ps) {
   constexpr int RB = rb_for(COLMODE, V);
@@ -473,18 +474,18 @@ __device__ __forceinline__ void fft_to_regs(const ThreadMap<L, NCOL, NT, COLMODE
   if constexpr (NP == 1) {
     if (PS::active(tm)) {
       ps.template load_ext<HIN ? PS::R / 2 : PS::R>(tm, ld);
-      ps.template compute<INV, HIN, HOUT>(tm, tw, twstride);
+      ps.template compute<INV, HIN, HOUT, TWS>(tm, tw, twstride);
     }
   } else {
     struct None {
       __device__ static constexpr bool kSmem() { return true; }
       __device__ void operator()(int, int, int, int, float2) const {}
     } none;
-    fft_head<L, 0, NP - 1, REV, NCOL, NT, COLMODE, V, INV, HIN>(tm, s, ld, none, tw, twstride);
+    fft_head<L, 0, NP - 1, REV, NCOL, NT, COLMODE, V, INV, HIN, TWS>(tm, s, ld, none, tw, twstride);
     __syncthreads();
     if (PS::active(tm)) {
       ps.template load_smem<PS::R, NP == 2 && IFACE0 == kPad>(tm, s);
-      ps.template compute<INV, false, HOUT>(tm, tw, twstride);
+      ps.template compute<INV, false, HOUT, TWS>(tm, tw, twstride);
     }
   }
 }
@@ -493,7 +494,8 @@ __device__ __forceinline__ void fft_to_regs(const ThreadMap<L, NCOL, NT, COLMODE
 // i = jb + PS::Cin(q, r)); compute it, then the remaining passes, the last one
 // writing through `st`.  The caller must __syncthreads() before if the smem
 // tile is still being read.
-template <int L, int NCOL, int NT, bool COLMODE, int V, bool INV, bool HOUT, bool REV, class ST, class PS>
+template <int L, int NCOL, int NT, bool COLMODE, int V, bool INV, bool HOUT, bool REV, bool TWS = false, class ST,
+          class PS>
 __device__ __forceinline__ void fft_from_regs(const ThreadMap<L, NCOL, NT, COLMODE>& tm, float2* s, const ST& st,
                                               const float2* __restrict__ tw, int twstride, PS& ps) {
   constexpr int RB = rb_for(COLMODE, V);
@@ -505,16 +507,16 @@ __device__ __forceinline__ void fft_from_regs(const ThreadMap<L, NCOL, NT, COLMO
   } none;
   if constexpr (NP == 1) {
     if (PS::active(tm)) {
-      ps.template compute<INV, false, HOUT>(tm, tw, twstride);
+      ps.template compute<INV, false, HOUT, TWS>(tm, tw, twstride);
       ps.template store_ext<HOUT ? PS::R / 2 : PS::R>(tm, st);
     }
   } else {
     if (PS::active(tm)) {
-      ps.template compute<INV, false, false>(tm, tw, twstride);
+      ps.template compute<INV, false, false, TWS>(tm, tw, twstride);
       ps.template store_smem<PS::R, IFACE0 == kPad>(tm, s);
     }
     __syncthreads();
-    fft_passes<L, 1, REV, NCOL, NT, COLMODE, V, INV, false, HOUT, kExt, kExt>(tm, s, none, st, tw, twstride);
+    fft_passes<L, 1, REV, NCOL, NT, COLMODE, V, INV, false, HOUT, kExt, kExt, TWS>(tm, s, none, st, tw, twstride);
   }
 }
 

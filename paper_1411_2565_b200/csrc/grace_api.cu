@@ -170,6 +170,15 @@ struct grace_ctx {
   cudaStream_t own = nullptr, stream = nullptr, cap = nullptr;
   cudaStream_t hs = nullptr;                  // distributed: halo exchange (C3) side stream
   cudaEvent_t evM = nullptr, evH = nullptr;   // fork (M[c] ready) / join (halos landed)
+  // Per-component pipelining of the transposes: K1, K2, K4
+  // and K5 run per magnetisation component, and the all-to-all of component q
+  // (C1 after K1, C2 after K4) runs on the comm stream `cs` while the step
+  // stream computes component q + 1 (K1 / K4) or consumes component q - 1 (K2 / K5).
+  bool pipe = false;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t evk[3] = {nullptr, nullptr, nullptr};  // component q computed (K1 / K4)
+  cudaEvent_t evc[3] = {nullptr, nullptr, nullptr};  // component q transposed (C1 / C2)
+  bool dist_graphs = true;                    // distributed step captured into graphs (else eager)
   cudaGraphExec_t g1[2] = {nullptr, nullptr}, gc[2] = {nullptr, nullptr};
   ncclComm_t comm = nullptr;
   ncclComm_t comm_halo = nullptr;  // C3's own communicator (NCCL orders work per communicator)
@@ -225,13 +234,17 @@ struct grace_ctx {
   // ---- exchanges (distributed modes) ----
   // all-to-all of [P][blk1] complex blocks: block q of rank s's send buffer goes to
   // block s of rank q's receive buffer.
-  cudaError_t alltoall(float2* Rank::*src, float2* Rank::*dst, cudaStream_t s) {
+  // comp < 0: all three components (whole blocks); else only component comp's
+  // sub-block [nzl][ny][Kb] of every block ([P][3][nzl][ny][Kb] layout).
+  cudaError_t alltoall(float2* Rank::*src, float2* Rank::*dst, cudaStream_t s, int comp = -1) {
     const long long blk = ranks[0].g.blk1;
+    const long long sub = blk / 3;
+    const long long off = comp < 0 ? 0 : comp * sub, cnt = comp < 0 ? blk : sub;
     if (mode == kVirtual) {
       for (int a = 0; a < P; ++a)
         for (int b = 0; b < P; ++b)
-          CE(cudaMemcpyAsync(ranks[b].*dst + (size_t)a * blk, ranks[a].*src + (size_t)b * blk,
-                             sizeof(float2) * blk, cudaMemcpyDeviceToDevice, s));
+          CE(cudaMemcpyAsync(ranks[b].*dst + (size_t)a * blk + off, ranks[a].*src + (size_t)b * blk + off,
+                             sizeof(float2) * cnt, cudaMemcpyDeviceToDevice, s));
       return cudaSuccess;
     }
     // grouped point-to-point: block q of the send buffer to rank q, block q of the
@@ -239,11 +252,18 @@ struct grace_ctx {
     Rank& rk = ranks[0];
     bool bad = g_nccl.groupStart() != 0;
     for (int q = 0; q < P && !bad; ++q) {
-      bad |= g_nccl.send(rk.*src + (size_t)q * blk, (size_t)blk * 2, kNcclFloat32, q, comm, s) != 0;
-      bad |= g_nccl.recv(rk.*dst + (size_t)q * blk, (size_t)blk * 2, kNcclFloat32, q, comm, s) != 0;
+      bad |= g_nccl.send(rk.*src + (size_t)q * blk + off, (size_t)cnt * 2, kNcclFloat32, q, comm, s) != 0;
+      bad |= g_nccl.recv(rk.*dst + (size_t)q * blk + off, (size_t)cnt * 2, kNcclFloat32, q, comm, s) != 0;
     }
     bad |= g_nccl.groupEnd() != 0;
     return bad ? cudaErrorUnknown : cudaSuccess;
+  }
+  // component q of rank rk's geometry (K1, K2, K4, K5 on one component)
+  static Geom comp_geom(const Rank& rk, int q) {
+    Geom g = rk.g;
+    g.c0 = q;
+    g.nc = 1;
+    return g;
   }
   // halo: plane nzl-1 of rank r-1 -> Hlo of rank r; plane 0 of rank r+1 -> Hhi of rank r.
   cudaError_t halo(int c, cudaStream_t s) {
@@ -324,16 +344,57 @@ struct grace_ctx {
       return cudaSuccess;
     }
     CE(halo_start(c, s));  // C3: one M plane to each neighbour, overlapped
-    for (auto& rk : ranks) CE(launch_k1(rk.g, rk.M[c], rk.A, tw, bump ? rk.prm : nullptr, s));
-    CE(alltoall(&Rank::A, &Rank::B, s));  // C1: z slabs -> kx blocks
-    for (auto& rk : ranks) {
-      if (rk.g.Kc > 0) {
-        CE(launch_k2(rk.g, rk.B, rk.X2, tw, s, rk.tma ? &rk.k2map : nullptr));
-        CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s, rk.tma3 ? &rk.k3x : nullptr, rk.tma3 ? &rk.k3k : nullptr));
-        CE(launch_k4(rk.g, rk.X2, rk.B, tw, s, rk.tma ? &rk.k4map : nullptr));
+    if (!pipe) {
+      for (auto& rk : ranks) CE(launch_k1(rk.g, rk.M[c], rk.A, tw, bump ? rk.prm : nullptr, s));
+      CE(alltoall(&Rank::A, &Rank::B, s));  // C1: z slabs -> kx blocks
+      for (auto& rk : ranks) {
+        if (rk.g.Kc > 0) {
+          CE(launch_k2(rk.g, rk.B, rk.X2, tw, s, rk.tma ? &rk.k2map : nullptr));
+          CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s, rk.tma3 ? &rk.k3x : nullptr, rk.tma3 ? &rk.k3k : nullptr));
+          CE(launch_k4(rk.g, rk.X2, rk.B, tw, s, rk.tma ? &rk.k4map : nullptr));
+        }
       }
+      return alltoall(&Rank::B, &Rank::A, s);  // C2: kx blocks -> z slabs
     }
-    CE(alltoall(&Rank::B, &Rank::A, s));  // C2: kx blocks -> z slabs
+    // pipelined: K1(q) | C1(q) on cs while K1(q+1); K2(q) once C1(q) has landed
+    for (int q = 0; q < 3; ++q) {
+      for (auto& rk : ranks) CE(launch_k1(comp_geom(rk, q), rk.M[c], rk.A, tw, (bump && q == 0) ? rk.prm : nullptr, s));
+      CE(cudaEventRecord(evk[q], s));
+      CE(cudaStreamWaitEvent(cs, evk[q], 0));
+      CE(alltoall(&Rank::A, &Rank::B, cs, q));
+      CE(cudaEventRecord(evc[q], cs));
+    }
+    for (int q = 0; q < 3; ++q) {
+      CE(cudaStreamWaitEvent(s, evc[q], 0));
+      for (auto& rk : ranks)
+        if (rk.g.Kc > 0) CE(launch_k2(comp_geom(rk, q), rk.B, rk.X2, tw, s, rk.tma ? &rk.k2map : nullptr));
+    }
+    for (auto& rk : ranks)
+      if (rk.g.Kc > 0)
+        CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s, rk.tma3 ? &rk.k3x : nullptr, rk.tma3 ? &rk.k3k : nullptr));
+    // K4(q) | C2(q) on cs while K4(q+1); k5_stage consumes component q once C2(q) landed
+    for (int q = 0; q < 3; ++q) {
+      for (auto& rk : ranks)
+        if (rk.g.Kc > 0) CE(launch_k4(comp_geom(rk, q), rk.X2, rk.B, tw, s, rk.tma ? &rk.k4map : nullptr));
+      CE(cudaEventRecord(evk[q], s));
+      CE(cudaStreamWaitEvent(cs, evk[q], 0));
+      CE(alltoall(&Rank::B, &Rank::A, cs, q));
+      CE(cudaEventRecord(evc[q], cs));
+    }
+    return cudaSuccess;
+  }
+
+  // K5 (C2R -> H_demag) of every rank after demag_stages; pipelined: component q
+  // as soon as its C2 transpose has landed.
+  cudaError_t k5_stage(cudaStream_t s) {
+    if (!pipe) {
+      for (auto& rk : ranks) CE(launch_k5(rk.g, rk.A, rk.Hd, tw, s));
+      return cudaSuccess;
+    }
+    for (int q = 0; q < 3; ++q) {
+      CE(cudaStreamWaitEvent(s, evc[q], 0));
+      for (auto& rk : ranks) CE(launch_k5(comp_geom(rk, q), rk.A, rk.Hd, tw, s));
+    }
     return cudaSuccess;
   }
 
@@ -341,17 +402,15 @@ struct grace_ctx {
   // (f0 kept in F), then H(M*) and the corrector updates M[c] in place.
   cudaError_t enqueue_heun(int c, cudaStream_t s) {
     CE(demag_stages(c, s, true));
+    CE(k5_stage(s));
     CE(halo_join(s));
-    for (auto& rk : ranks) {
-      CE(launch_k5(rk.g, rk.A, rk.Hd, tw, s));
+    for (auto& rk : ranks)
       CE(launch_k6(rk.g, 3, rk.Hd, rk.M[c], rk.M[1 - c], rk.F, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
-    }
     CE(demag_stages(1 - c, s, false));
+    CE(k5_stage(s));
     CE(halo_join(s));
-    for (auto& rk : ranks) {
-      CE(launch_k5(rk.g, rk.A, rk.Hd, tw, s));
+    for (auto& rk : ranks)
       CE(launch_k6(rk.g, 4, rk.Hd, rk.M[1 - c], rk.M[c], rk.F, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
-    }
     return cudaSuccess;
   }
   // buffer index after one step from c
@@ -364,8 +423,8 @@ struct grace_ctx {
     const int nk = kernel_count(g0);
     const int k5 = 2 * (nk - 2);
     if (ev) cudaEventRecord(ev[k5], s);
+    CE(k5_stage(s));
     CE(halo_join(s));
-    for (auto& rk : ranks) CE(launch_k5(rk.g, rk.A, rk.Hd, tw, s));
     if (ev) cudaEventRecord(ev[k5 + 1], s);
     if (ev) cudaEventRecord(ev[k5 + 2], s);
     for (auto& rk : ranks)
@@ -394,11 +453,25 @@ struct grace_ctx {
   // chunks and single steps, from either M buffer) ahead of time, so no
   // grace_step call pays a capture: done at create and after anything that
   // invalidates them (integrator, geometry mask).
+  // The distributed step is captured too (NCCL calls, the comm and halo streams
+  // forked and joined by events); if capture fails there (e.g. an NCCL build
+  // without graph support) it runs eagerly instead.
   cudaError_t prepare_graphs() {
-    if (mode != kSingle) return cudaSuccess;
+    if (mode != kSingle && (!dist_graphs || getenv("GRACE_DIST_EAGER"))) {
+      dist_graphs = false;
+      return cudaSuccess;
+    }
     for (int c = 0; c < 2; ++c) {
-      if (!gc[c]) CE(build_graph(c, kChunk, &gc[c]));
-      if (!g1[c]) CE(build_graph(c, 1, &g1[c]));
+      cudaError_t e = cudaSuccess;
+      if (!gc[c]) e = build_graph(c, kChunk, &gc[c]);
+      if (e == cudaSuccess && !g1[c]) e = build_graph(c, 1, &g1[c]);
+      if (e != cudaSuccess) {
+        if (mode == kSingle) return e;
+        cudaGetLastError();
+        drop_graphs();
+        dist_graphs = false;
+        return cudaSuccess;
+      }
     }
     return cudaSuccess;
   }
@@ -431,6 +504,11 @@ struct grace_ctx {
     if (hs) cudaStreamDestroy(hs);
     if (evM) cudaEventDestroy(evM);
     if (evH) cudaEventDestroy(evH);
+    if (cs) cudaStreamDestroy(cs);
+    for (int q = 0; q < 3; ++q) {
+      if (evk[q]) cudaEventDestroy(evk[q]);
+      if (evc[q]) cudaEventDestroy(evc[q]);
+    }
   }
 };
 
@@ -467,6 +545,8 @@ int make_geom(int nx, int ny, int nz, double dx, double dy, double dz, double Ms
   g.Kc = g.Kx;
   g.pitch2 = g.Kxp;
   g.has_lo = g.has_hi = 0;
+  g.c0 = 0;
+  g.nc = 3;
   int dev = 0, nsm = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   cudaGetLastError();
@@ -548,6 +628,11 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
     if (e == cudaSuccess && mode != grace_ctx::kSingle) e = cudaStreamCreateWithFlags(&h->hs, cudaStreamNonBlocking);
     if (e == cudaSuccess && mode != grace_ctx::kSingle) e = cudaEventCreateWithFlags(&h->evM, cudaEventDisableTiming);
     if (e == cudaSuccess && mode != grace_ctx::kSingle) e = cudaEventCreateWithFlags(&h->evH, cudaEventDisableTiming);
+    if (e == cudaSuccess && mode != grace_ctx::kSingle) e = cudaStreamCreateWithFlags(&h->cs, cudaStreamNonBlocking);
+    for (int q = 0; q < 3 && e == cudaSuccess && mode != grace_ctx::kSingle; ++q) {
+      e = cudaEventCreateWithFlags(&h->evk[q], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->evc[q], cudaEventDisableTiming);
+    }
     if (e != cudaSuccess) return bail(fail(GRACE_ECUDA, "stream creation: %s", cudaGetErrorString(e)));
   }
   h->stream = h->own;
@@ -585,6 +670,10 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
       return bail(rc);
   }
   if ((rc = h->alloc((void**)&h->tw, sizeof(float2) * g0.Lmax))) return bail(rc);
+  if (dlay && !getenv("GRACE_NO_PIPE")) {
+    h->pipe = true;
+    for (auto& rk : h->ranks) h->pipe = h->pipe && comp_split_ok(rk.g);
+  }
   // TMA descriptors for the y-pencil kernels (K2 reads the x-row layout, K4 reads X2)
   if (!h->fused && !getenv("GRACE_NO_TMA"))
     for (auto& rk : h->ranks) {
@@ -933,7 +1022,7 @@ int grace_step(grace_ctx* h, int n, double dt) {
   cudaStream_t s = h->stream;
   CUDA_OR(h->upload_params(dt));
   const int nk = kernel_count(h->g0);
-  if (h->mode != grace_ctx::kSingle) {
+  if (h->mode != grace_ctx::kSingle && !h->dist_graphs) {
     for (int i = 0; i < n; ++i) {
       cudaError_t e = h->enqueue_step(h->cur, s);
       if (e != cudaSuccess) return fail(GRACE_ECUDA, "distributed step: %s", cudaGetErrorString(e));
@@ -1127,8 +1216,10 @@ int grace_geometry(grace_ctx* h, long long* o) {
 int grace_partition(grace_ctx* h, long long* o) {
   if (!h || !o) return fail(GRACE_EINVAL, "NULL argument");
   const Geom& g = h->ranks[0].g;
-  const long long v[8] = {h->P, h->ranks[0].r, g.nzl, (long long)h->ranks[0].r * g.nzl, g.kb, g.Kc, g.pitch1,
-                          g.pitch2};
+  const long long v[11] = {h->P,      h->ranks[0].r, g.nzl,    (long long)h->ranks[0].r * g.nzl,
+                           g.kb,      g.Kc,          g.pitch1, g.pitch2,
+                           h->pipe,   (h->mode == grace_ctx::kSingle || h->dist_graphs) ? 1 : 0,
+                           h->comm_halo != nullptr};
   std::memcpy(o, v, sizeof v);
   return GRACE_OK;
 }

@@ -54,6 +54,8 @@ struct Geom {
   int has_lo, has_hi;  // z-1 / z+1 halo planes present
   int nsm;             // SMs of the device (persistent grids)
   int masked;          // geometry mask set (grace_set_geometry): M = 0 marks an empty cell (reading Q26)
+  int c0, nc;          // components c0 .. c0 + nc - 1 handled by K1, K2, K4, K5 (default 0, 3; the
+                       // distributed step runs them per component to pipeline the transposes)
   float cx, cy, cz; // exchange 2A/(mu0 Ms^2 d^2) per axis (0 for a singleton axis)
   float ck;         // anisotropy 2Ku/(mu0 Ms^2)
   float Ms;
@@ -91,6 +93,7 @@ cudaError_t launch_k6(const Geom& g, int mode, const float* Hd, const float* M, 
                       const StepParams* prm, unsigned long long* flag, cudaStream_t st, const float* Hlo,
                       const float* Hhi);
 bool fused_y_path(const Geom& g);  // nz == 1 and the y-pencils of 3 components fit one CTA
+bool comp_split_ok(const Geom& g); // K1 .. K5 can run per component (bulk-copy x kernels)
 int kernel_count(const Geom& g);   // kernels per step
 
 // Utilities (step_kernels.cu).

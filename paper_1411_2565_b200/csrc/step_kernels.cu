@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(NT, MINB) k_y(const float2* __restrict__ in, f
   pdl_wait();
   extern __shared__ float2 smem[];
   const int kx0 = blockIdx.x * NCOL;
-  const size_t slab = blockIdx.y;
+  const size_t slab = blockIdx.y + (size_t)g.c0 * g.nz;  // components c0 .. c0 + nc - 1
   struct Ld {
     __device__ static constexpr bool kSmem() { return false; }
     const float2* p;
@@ -251,9 +251,10 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? 2 : GRACE_YT_MINB
 #endif
   fill_pass_twiddles<typename Y::PL, L>(tws, tw, g.Lmax / L, threadIdx.x, NT);
   const int ntx = (g.Kc + NCOL - 1) / NCOL;
-  const int ntiles = ntx * 3 * g.nz;
+  const int ntiles = ntx * g.nc * g.nz;  // components c0 .. c0 + nc - 1
+  const int slab0 = g.c0 * g.nz;
   auto issue = [&](int t, float2* dst, uint64_t* b) {
-    const int slab = t / ntx, xt = t - slab * ntx;
+    const int slab = slab0 + t / ntx, xt = t - (t / ntx) * ntx;
     const int c = slab / g.nz, z = slab - c * g.nz;
     int c2 = z, c4 = 0;
     if (!INV) {  // x-row layout [q][c][zl][y][kx]
@@ -305,7 +306,7 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? 2 : GRACE_YT_MINB
       }
       mbar_wait(bar, k & 1);
     }
-    const int slab = t / ntx, xt = t - slab * ntx;
+    const int slab = slab0 + t / ntx, xt = t - (t / ntx) * ntx;
     const int kx0 = xt * NCOL;
     float2* o = out + (INV ? xrow_slab(g, slab) : (size_t)slab * g.Py * g.pitch2) + kx0;
     const int pitch = INV ? g.pitch1 : g.pitch2;
@@ -355,9 +356,10 @@ __global__ void __launch_bounds__(YStage<L>::NT, (L == 2048 ? GRACE_YSTAGE_MINB 
   uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + Y::WB + Y::SB);
   pdl_trigger();
   const int ntx = (g.Kc + NCOL - 1) / NCOL;
-  const int ntiles = ntx * 3 * g.nz;
+  const int ntiles = ntx * g.nc * g.nz;  // components c0 .. c0 + nc - 1
+  const int slab0 = g.c0 * g.nz;
   auto issue = [&](int t) {
-    const int slab = t / ntx, xt = t - slab * ntx;
+    const int slab = slab0 + t / ntx, xt = t - (t / ntx) * ntx;
     const int c = slab / g.nz, z = slab - c * g.nz;
     const int c4 = z / g.nzl, c2 = z - c4 * g.nzl;  // x-row layout [q][c][zl][y][kx]
     mbar_expect_tx(bar, TX);
@@ -390,7 +392,7 @@ __global__ void __launch_bounds__(YStage<L>::NT, (L == 2048 ? GRACE_YSTAGE_MINB 
   const ThreadMap<L, NCOL, NT, true> tm;
   for (int k = 0; t < ntiles; ++k, t += gridDim.x) {
     mbar_wait(bar, k & 1);
-    const int slab = t / ntx, xt = t - slab * ntx;
+    const int slab = slab0 + t / ntx, xt = t - (t / ntx) * ntx;
     const int kx0 = xt * NCOL;
     const St st{out + (size_t)slab * g.Py * g.pitch2 + kx0, g.pitch2, g.Kc - kx0};
     // pass 0: staged rows (< L/2, the rest is the zero padding) -> work tile
@@ -496,7 +498,10 @@ struct ZPlan {
 
 // kw(): called before the multiply's barrier -- waits for this thread's part of
 // the KS slice (cp.async group or TMA mbarrier).
-template <int L, int B, int NT, class LD, class ST, class KW>
+// TWS (fused plans only): tw is a shared table holding the forward plan's per-pass
+// twiddles followed by the reversed (inverse) plan's (fill_pass_twiddles of
+// Plan<L, false> then Plan<L, true>); else tw is the global table.
+template <int L, int B, int NT, bool TWS = false, class LD, class ST, class KW>
 __device__ __forceinline__ void pencil_conv(float2* smem, const LD& ld, const ST& st, const float* kss, int KH,
                                             const float2* __restrict__ tw, int twstride, int P_other, int k_other,
                                             bool fold_is_y, const KW& kw) {
@@ -515,12 +520,14 @@ __device__ __forceinline__ void pencil_conv(float2* smem, const LD& ld, const ST
     }
   };
   const ThreadMap<L, B, NT, true> tm;
+  static_assert(!TWS || ZPlan<L>::FUSE, "shared twiddle tables: fused plans only");
   if constexpr (ZPlan<L>::FUSE) {
     using PF = Pass<L, fft_npass(L) - 1, false, B, NT, true, 3>;
     using PI = Pass<L, 0, true, B, NT, true, 3>;
     static_assert(PF::R == PI::R && PF::UPT == 1 && PI::UPT == 1, "fused plan");
     PF pf;
-    fft_to_regs<L, B, NT, true, 3, false, true, false, false>(tm, smem, ld, tw, twstride, pf);
+    const float2* twi = TWS ? tw + Plan<L, false, 4>::TW_ELEMS : tw;
+    fft_to_regs<L, B, NT, true, 3, false, true, false, false, TWS>(tm, smem, ld, tw, twstride, pf);
     kw();
     __syncthreads();
     PI pi;
@@ -536,7 +543,7 @@ __device__ __forceinline__ void pencil_conv(float2* smem, const LD& ld, const ST
       pi.v[0][1][r] = b;
       pi.v[0][2][r] = c;
     }
-    fft_from_regs<L, B, NT, true, 3, true, true, true>(tm, smem, st, tw, twstride, pi);
+    fft_from_regs<L, B, NT, true, 3, true, true, true, TWS>(tm, smem, st, twi, twstride, pi);
   } else {
     using T = TileIdx<L, B, true>;
     fft_tile<L, B, NT, true, false, (L > 1), false, 3>(smem, ld, SmemSt<L, B, true>{smem}, tw, twstride);
@@ -635,9 +642,12 @@ struct Z3Tma {
   static constexpr size_t STAGE = 3 * (size_t)H * B * 8;
   static constexpr size_t KSB = 6 * (size_t)KZH * B * 4;
   static constexpr size_t KSB16 = (KSB + 15) / 16 * 16;
-  static constexpr bool PRE = (WORK + STAGE + KSB16 + 64) * 4 <= 220 * 1024;
+  static constexpr int TWF = Plan<L, false, 4>::TW_ELEMS, TWI = Plan<L, true, 4>::TW_ELEMS;
+  static constexpr size_t TWB = (size_t)(TWF + TWI) * 8;  // per-pass twiddles, forward then inverse plan
+  static constexpr bool PRE = (WORK + STAGE + KSB16 + TWB + 64) * 4 <= 220 * 1024;
   static constexpr size_t KSOFF = WORK + (PRE ? STAGE : 0);
-  static constexpr size_t SMEM = KSOFF + KSB16 + 64;
+  static constexpr size_t TWOFF = KSOFF + KSB16;
+  static constexpr size_t SMEM = TWOFF + TWB + 64;
 };
 
 template <int L, int MINB>
@@ -651,7 +661,8 @@ __global__ void __launch_bounds__(Z3Tma<L>::NT, MINB)
   float2* work = reinterpret_cast<float2*>(smraw);
   float2* stage = reinterpret_cast<float2*>(smraw + Z::WORK);
   float* kss = reinterpret_cast<float*>(smraw + Z::KSOFF);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + Z::KSOFF + Z::KSB16);  // KS, work, stage
+  float2* tws = reinterpret_cast<float2*>(smraw + Z::TWOFF);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + Z::TWOFF + Z::TWB);  // KS, work, stage
   const int kx0 = blockIdx.x * B;
   const int kyf = blockIdx.y;
   const int nky = (kyf == 0 || 2 * kyf == g.Py) ? 1 : 2;
@@ -667,6 +678,10 @@ __global__ void __launch_bounds__(Z3Tma<L>::NT, MINB)
     mbar_expect_tx(bar, (unsigned)Z::KSB);
     tma_load_4d(kss, &kmap, bar, kx0, kyf, 0, 0);
   }
+  // per-pass twiddle tables in smem (the global table's lines would miss the
+  // minimal L1 of a shared-memory-carveout kernel)
+  fill_pass_twiddles<Plan<L, false, 4>, L>(tws, tw, g.Lmax / L, threadIdx.x, NT);
+  fill_pass_twiddles<Plan<L, true, 4>, L>(tws + Z::TWF, tw, g.Lmax / L, threadIdx.x, NT);
   __syncthreads();
   pdl_wait();  // X2 comes from K2
   auto issue = [&](float2* dst, int ky, uint64_t* b, int cstep) {
@@ -701,11 +716,11 @@ __global__ void __launch_bounds__(Z3Tma<L>::NT, MINB)
     };
     if (rep == 0) {
       mbar_wait(bar + 1, 0);
-      pencil_conv<L, B, NT>(work, SmemLd<L, B, true>{work}, st, kss, Z::KZH, tw, g.Lmax / L, g.Py, ky, false, kw);
+      pencil_conv<L, B, NT, true>(work, SmemLd<L, B, true>{work}, st, kss, Z::KZH, tws, 1, g.Py, ky, false, kw);
     } else if constexpr (Z::PRE) {
       __syncthreads();  // the work tile is free
       mbar_wait(bar + 2, 0);
-      pencil_conv<L, B, NT>(work, StageLd{stage}, st, kss, Z::KZH, tw, g.Lmax / L, g.Py, ky, false, kw);
+      pencil_conv<L, B, NT, true>(work, StageLd{stage}, st, kss, Z::KZH, tws, 1, g.Py, ky, false, kw);
     } else {
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -713,7 +728,7 @@ __global__ void __launch_bounds__(Z3Tma<L>::NT, MINB)
         issue(work, ky, bar + 1, Z::T::ELEMS);
       }
       mbar_wait(bar + 1, 1);
-      pencil_conv<L, B, NT>(work, SmemLd<L, B, true>{work}, st, kss, Z::KZH, tw, g.Lmax / L, g.Py, ky, false, kw);
+      pencil_conv<L, B, NT, true>(work, SmemLd<L, B, true>{work}, st, kss, Z::KZH, tws, 1, g.Py, ky, false, kw);
     }
   }
 }
@@ -947,7 +962,8 @@ __global__ void __launch_bounds__(XBulk<L>::NT, GRACE_XB_MINB)
   if constexpr (FWD)
     for (int kk = threadIdx.x; kk < X::PPE; kk += NT) twp[kk] = __ldg(tw + kk * (g.Lmax / (2 * L)));
   const int nrows = g.nzl * g.ny;
-  const int total = 3 * nrows;
+  const int total = g.nc * nrows;  // rows of components c0 .. c0 + nc - 1
+  const size_t rowoff = (size_t)g.c0 * nrows;
   const int ntiles = (total + RB - 1) / RB;
   const int nseg = (!FWD && DIST) ? g.nz / g.nzl : 1;
   const unsigned seg = FWD ? 4u * g.nx : (DIST ? 8u * g.kb : 8u * (L + 2));
@@ -960,7 +976,7 @@ __global__ void __launch_bounds__(XBulk<L>::NT, GRACE_XB_MINB)
     __syncwarp();
     for (int u = lane; u < nv * nseg; u += 32) {
       const int bb = u / nseg, q = u - bb * nseg;
-      const size_t gr = (size_t)(r0 + bb);
+      const size_t gr = rowoff + (size_t)(r0 + bb);
       const void* src;
       if constexpr (FWD) src = static_cast<const float*>(in) + gr * g.nx;
       else if constexpr (DIST) src = static_cast<const float2*>(in) + q * g.blk1 + gr * g.pitch1;
@@ -1006,7 +1022,7 @@ __global__ void __launch_bounds__(XBulk<L>::NT, GRACE_XB_MINB)
       const int b = threadIdx.x / TPC, jb = threadIdx.x - b * TPC;
       if (b < nv) {
         float2* X1 = static_cast<float2*>(out);
-        const size_t gr = (size_t)(r0 + b);
+        const size_t gr = rowoff + (size_t)(r0 + b);
         auto at = [&](int kk) -> size_t {
           if constexpr (DIST) {
             const int q = kk / g.kb;
@@ -1052,7 +1068,7 @@ __global__ void __launch_bounds__(XBulk<L>::NT, GRACE_XB_MINB)
           return make_float2(S.x - wD.y, S.y + wD.x);  // S + i w^-k D
         }
       } ld{cur, tw, twpx};
-      float* H = static_cast<float*>(out) + (size_t)r0 * g.nx;
+      float* H = static_cast<float*>(out) + (rowoff + (size_t)r0) * g.nx;
       if (nv == RB && g.nx == L)  // the pruned last pass produces exactly the nx outputs
         fft_tile<L, RB, NT, false, true, false, true, 1, false, true>(cur, ld, XbSt<false>{H, g.nx, nv}, tws, 1);
       else
@@ -1385,7 +1401,7 @@ static cudaError_t xbulk_launch(const Geom& g, const void* in, void* out, const 
   auto kern = k_x_bulk<L, FWD, DIST>;
   cudaError_t e = prep(kern, X::SMEM);
   if (e != cudaSuccess) return e;
-  const int ntiles = (3 * g.nzl * g.ny + X::RB - 1) / X::RB;
+  const int ntiles = (g.nc * g.nzl * g.ny + X::RB - 1) / X::RB;
   int per_sm = 0;  // resident CTAs per SM (shared memory may allow fewer than GRACE_XB_MINB)
   GRACE_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, X::NT, X::SMEM));
   const int cap = g.nsm * (per_sm < 1 ? 1 : (per_sm < GRACE_XB_MINB ? per_sm : GRACE_XB_MINB));
@@ -1437,7 +1453,7 @@ static cudaError_t ky_launch(const Geom& g, const float2* in, float2* out, const
   auto kern = k_y<L, C::NCOL, C::NT, C::MINB, INV>;
   cudaError_t e = prep(kern, smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((g.Kc + C::NCOL - 1) / C::NCOL, 3 * g.nz);
+  dim3 grid((g.Kc + C::NCOL - 1) / C::NCOL, g.nc * g.nz);
   GRACE_TRY(launch_k(INV ? 8 : 2, kern, grid, C::NT, smem, st, in, out, tw, g, in_rows, out_rows, n_in, n_out));
   return cudaGetLastError();
 }
@@ -1460,7 +1476,7 @@ static cudaError_t ky_tma_launch(const Geom& g, float2* out, const float2* tw, c
   auto kern = k_y_tma<L, NCOL, INV, NB>;
   cudaError_t e = prep(kern, Y::SMEM);
   if (e != cudaSuccess) return e;
-  const int ntiles = ((g.Kc + NCOL - 1) / NCOL) * 3 * g.nz;
+  const int ntiles = ((g.Kc + NCOL - 1) / NCOL) * g.nc * g.nz;
   const int want = NB == 1 ? 2 : GRACE_YT_MINB;
   const int per_sm = (int)(220 * 1024 / Y::SMEM) < want ? (int)(220 * 1024 / Y::SMEM) : want;
   const int cap = g.nsm * (per_sm > 0 ? per_sm : 1);
@@ -1479,7 +1495,7 @@ static cudaError_t ky_stage_launch(const Geom& g, float2* out, const float2* tw,
   auto kern = k_y_stage<L>;
   cudaError_t e = prep(kern, Y::SMEM);
   if (e != cudaSuccess) return e;
-  const int ntiles = ((g.Kc + Y::NCOL - 1) / Y::NCOL) * 3 * g.nz;
+  const int ntiles = ((g.Kc + Y::NCOL - 1) / Y::NCOL) * g.nc * g.nz;
   const int cap = g.nsm * (L == 2048 ? GRACE_YSTAGE_MINB : 1);
   const int grid = ntiles < cap ? ntiles : cap;
   CUtensorMap map;
@@ -1678,6 +1694,19 @@ cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* 
 }
 
 bool fused_y_path(const Geom& g) { return g.Pz == 1 && g.Py <= 512; }
+
+// K1 and K5 take the persistent bulk-copy kernels (which, like K2 and K4, can run
+// on a range of components): the distributed step may then pipeline the
+// transposes per component.
+bool comp_split_ok(const Geom& g) {
+  if (g.Px < 2 || fused_y_path(g)) return false;
+#define CASE(v) case v: return (v >= kXBulkMinL && v <= kXBulkMaxL) && xbulk_ok<(v >= kXBulkMinL && v <= kXBulkMaxL ? v : kXBulkMinL)>(g, true) && xbulk_ok<(v >= kXBulkMinL && v <= kXBulkMaxL ? v : kXBulkMinL)>(g, false);
+  switch (g.Px / 2) {
+    CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64) CASE(128) CASE(256) CASE(512) CASE(1024) CASE(2048) CASE(4096)
+    default: return false;
+  }
+#undef CASE
+}
 int kernel_count(const Geom& g) { return (fused_y_path(g) ? 3 : 5) + 1; }
 
 template <int HEUN, bool MASK>

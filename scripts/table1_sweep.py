@@ -8,7 +8,7 @@ loop, steps timed with CUDA events after warm-up) and, for small N, the fp64
 oracle on this host, and prints one JSON object plus a markdown table.  Also
 times the SP4 grids (BASELINE configs 1-2), whose steps are launch-bound.
 
-python scripts/table1_sweep.py [--out profiles/r01_table1]
+python scripts/table1_sweep.py [--out profiles/r02_table1] [--oracle-max 128]
 """
 import argparse
 import json
@@ -50,31 +50,43 @@ def gpu_ms_per_step(w, steps):
 
 
 def oracle_ms_per_step(w, steps=3):
+    """fp64 oracle on this host: (single-thread ms/step, all-core ms/step, setup s).
+    Single thread: numpy.fft; all cores: scipy.fft workers = affinity size
+    (BASELINE.md Sec. 4); setup = tensor octant + kernel spectrum, once."""
     from oracle.demag import DemagFFT
     from oracle.llg import Sim
     from oracle.tensor import tensor_octant
 
-    sim = Sim(random_m(w.n, w.Ms), DemagFFT(tensor_octant(*w.n, *w.d)), w.Ms, w.A, w.Ku, w.alpha, w.gamma0, w.d)
-    sim.euler_step(w.dt)
+    ncores = len(os.sched_getaffinity(0))
     t = time.perf_counter()
-    sim.run(steps, w.dt)
-    return (time.perf_counter() - t) / steps * 1e3
+    oct_ = tensor_octant(*w.n, *w.d)
+    op = DemagFFT(oct_)
+    setup = time.perf_counter() - t
+    res = []
+    for o in (op, DemagFFT(oct_, workers=ncores)):
+        sim = Sim(random_m(w.n, w.Ms), o, w.Ms, w.A, w.Ku, w.alpha, w.gamma0, w.d)
+        sim.euler_step(w.dt)
+        t = time.perf_counter()
+        sim.run(steps, w.dt)
+        res.append((time.perf_counter() - t) / steps * 1e3)
+    return res[0], res[1], setup
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
-    ap.add_argument("--oracle-max", type=int, default=32)
+    ap.add_argument("--oracle-max", type=int, default=128)
     args = ap.parse_args()
     rows = []
     for N in (8, 16, 32, 64, 128, 256, 512):
         w = table1_cube(N)
         steps = 2000 if N <= 64 else (400 if N <= 128 else 50)
         gms = gpu_ms_per_step(w, steps)
-        oms = oracle_ms_per_step(w) if N <= args.oracle_max else None
+        oms, omk, osetup = oracle_ms_per_step(w) if N <= args.oracle_max else (None, None, None)
         cpu_p, gpu_p = PAPER.get(N, (None, None))
         rows.append({"N": N, "cells": N ** 3, "b200_ms": gms, "b200_Mcell_s": N ** 3 / gms / 1e3,
-                     "oracle_ms_this_host": oms, "paper_hd7970_ms": gpu_p, "paper_oommf_i7_ms": cpu_p})
+                     "oracle_ms_this_host": oms, "oracle_ms_all_cores": omk, "oracle_setup_s": osetup,
+                     "paper_hd7970_ms": gpu_p, "paper_oommf_i7_ms": cpu_p})
     sp4 = []
     for name in ("sp4_field1", "sp4_field2_refined"):
         w = WORKLOADS[name]
@@ -83,12 +95,18 @@ def main():
                     "ns_simulated_per_s": w.dt * 1e9 / (gms * 1e-3)})
     out = {"table1": rows, "sp4": sp4, "note": "B200 numbers: CUDA events around grace_step(K) after 32 warm-up "
            "steps (graph replay); paper numbers are other hardware (HD 7970 / OOMMF on i7-930), context only"}
-    lines = ["| N | cells | B200 ms/step | B200 Mcell-updates/s | fp64 oracle ms/step (this host) | paper HD 7970 ms | "
-             "paper OOMMF i7-930 ms |", "|---|---|---|---|---|---|---|"]
+    ncores = len(os.sched_getaffinity(0))
+    lines = ["| N | cells | B200 ms/step | B200 Mcell-updates/s | fp64 oracle ms/step, 1 thread | "
+             f"fp64 oracle ms/step, {ncores} threads | oracle setup s | B200 speed-up vs oracle (1 thr / all) | "
+             "paper HD 7970 ms | paper OOMMF i7-930 ms | paper GPU/CPU |", "|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         f = lambda v: "-" if v is None else f"{v:.4g}"  # noqa: E731
+        sp = "-" if r["oracle_ms_this_host"] is None else \
+            f"{r['oracle_ms_this_host'] / r['b200_ms']:.0f} / {r['oracle_ms_all_cores'] / r['b200_ms']:.0f}"
+        pr = "-" if r["paper_hd7970_ms"] is None else f"{r['paper_oommf_i7_ms'] / r['paper_hd7970_ms']:.3g}"
         lines.append(f"| {r['N']} | {r['cells']} | {r['b200_ms']:.4f} | {r['b200_Mcell_s']:.1f} | "
-                     f"{f(r['oracle_ms_this_host'])} | {f(r['paper_hd7970_ms'])} | {f(r['paper_oommf_i7_ms'])} |")
+                     f"{f(r['oracle_ms_this_host'])} | {f(r['oracle_ms_all_cores'])} | {f(r['oracle_setup_s'])} | {sp} | "
+                     f"{f(r['paper_hd7970_ms'])} | {f(r['paper_oommf_i7_ms'])} | {pr} |")
     lines += ["", "| SP4 workload | grid | B200 us/step | simulated ns per wall-clock s |", "|---|---|---|---|"]
     for r in sp4:
         lines.append(f"| {r['workload']} | {r['grid']} | {r['b200_us_per_step']:.2f} | {r['ns_simulated_per_s']:.3f} |")

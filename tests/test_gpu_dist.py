@@ -161,3 +161,64 @@ def test_nccl_path_one_rank_masked_matches_single(monkeypatch):
     np.testing.assert_allclose(ea, eb, rtol=1e-9, atol=0)
     pb.grace_destroy(h)
     ref.close()
+
+
+@pytest.mark.parametrize("n,P", [((128, 64, 16), 4), ((64, 48, 16), 2)])
+def test_pipelined_graph_step_bitwise_equals_unpipelined_eager(n, P, monkeypatch):
+    """Per-component pipelined transposes (comm stream, events) captured into CUDA
+    graphs = the unpipelined eager distributed step = the single-GPU step, bitwise."""
+    d = (1e-9, 1e-9, 1e-9)
+    M = random_m(n, 1e6, seed=61)
+    out = []
+    for env in ({}, {"GRACE_NO_PIPE": "1"}, {"GRACE_DIST_EAGER": "1"}, {"GRACE_NO_PIPE": "1", "GRACE_DIST_EAGER": "1"}):
+        for k in ("GRACE_NO_PIPE", "GRACE_DIST_EAGER"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        g = pb.Grace(n, d, 1e6, 1e-11, 6.2832e4, 0.5, GAMMA0, virtual_ranks=P)
+        part = pb.grace_partition(g.h)
+        assert part["pipelined"] == (0 if "GRACE_NO_PIPE" in env else 1)
+        assert part["graphs"] == (0 if "GRACE_DIST_EAGER" in env else 1)
+        g.set_m(M)
+        g.set_hext((1e4, 0, 0))
+        g.step(19, 1e-15)  # one 16-step chunk + 3 single steps
+        H = g.heff()
+        out.append((g.get_m(), H))
+        g.close()
+    ref = pb.Grace(n, d, 1e6, 1e-11, 6.2832e4, 0.5, GAMMA0)
+    ref.set_m(M)
+    ref.set_hext((1e4, 0, 0))
+    ref.step(19, 1e-15)
+    out.append((ref.get_m(), ref.heff()))
+    ref.close()
+    for Mo, Ho in out[1:]:
+        assert np.array_equal(out[0][0], Mo)
+        assert np.array_equal(out[0][1], Ho)
+
+
+def test_nccl_one_rank_graphs_pipeline_and_agreed_nonfinite(monkeypatch):
+    """NCCL path on a one-rank communicator: the pipelined step is graph-captured
+    (NCCL calls inside the graph), the halo has its own split communicator, and a
+    non-finite step reports the same (step, global cell) as the single context."""
+    monkeypatch.setenv("GRACE_FORCE_NCCL", "1")
+    n, d, Ms = (64, 20, 8), (2e-9, 2e-9, 3e-9), 8e5
+    M = random_m(n, Ms, seed=57)
+    h = pb.grace_create_dist(*n, *d, Ms, 1.3e-11, 2e4, 0.3, GAMMA0, 0, 1, pb.grace_nccl_unique_id())
+    part = pb.grace_partition(h)
+    assert part["pipelined"] == 1 and part["graphs"] == 1
+    ref = pb.Grace(n, d, Ms, 1.3e-11, 2e4, 0.3, GAMMA0)
+    res = []
+    for hh in (h, ref.h):
+        pb.grace_set_m(hh, M.ravel().copy())
+        pb.grace_step(hh, 20, 2e-14)
+        Mo = np.empty(3 * M[0].size)
+        pb.grace_get_m(hh, Mo)
+        pb.grace_set_hext(hh, 3e38, 3e38, 3e38)
+        with pytest.raises(pb.GraceError) as e:
+            pb.grace_step(hh, 2, 1e-13)
+        assert e.value.code == pb.GRACE_ENONFINITE
+        res.append((Mo, pb.grace_last_nonfinite(hh)))
+    assert np.array_equal(res[0][0], res[1][0])
+    assert res[0][1] == res[1][1]
+    pb.grace_destroy(h)
+    ref.close()
