@@ -316,7 +316,9 @@ struct grace_ctx {
     return (mode == kSingle || (mode == kNccl && !comm_halo)) ? cudaSuccess : cudaStreamWaitEvent(s, evH, 0);
   }
 
-  // H~ for every rank: K1 .. K4 plus the transposes.  M[c] is the input.
+  // H~ for every rank: K1 .. K4 plus the transposes.  M[c] is the input.  Always
+  // follow it with k5_stage (on the pipelined path the C2 transposes are still in
+  // flight on the comm stream when this returns; k5_stage joins them).
   cudaError_t demag_stages(int c, cudaStream_t s, bool bump, cudaEvent_t* ev = nullptr) {
     auto rec = [&](int idx) {
       if (ev) cudaEventRecord(ev[idx], s);
@@ -364,11 +366,19 @@ struct grace_ctx {
       CE(alltoall(&Rank::A, &Rank::B, cs, q));
       CE(cudaEventRecord(evc[q], cs));
     }
+    set_pdl_blocked(true);  // K2(q) waits on the comm stream: no programmatic edge
     for (int q = 0; q < 3; ++q) {
       CE(cudaStreamWaitEvent(s, evc[q], 0));
-      for (auto& rk : ranks)
-        if (rk.g.Kc > 0) CE(launch_k2(comp_geom(rk, q), rk.B, rk.X2, tw, s, rk.tma ? &rk.k2map : nullptr));
+      for (auto& rk : ranks) {
+        if (rk.g.Kc == 0) continue;
+        const cudaError_t e = launch_k2(comp_geom(rk, q), rk.B, rk.X2, tw, s, rk.tma ? &rk.k2map : nullptr);
+        if (e != cudaSuccess) {
+          set_pdl_blocked(false);
+          return e;
+        }
+      }
     }
+    set_pdl_blocked(false);
     for (auto& rk : ranks)
       if (rk.g.Kc > 0)
         CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s, rk.tma3 ? &rk.k3x : nullptr, rk.tma3 ? &rk.k3k : nullptr));
@@ -391,11 +401,15 @@ struct grace_ctx {
       for (auto& rk : ranks) CE(launch_k5(rk.g, rk.A, rk.Hd, tw, s));
       return cudaSuccess;
     }
-    for (int q = 0; q < 3; ++q) {
-      CE(cudaStreamWaitEvent(s, evc[q], 0));
-      for (auto& rk : ranks) CE(launch_k5(comp_geom(rk, q), rk.A, rk.Hd, tw, s));
+    set_pdl_blocked(true);  // K5(q) waits on the comm stream: no programmatic edge
+    cudaError_t e = cudaSuccess;
+    for (int q = 0; q < 3 && e == cudaSuccess; ++q) {
+      e = cudaStreamWaitEvent(s, evc[q], 0);
+      for (auto& rk : ranks)
+        if (e == cudaSuccess) e = launch_k5(comp_geom(rk, q), rk.A, rk.Hd, tw, s);
     }
-    return cudaSuccess;
+    set_pdl_blocked(false);
+    return e;
   }
 
   // One Heun step, M[c] -> M[c]: predictor M* = renorm(M + dt f0) into M[1-c]
@@ -997,11 +1011,10 @@ int grace_heff(grace_ctx* h, double* out) {
     }
   CUDA_OR(h->upload_params(1e-15, true));
   CUDA_OR(h->demag_stages(h->cur, s, false));
+  CUDA_OR(h->k5_stage(s));
   CUDA_OR(h->halo_join(s));
-  for (auto& rk : h->ranks) {
-    CUDA_OR(launch_k5(rk.g, rk.A, rk.Hd, h->tw, s));
+  for (auto& rk : h->ranks)
     CUDA_OR(launch_k6(rk.g, 1, rk.Hd, rk.M[h->cur], nullptr, rk.Hbuf, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
-  }
   for (auto& rk : h->ranks) {
     double* stage = reinterpret_cast<double*>(rk.A);
     const size_t off = slab_offset(h, rk);
@@ -1122,9 +1135,8 @@ static int diagnostics(grace_ctx* h, double S[5]) {
   }
   CUDA_OR(h->upload_params(1e-15, true));
   CUDA_OR(h->demag_stages(h->cur, s, false));
+  CUDA_OR(h->k5_stage(s));
   CUDA_OR(h->halo_join(s));
-  for (auto& rk : h->ranks)
-    CUDA_OR(launch_k5(rk.g, rk.A, rk.Hd, h->tw, s));
   for (int q = 0; q < 4; ++q) S[q] = 0.0;
   S[4] = 0.0;
   for (auto& rk : h->ranks) {

@@ -94,6 +94,7 @@ cudaError_t launch_k6(const Geom& g, int mode, const float* Hd, const float* M, 
                       const float* Hhi);
 bool fused_y_path(const Geom& g);  // nz == 1 and the y-pencils of 3 components fit one CTA
 bool comp_split_ok(const Geom& g); // K1 .. K5 can run per component (bulk-copy x kernels)
+void set_pdl_blocked(bool b);      // this thread's next launches without programmatic dependent launch
 int kernel_count(const Geom& g);   // kernels per step
 
 // Utilities (step_kernels.cu).

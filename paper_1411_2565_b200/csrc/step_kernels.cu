@@ -1349,9 +1349,14 @@ struct ZCfg {  // K3 and K2'
 // an early-launched persistent K4 behind K3, or K6 behind K5, measured slower on
 // the slab (+0.14 / +0.08 ms); the rest gain 4-10% on small grids (SP4, film).
 // GRACE_PDL_MASK overrides, GRACE_NO_PDL turns it off.
+// A kernel that follows a wait on another stream's event (the pipelined
+// distributed step: K2 after its C1 transpose, K5 after its C2) is launched
+// without PDL: the programmatic edge would tie it to the preceding kernel only.
+static thread_local bool t_no_pdl = false;
+void set_pdl_blocked(bool b) { t_no_pdl = b; }
 static bool pdl_on(int kid) {
   static const int mask = getenv("GRACE_NO_PDL") ? 0 : (getenv("GRACE_PDL_MASK") ? atoi(getenv("GRACE_PDL_MASK")) : 23);
-  return (mask & kid) != 0;
+  return !t_no_pdl && (mask & kid) != 0;
 }
 // Step-kernel launch with programmatic stream serialization (PDL, see pdl_wait).
 template <class... E, class... A>
