@@ -105,6 +105,45 @@ class Sim:
         self.M = Mn
         self.step_count += 1
 
+    def adaptive_run(self, t_span, dt0, tol, safety=0.9, fac_min=0.2, fac_max=5.0, max_attempts=10**7):
+        """Adaptive time steps ("adaptive time steps" -- the paper's stated
+        future work) by the embedded Euler / Heun pair.
+
+        One attempt from M_k with step dt (H_eff as in euler_step / heun_step):
+            f0 = rhs(M_k, H(M_k));       M_E = renorm(M_k + dt f0)   (Euler, order 1)
+            f1 = rhs(M_E, H(M_E));       M_H = renorm(M_k + dt (f0 + f1)/2)   (Heun, order 2)
+            err = max over cells |M_H - M_E| / Ms   (estimate of the Euler step's local error, O(dt^2))
+        err <= tol: accept (M <- M_H, t <- t + dt), else reject (M kept).  Either
+        way the next dt = dt * min(fac_max, max(fac_min, safety * sqrt(tol / err)))
+        (fac_max when err = 0), and the step that would pass t_span is shortened to
+        end on it.  A constant applied field only (a step-indexed schedule has no
+        meaning here).  Returns (log of (t, dt, err, accepted) per attempt, next dt)."""
+        if self.schedule is not None:
+            raise ValueError("adaptive steps take a constant applied field")
+        t, dt, log = 0.0, float(dt0), []
+        for _ in range(max_attempts):
+            if t >= t_span:
+                break
+            last = t + dt >= t_span
+            h = t_span - t if last else dt
+            f0 = llg_rhs(self.M, self.heff(), self.alpha, self.gamma0, self.Ms)
+            ME = renormalize(self.M + h * f0, self.Ms, self.mask)
+            f1 = llg_rhs(ME, self.heff(ME), self.alpha, self.gamma0, self.Ms)
+            MH = renormalize(self.M + (0.5 * h) * (f0 + f1), self.Ms, self.mask)
+            d = MH - ME
+            err = float(np.sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]).max()) / self.Ms
+            if not np.isfinite(err) or not np.isfinite(MH).all():
+                raise NonFinite(self.step_count, int(np.flatnonzero((~np.isfinite(MH).all(axis=0)).ravel())[0]))
+            ok = err <= tol
+            log.append((t, h, err, ok))
+            fac = fac_max if err == 0.0 else min(fac_max, max(fac_min, safety * np.sqrt(tol / err)))
+            if ok:
+                self.M = MH
+                self.step_count += 1
+                t = t_span if last else t + h
+            dt = h * fac
+        return log, dt
+
     def run(self, n, dt, method="euler"):
         step = self.heun_step if method == "heun" else self.euler_step
         for _ in range(n):

@@ -267,3 +267,56 @@ def test_heun_second_order_vs_euler_first_order():
     err = {m: [np.abs(run(m, T / (base * k), base * k) - ref).max() for k in (1, 2)] for m in ("euler", "heun")}
     assert 3.5 < err["heun"][0] / err["heun"][1] < 4.5, err
     assert 1.7 < err["euler"][0] / err["euler"][1] < 2.3, err
+
+
+# ---------------------------------------------------------------- adaptive steps
+
+def test_adaptive_single_cell_precession_closed_forms():
+    """One cube cell, alpha = 0, H perpendicular to M (its demag field is parallel to M):
+    the Euler attempt rotates by atan(phi) and the Heun one by psi(phi) (the exact maps
+    pinned above), phi = gamma0 H dt, so the error estimate of an attempt of step dt is
+    exactly 2 sin(|psi - atan(phi)|/2), and the accepted steps rotate by the sum of psi."""
+    g0, Hm, Ms = 2.211e5, 1e5, 8e5
+    M0 = np.zeros((3, 1, 1, 1))
+    M0[0] = Ms
+    sim = Sim(M0, _one_cube(), Ms, 0.0, 0.0, 0.0, g0, (2e-9,) * 3, hext=(0, 0, Hm))
+    tol, T = 1e-5, 3e-11
+    log, dt_next = sim.adaptive_run(T, 1e-15, tol)
+    ang = 0.0
+    for t, h, err, ok in log:
+        phi = g0 * Hm * h
+        want = 2.0 * np.sin(abs(heun_precession_angle(phi) - np.arctan(phi)) / 2.0)
+        assert abs(err - want) <= 1e-12, (h, err, want)
+        assert ok == (err <= tol)
+        if ok:
+            ang += heun_precession_angle(phi)
+    acc = [x for x in log if x[3]]
+    assert abs(sum(x[1] for x in acc) - T) <= 1e-9 * T  # lands on T
+    assert any(not x[3] for x in log) or len(acc) == len(log)
+    np.testing.assert_allclose(sim.M[:, 0, 0, 0], Ms * np.array([np.cos(ang), np.sin(ang), 0.0]), rtol=0,
+                               atol=1e-12 * Ms)
+    # the controller grows a tiny first step and then runs near the tolerance
+    assert acc[-2][2] > 0.1 * tol and max(x[2] for x in acc) <= tol
+    assert dt_next > 0
+
+
+def test_adaptive_tolerance_controls_the_global_error():
+    """Multi-cell case through the full H_eff: the error at a fixed time against a
+    fine fixed-step Heun reference falls with the tolerance, and a tighter
+    tolerance takes more steps."""
+    n, d, Ms = (4, 3, 2), (3e-9, 3e-9, 3e-9), 8e5
+    M0 = RNG.standard_normal((3,) + n[::-1])
+    M0 *= Ms / np.sqrt((M0 * M0).sum(0))
+    op = DemagFFT(tensor_octant(*n, *d))
+    T = 2e-12
+    ref = Sim(M0, op, Ms, 1.3e-11, 2e4, 0.05, 2.211e5, d, hext=(1e4, 0, 5e4))
+    ref.run(6400, T / 6400, "heun")
+    res = []
+    for tol in (1e-3, 1e-4, 1e-5):
+        s = Sim(M0, op, Ms, 1.3e-11, 2e4, 0.05, 2.211e5, d, hext=(1e4, 0, 5e4))
+        log, _ = s.adaptive_run(T, 1e-16, tol)
+        res.append((np.abs(s.M - ref.M).max() / Ms, sum(1 for x in log if x[3])))
+        assert np.abs(np.sqrt((s.M ** 2).sum(0)) / Ms - 1).max() <= 1e-12
+    assert res[0][0] > res[1][0] > res[2][0], res
+    assert res[0][1] < res[1][1] < res[2][1], res
+    assert res[2][0] < 1e-4, res
