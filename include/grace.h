@@ -141,6 +141,22 @@ int grace_set_field_schedule(grace_ctx *h, double h0x, double h0y, double h0z, l
  * returns GRACE_EUNSUPPORTED for Heun in profiling mode. */
 int grace_set_integrator(grace_ctx *h, int kind);
 
+/* Adaptive time steps ("adaptive time steps" -- the paper's future work;
+ * SURVEY 8(f) #4(iv); the oracle twin is oracle.llg.Sim.adaptive_run).  Advances
+ * the state by t_span seconds with the embedded Euler / Heun pair: an attempt
+ * of step dt computes the Euler step M_E = renorm(M + dt f0) and the Heun step
+ * M_H = renorm(M + dt (f0 + f(M_E))/2); err = max over cells |M_H - M_E| / Ms
+ * (the Euler step's local error estimate).  err <= tol accepts M_H, else the
+ * attempt is discarded; the next dt = dt * min(5, max(0.2, 0.9 sqrt(tol/err))),
+ * and the last step is shortened to end on t_span.  *dt_io: first trial step in,
+ * suggested next step out.  Eager launches and one device-to-host read per
+ * attempt.  accepted / rejected: attempts of each kind (accepted ones advance
+ * grace_step_count).  GRACE_EINVAL for t_span < 0, dt <= 0, tol <= 0,
+ * max_attempts < 1; GRACE_EUNSUPPORTED with a field schedule; GRACE_ENONFINITE
+ * as grace_step.  Collective on the NCCL path (the error is max-reduced). */
+int grace_step_adaptive(grace_ctx *h, double t_span, double *dt_io, double tol, long long max_attempts,
+                        long long *accepted, long long *rejected);
+
 /* Geometry mask (the paper's "non-regular geometry", P:L121;
  * DESIGN.md reading Q26).  mask: host uint8 [nz][ny][nx] (the rank-local slab
  * [nz/P][ny][nx] for grace_create_dist), nonzero = magnetic cell, copied before
@@ -199,7 +215,7 @@ int grace_kernel_times(grace_ctx *h, double *ms, long long *launches, int *nk, i
  *
  * Collective calls on the NCCL path (call them on every rank, in the same order):
  * grace_create_dist, grace_step, grace_heff, grace_mavg, grace_energy,
- * grace_max_torque, grace_relax, grace_set_geometry, grace_set_m,
+ * grace_max_torque, grace_relax, grace_step_adaptive, grace_set_geometry, grace_set_m,
  * grace_set_m_device (their status is agreed over the ranks: a non-finite value
  * or zero cell anywhere is reported by every rank, with the global cell index). */
 

@@ -64,6 +64,7 @@ SIGNATURES = [
     ("grace_create_dist", _I, [_I, _I, _I, _D, _D, _D, _D, _D, _D, _D, _D, _I, _I, _P, ctypes.POINTER(_P)]),
     ("grace_partition", _I, [_P, _PLL]),
     ("grace_set_geometry", _I, [_P, _P]),
+    ("grace_step_adaptive", _I, [_P, _D, _PD, _D, ctypes.c_longlong, _PLL, _PLL]),
 ]
 
 _lib = None
@@ -221,6 +222,15 @@ def grace_set_field_schedule(h, h0, start, decay, stop):
                                            int(stop)))
 
 
+def grace_step_adaptive(h, t_span, dt, tol, max_attempts=10**9):
+    """Advance t_span seconds with adaptive steps; returns (next dt, accepted, rejected)."""
+    d = ctypes.c_double(dt)
+    a, r = ctypes.c_longlong(0), ctypes.c_longlong(0)
+    _check(load().grace_step_adaptive(h, t_span, ctypes.byref(d), tol, max_attempts, ctypes.byref(a),
+                                      ctypes.byref(r)))
+    return d.value, a.value, r.value
+
+
 def grace_set_integrator(h, kind):
     _check(load().grace_set_integrator(h, {"euler": 0, "heun": 1}.get(kind, kind)))
 
@@ -375,6 +385,9 @@ class Grace:
         if m.size != int(np.prod(self.shape[1:])):
             raise ValueError(f"mask of {m.size} cells for a grid of {int(np.prod(self.shape[1:]))}")
         grace_set_geometry(self.h, m.ctypes.data)
+
+    def step_adaptive(self, t_span, dt, tol, max_attempts=10**9):
+        return grace_step_adaptive(self.h, t_span, dt, tol, max_attempts)
 
     def set_integrator(self, kind):
         """'euler' (the paper's, default) or 'heun' (second order, two H_eff per step)."""

@@ -71,7 +71,7 @@ typedef int ncclResult_t;
 struct ncclUniqueId {
   char internal[128];
 };
-enum { kNcclUint64 = 5, kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0, kNcclMax = 2, kNcclMin = 3 };
+enum { kNcclUint32 = 3, kNcclUint64 = 5, kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0, kNcclMax = 2, kNcclMin = 3 };
 struct Nccl {
   void* h = nullptr;
   ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
@@ -140,6 +140,7 @@ struct Rank {
   float* Hbuf = nullptr;
   float* Hd = nullptr;                 // H_demag [3][nzl][ny][nx] (split K5/K6 step)
   float* F = nullptr;                  // Heun: dM/dt of the predictor stage
+  unsigned* aerr = nullptr;            // grace_step_adaptive: error estimate (float bits), allocated on first use
   unsigned char* mask = nullptr;       // geometry mask [nzl][ny][nx] (grace_set_geometry; null: none)
   bool tma = false;                    // TMA descriptors of the K2 / K4 inputs built
   TmapBlob k2map{}, k4map{};
@@ -504,8 +505,8 @@ struct grace_ctx {
     }
     for (auto e : ev) cudaEventDestroy(e);
     for (auto& rk : ranks) {
-      void* ptrs[] = {rk.M[0], rk.M[1], rk.A,   rk.B,    rk.X2,  rk.KS,   rk.Hlo,
-                      rk.Hhi,  rk.prm,  rk.flag, rk.red, rk.Hbuf, rk.Hd,  rk.dred, rk.F, rk.mask};
+      void* ptrs[] = {rk.M[0], rk.M[1], rk.A,   rk.B,    rk.X2,  rk.KS,   rk.Hlo, rk.Hhi,
+                      rk.prm,  rk.flag, rk.red, rk.Hbuf, rk.Hd,  rk.dred, rk.F,   rk.mask, rk.aerr};
       for (void* p : ptrs)
         if (p) cudaFree(p);
     }
@@ -1093,6 +1094,93 @@ int grace_step(grace_ctx* h, int n, double dt) {
     h->nf_cell = (long long)(f & ((1ULL << 36) - 1));
     return fail(GRACE_ENONFINITE, "non-finite magnetisation at step %lld, cell %lld (dt too large?)", h->nf_step,
                 h->nf_cell);
+  }
+  return GRACE_OK;
+}
+
+int grace_step_adaptive(grace_ctx* h, double t_span, double* dt_io, double tol, long long max_attempts,
+                        long long* accepted, long long* rejected) {
+  if (!h || !dt_io || !accepted || !rejected) return fail(GRACE_EINVAL, "NULL argument");
+  if (!std::isfinite(t_span) || t_span < 0 || !finite_pos(*dt_io) || !finite_pos(tol) || max_attempts < 1)
+    return fail(GRACE_EINVAL, "adaptive steps need t_span >= 0, dt > 0, tol > 0, max_attempts >= 1");
+  if (h->has_sched) return fail(GRACE_EUNSUPPORTED, "adaptive steps take a constant applied field (no schedule)");
+  cudaStream_t s = h->stream;
+  for (auto& rk : h->ranks) {
+    if (!rk.F) {
+      int rc = h->alloc((void**)&rk.F, sizeof(float) * 3 * (size_t)rk.Nl);
+      if (rc) return rc;
+    }
+    if (!rk.aerr) {
+      int rc = h->alloc((void**)&rk.aerr, sizeof(unsigned));
+      if (rc) return rc;
+    }
+  }
+  // controller constants (the oracle's Sim.adaptive_run)
+  const double safety = 0.9, fac_min = 0.2, fac_max = 5.0;
+  const int c = h->cur;
+  double t = 0.0, dt = *dt_io;
+  long long acc = 0, rej = 0;
+  int rc = GRACE_OK;
+  while (t < t_span && acc + rej < max_attempts) {
+    const bool last = t + dt >= t_span;
+    const double hs = last ? t_span - t : dt;
+    if (!(hs > 0)) break;
+    CUDA_OR(h->upload_params(hs));
+    for (auto& rk : h->ranks) CUDA_OR(cudaMemsetAsync(rk.aerr, 0, sizeof(unsigned), s));
+    // Euler attempt M_E = renorm(M + dt f0) into M[1-c] (f0 kept in F) ...
+    CUDA_OR(h->demag_stages(c, s, false));
+    CUDA_OR(h->k5_stage(s));
+    CUDA_OR(h->halo_join(s));
+    for (auto& rk : h->ranks)
+      CUDA_OR(launch_k6(rk.g, 3, rk.Hd, rk.M[c], rk.M[1 - c], rk.F, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi));
+    // ... and the Heun step M_H = renorm(M + dt (f0 + f(M_E))/2) over F, with max |M_H - M_E| / Ms
+    CUDA_OR(h->demag_stages(1 - c, s, false));
+    CUDA_OR(h->k5_stage(s));
+    CUDA_OR(h->halo_join(s));
+    for (auto& rk : h->ranks)
+      CUDA_OR(launch_k6(rk.g, 5, rk.Hd, rk.M[1 - c], rk.M[c], rk.F, rk.prm, rk.flag, s, rk.Hlo, rk.Hhi, rk.aerr));
+    unsigned bits = 0;
+    for (auto& rk : h->ranks) {
+      if (h->mode == grace_ctx::kNccl) {
+        const ncclResult_t r = g_nccl.allReduce(rk.aerr, rk.aerr, 1, kNcclUint32, kNcclMax, h->comm, s);
+        if (r != 0) return fail(GRACE_ECUDA, "ncclAllReduce: %s", g_nccl.errStr(r));
+      }
+      CUDA_OR(cudaMemcpyAsync(&h->pin->flag, rk.aerr, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+      CUDA_OR(cudaStreamSynchronize(s));
+      unsigned b;
+      std::memcpy(&b, &h->pin->flag, sizeof b);
+      bits = std::max(bits, b);
+    }
+    float errf;
+    std::memcpy(&errf, &bits, sizeof errf);
+    const double err = errf;
+    if (!std::isfinite(err)) {
+      rc = fail(GRACE_ENONFINITE, "non-finite magnetisation in an adaptive attempt (dt %g s)", hs);
+      break;
+    }
+    const double fac = err == 0.0 ? fac_max : std::min(fac_max, std::max(fac_min, safety * std::sqrt(tol / err)));
+    if (err <= tol) {  // accept: M[c] <- M_H
+      for (auto& rk : h->ranks)
+        CUDA_OR(cudaMemcpyAsync(rk.M[c], rk.F, sizeof(float) * 3 * (size_t)rk.Nl, cudaMemcpyDeviceToDevice, s));
+      t = last ? t_span : t + hs;
+      ++acc;
+      ++h->steps;
+    } else {
+      ++rej;
+    }
+    dt = hs * fac;
+  }
+  unsigned long long f;
+  int rc2 = check_flags(h, 0, &f);
+  *dt_io = dt;
+  *accepted = acc;
+  *rejected = rej;
+  if (rc) return rc;
+  if (rc2) return rc2;
+  if (f != kNoFlag) {
+    h->nf_step = (long long)(f >> 36);
+    h->nf_cell = (long long)(f & ((1ULL << 36) - 1));
+    return fail(GRACE_ENONFINITE, "non-finite magnetisation at cell %lld", h->nf_cell);
   }
   return GRACE_OK;
 }

@@ -89,9 +89,10 @@ cudaError_t launch_k2f(const Geom& g, float2* X1, const float* KS, const float2*
 cudaError_t launch_k5(const Geom& g, const float2* X1, float* Hd, const float2* tw, cudaStream_t st);
 // K6: local terms + LLG + Euler from H_demag (mode 0: M -> Mn; mode 1: H_eff -> Hout).
 // Hlo / Hhi: halo planes [3][ny][nx] of z-1 / z+1 (used when g.has_lo / g.has_hi).
+// mode 3 / 4: Heun predictor / corrector; mode 5: adaptive-step corrector (error into *aerr).
 cudaError_t launch_k6(const Geom& g, int mode, const float* Hd, const float* M, float* Mn, float* Hout,
                       const StepParams* prm, unsigned long long* flag, cudaStream_t st, const float* Hlo,
-                      const float* Hhi);
+                      const float* Hhi, unsigned* aerr = nullptr);
 bool fused_y_path(const Geom& g);  // nz == 1 and the y-pencils of 3 components fit one CTA
 bool comp_split_ok(const Geom& g); // K1 .. K5 can run per component (bulk-copy x kernels)
 void set_pdl_blocked(bool b);      // this thread's next launches without programmatic dependent launch

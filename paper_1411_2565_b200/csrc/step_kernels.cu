@@ -1088,7 +1088,10 @@ __global__ void __launch_bounds__(XBulk<L>::NT, GRACE_XB_MINB)
 #endif
 // HEUN = 3: predictor (also stores f = dM/dt into Hout); HEUN = 4: corrector,
 // M' = renorm(M0 + dt (f0 + f(M*)) / 2) with M0 = Mn (updated in place), f0 = Hout,
-// M* = M; the applied field of the next timestep.  HEUN = 0: modes 0 / 1.
+// M* = M; the applied field of the next timestep.  HEUN = 5: the adaptive-step
+// corrector (grace_step_adaptive): the same M' written over f0 in Hout (M0 kept
+// for a rejected attempt), and max over cells |M' - M*| / Ms -- the Euler step's
+// local error estimate -- into *aerr (float bits, atomic max).  HEUN = 0: modes 0 / 1.
 // MASK (geometry mask, reading Q26): a cell with M = 0 is empty; an empty
 // neighbour is a free surface (replaced by the centre, like a missing one), an
 // empty centre stays 0 (H_eff 0, f 0).
@@ -1096,7 +1099,8 @@ template <bool VEC, bool DIST, int HEUN = 0, bool MASK = false>
 __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __restrict__ Hd, const float* __restrict__ M,
                                               float* __restrict__ Mn, float* __restrict__ Hout, Geom g,
                                               const StepParams* __restrict__ prm, unsigned long long* __restrict__ flag,
-                                              int mode, const float* __restrict__ Hlo, const float* __restrict__ Hhi) {
+                                              int mode, const float* __restrict__ Hlo, const float* __restrict__ Hhi,
+                                              unsigned* __restrict__ aerr) {
   pdl_trigger();
   pdl_wait();
   constexpr int W = VEC ? 4 : 1;
@@ -1120,7 +1124,7 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
   float ha[3];
   {
     StepParams pf = p;
-    if (HEUN == 4) pf.step += 1;  // the corrector's field: timestep k + 1
+    if (HEUN >= 4) pf.step += 1;  // the corrector's field: timestep k + 1
     applied_field(pf, ha);
   }
   // all 24 loads (3 components x centre, Hd, 4 neighbour rows, 2 row ends) first
@@ -1187,7 +1191,7 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
     }
   }
   float o[3][W], f[3][W], m0[3][W];
-  if constexpr (HEUN == 4) {
+  if constexpr (HEUN >= 4) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       ldw(Hout + c * N + i, f[c]);
@@ -1216,7 +1220,7 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
     const float ax = my * hz - mz * hy, ay = mz * hx - mx * hz, az = mx * hy - my * hx;
     const float bx = my * az - mz * ay, by = mz * ax - mx * az, bz = mx * ay - my * ax;
     float sx, sy, sz;
-    if constexpr (HEUN == 4) {
+    if constexpr (HEUN >= 4) {
       const float dx = p.c_prec * ax + p.c_damp * bx, dy = p.c_prec * ay + p.c_damp * by,
                   dz = p.c_prec * az + p.c_damp * bz;
       const float hdt = 0.5f * p.dt;
@@ -1240,7 +1244,19 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
     if (!(isfinite(o[0][s]) && isfinite(o[1][s]) && isfinite(o[2][s])))
       atomicMin(flag, ((unsigned long long)(p.step - 1) << 36) | (unsigned long long)(i + s));
   }
-  float* dst = (HEUN == 0 && mode == 1) ? Hout : Mn;
+  if constexpr (HEUN == 5) {  // local error estimate |M_Heun - M_Euler| / Ms, max over cells
+    float e2 = 0.f;
+#pragma unroll
+    for (int s = 0; s < W; ++s) {
+      const float d0 = o[0][s] - m[0][s], d1 = o[1][s] - m[1][s], d2 = o[2][s] - m[2][s];
+      e2 = fmaxf(e2, d0 * d0 + d1 * d1 + d2 * d2);
+    }
+    const float ev = sqrtf(e2) / g.Ms;
+    // non-negative floats order like their bit patterns; NaN (all bits set past inf) wins the max
+    const unsigned bits = __reduce_max_sync(__activemask(), isnan(ev) ? 0x7fffffffu : __float_as_uint(ev));
+    if ((threadIdx.x & 31) == __ffs(__activemask()) - 1 && bits != 0u) atomicMax(aerr, bits);
+  }
+  float* dst = (HEUN == 0 && mode == 1) || HEUN == 5 ? Hout : Mn;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     if constexpr (VEC) *reinterpret_cast<float4*>(dst + c * N + i) = make_float4(o[c][0], o[c][1], o[c][2], o[c][3]);
@@ -1717,34 +1733,37 @@ int kernel_count(const Geom& g) { return (fused_y_path(g) ? 3 : 5) + 1; }
 template <int HEUN, bool MASK>
 static cudaError_t k6_launch(const Geom& g, int mode, const float* Hd, const float* M, float* Mn, float* Hout,
                              const StepParams* prm, unsigned long long* flag, cudaStream_t st, const float* Hlo,
-                             const float* Hhi) {
+                             const float* Hhi, unsigned* aerr) {
   const long long N = (long long)g.nzl * g.ny * g.nx;
   const bool vec = g.nx % 4 == 0;
   const long long threads = vec ? N / 4 : N;
   const unsigned grid = (unsigned)((threads + 255) / 256);
   if (vec) {
-    if (g.kb) GRACE_TRY(launch_k(32, k6_llg<true, true, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
-    else GRACE_TRY(launch_k(32, k6_llg<true, false, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
+    if (g.kb) GRACE_TRY(launch_k(32, k6_llg<true, true, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi, aerr));
+    else GRACE_TRY(launch_k(32, k6_llg<true, false, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi, aerr));
   } else {
-    if (g.kb) GRACE_TRY(launch_k(32, k6_llg<false, true, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
-    else GRACE_TRY(launch_k(32, k6_llg<false, false, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi));
+    if (g.kb) GRACE_TRY(launch_k(32, k6_llg<false, true, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi, aerr));
+    else GRACE_TRY(launch_k(32, k6_llg<false, false, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi, aerr));
   }
   return cudaGetLastError();
 }
 
 // mode 0: Euler step M -> Mn; 1: H_eff -> Hout; 3: Heun predictor (M* -> Mn,
-// dM/dt -> Hout); 4: Heun corrector (M = M*, Mn = M_k updated in place, Hout = f0).
+// dM/dt -> Hout); 4: Heun corrector (M = M*, Mn = M_k updated in place, Hout = f0);
+// 5: adaptive corrector (M = M*, Mn = M_k kept, Hout = f0 -> M', error into aerr).
 cudaError_t launch_k6(const Geom& g, int mode, const float* Hd, const float* M, float* Mn, float* Hout,
                       const StepParams* prm, unsigned long long* flag, cudaStream_t st, const float* Hlo,
-                      const float* Hhi) {
+                      const float* Hhi, unsigned* aerr) {
   if (g.masked) {  // geometry mask (reading Q26)
-    if (mode == 3) return k6_launch<3, true>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
-    if (mode == 4) return k6_launch<4, true>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
-    return k6_launch<0, true>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
+    if (mode == 3) return k6_launch<3, true>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi, aerr);
+    if (mode == 4) return k6_launch<4, true>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi, aerr);
+    if (mode == 5) return k6_launch<5, true>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi, aerr);
+    return k6_launch<0, true>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi, aerr);
   }
-  if (mode == 3) return k6_launch<3, false>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
-  if (mode == 4) return k6_launch<4, false>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
-  return k6_launch<0, false>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi);
+  if (mode == 3) return k6_launch<3, false>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi, aerr);
+  if (mode == 4) return k6_launch<4, false>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi, aerr);
+  if (mode == 5) return k6_launch<5, false>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi, aerr);
+  return k6_launch<0, false>(g, mode, Hd, M, Mn, Hout, prm, flag, st, Hlo, Hhi, aerr);
 }
 
 template <int L>
