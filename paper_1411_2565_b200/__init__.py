@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgrace.so")
+# GRACE_LIB_PATH: an alternative in-tree build (tuning sweeps of compile-time knobs)
+LIB_PATH = os.environ.get("GRACE_LIB_PATH") or os.path.join(_HERE, "libgrace.so")
 
 GRACE_OK = 0
 GRACE_EINVAL = -1
