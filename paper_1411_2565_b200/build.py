@@ -21,8 +21,9 @@ UNITS = {
     "step_kernels.cu": (["--split-compile=0"] if os.environ.get("GRACE_SPLIT_COMPILE") else [])
     + (["-Xptxas", "-v"] if os.environ.get("GRACE_PTXAS_V") else []),
     "tensor_setup.cu": ["-fmad=false"],
+    "small_step.cu": [],
 }
-HEADERS = ["fft_engine.cuh", "internal.h"]
+HEADERS = ["fft_engine.cuh", "internal.h", "pencil.cuh"]
 
 
 def _mtime(p):

@@ -1042,6 +1042,12 @@ int grace_step(grace_ctx* h, int n, double dt) {
       if (e != cudaSuccess) return fail(GRACE_ECUDA, "distributed step: %s", cudaGetErrorString(e));
       h->cur = h->next(h->cur);
     }
+  } else if (h->mode == grace_ctx::kSingle && !h->profiling && h->integrator == 0 && small_path_ok(h->ranks[0].g)) {
+    // small nz = 1 grids: the whole call in one cluster-resident kernel (small_step.cu)
+    Rank& rk = h->ranks[0];
+    const int dst = h->cur ^ (n & 1);
+    CUDA_OR(launch_small_step(rk.g, rk.M[h->cur], rk.M[dst], rk.KS, h->tw, rk.prm, rk.flag, n, s));
+    h->cur = dst;
   } else if (h->profiling && h->integrator != 0) {
     return fail(GRACE_EUNSUPPORTED, "profiling mode times the Euler step only");
   } else if (h->profiling) {

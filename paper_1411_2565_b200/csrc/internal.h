@@ -98,6 +98,12 @@ bool comp_split_ok(const Geom& g); // K1 .. K5 can run per component (bulk-copy 
 void set_pdl_blocked(bool b);      // this thread's next launches without programmatic dependent launch
 int kernel_count(const Geom& g);   // kernels per step
 
+// Small-grid latency path (small_step.cu): n Euler steps of an nz = 1
+// grid in one thread-block cluster, all intermediates in distributed shared memory.
+bool small_path_ok(const Geom& g);
+cudaError_t launch_small_step(const Geom& g, const float* Min, float* Mout, const float* KS, const float2* tw,
+                              StepParams* prm, unsigned long long* flag, int nsteps, cudaStream_t st);
+
 // Utilities (step_kernels.cu).
 cudaError_t launch_twiddles(float2* tw, int Lmax, cudaStream_t st);
 cudaError_t launch_set_m_f64(const double* src, float* M, long long n, double Ms, const unsigned char* mask,

@@ -24,6 +24,7 @@
 
 #include "fft_engine.cuh"
 #include "internal.h"
+#include "pencil.cuh"
 
 namespace grace {
 
@@ -444,24 +445,6 @@ __global__ void __launch_bounds__(YStage<L>::NT, (L == 2048 ? GRACE_YSTAGE_MINB 
 }
 
 // ---------------------------------------------------------------------------
-// k-space multiply with the CTA's folded KS slice staged in smem:
-// kss[c][kf][b], c = 0..5 (xx xy xz yy yz zz), kf the folded index of the
-// staged axis.  fy / fz: the k index was folded along y / z, which flips the
-// sign of the components odd in that axis (xy, yz odd in y; xz, yz odd in z).
-__device__ __forceinline__ void kmul_s(float2& a, float2& b, float2& c, const float* kss, int KH, int B, int kf,
-                                       int bcol, bool fy, bool fz) {
-  const int cs = KH * B;
-  const float* p = kss + kf * B + bcol;
-  const float nxx = p[0], nyy = p[3 * cs], nzz = p[5 * cs];
-  const float nxy = fy ? -p[cs] : p[cs];
-  const float nxz = fz ? -p[2 * cs] : p[2 * cs];
-  const float nyz = (fy != fz) ? -p[4 * cs] : p[4 * cs];
-  const float2 mx = a, my = b, mz = c;
-  a = make_float2(nxx * mx.x + nxy * my.x + nxz * mz.x, nxx * mx.y + nxy * my.y + nxz * mz.y);
-  b = make_float2(nxy * mx.x + nyy * my.x + nyz * mz.x, nxy * mx.y + nyy * my.y + nyz * mz.y);
-  c = make_float2(nxz * mx.x + nyz * my.x + nzz * mz.x, nxz * mx.y + nyz * my.y + nzz * mz.y);
-}
-
 // Stage KS[c][k1][k2][kx0 .. kx0+B) for c = 0..5 into kss[c][k][b] with cp.async,
 // where the staged axis k runs over KH entries at stride kstride (floats) from `base`.
 // Columns at or beyond `avail` (= KSp - kx0: past the end of the KS row) are
@@ -485,117 +468,6 @@ __device__ __forceinline__ void stage_ks(float* kss, const float* __restrict__ b
       if (bb < avail) cp_async4(kss + r * B + bb, base + comp * cstride + k * kstride + bb);
       else kss[r * B + bb] = 0.f;
     }
-  }
-}
-
-// FFT along one pencil axis of the three components, H~ = KS . M~, inverse FFT.
-// The forward input has n nonzero of L (HIN), the inverse keeps n outputs (HOUT).
-// FUSE (L <= 64): the forward last pass, the multiply and the inverse first pass
-// (reversed radix plan) run in registers without a shared-memory round trip.
-#ifndef GRACE_ZB
-#define GRACE_ZB 16  // kx columns per K3 / K2' CTA (at most, except short pencils)
-#endif
-#ifndef GRACE_Z_MINNT
-#define GRACE_Z_MINNT 128
-#endif
-#ifndef GRACE_ZB_128
-#define GRACE_ZB_128 16
-#endif
-#ifndef GRACE_ZB_256
-#define GRACE_ZB_256 4
-#endif
-#ifndef GRACE_ZB_512
-#define GRACE_ZB_512 8
-#endif
-template <int L>
-struct ZPlan {
-  static constexpr bool FUSE = L >= 2 && L <= 64;
-  static constexpr int RLAST = L <= 1 ? 1 : 1 << fft_pass_bits(L, fft_npass(L) - 1);
-  // threads per column, unfused: L / R for the plan's largest radix R up to
-  // L = 512, so no pass leaves threads idle (L / 8 idled half of them in the
-  // radix-16 passes: 128^3 cube K3 0.32 -> 0.17 ms, block 17.9 -> 12.1 ms);
-  // L / 8 for L = 1024 (16.8.8: more threads beat the idle pass, 20.7 vs 23.0 ms)
-  static constexpr int R0 = L <= 1 ? 1 : 1 << fft_pass_bits(L, 0);
-  static constexpr int TPC = L <= 1 ? 1 : (FUSE ? L / RLAST : (L <= 512 ? L / R0 : L / 8));
-  // fused (short) pencils: at least GRACE_Z_MINNT threads per CTA; unfused:
-  // GRACE_Z_ELEMS values per component per CTA (smem: 3 components resident)
-  static constexpr int BF = (GRACE_Z_MINNT / TPC > GRACE_ZB ? GRACE_Z_MINNT / TPC : GRACE_ZB);
-  // unfused columns per CTA by length, measured (K3 ms): L = 128 16 (block
-  // 2048x2048x64: 12.1 vs 15.9 at 8; the 64^3 cube prefers 8, 0.021 vs 0.025);
-  // L = 256 (128^3) 4 (0.17, same at 8); L = 512 (256^3) 8 (1.45 vs 1.50 at 4,
-  // 2.17 at 2); L = 1024 (512^3) 4 (20.7 vs 26.9 at 2)
-  static constexpr int BN = L <= 128 ? GRACE_ZB_128 : (L == 256 ? GRACE_ZB_256 : (L == 512 ? GRACE_ZB_512 : (L == 1024 ? 4 : (2048 / L > 1 ? 2048 / L : 1))));
-  static constexpr int B = L <= 1 ? GRACE_ZB : (FUSE ? (BF < 2048 / L ? BF : 2048 / L) : BN);
-  static constexpr int NT = B * TPC < 32 ? 32 : B * TPC;
-};
-
-// kw(): called before the multiply's barrier -- waits for this thread's part of
-// the KS slice (cp.async group or TMA mbarrier).
-// TWS (fused plans only): tw is a shared table holding the forward plan's per-pass
-// twiddles followed by the reversed (inverse) plan's (fill_pass_twiddles of
-// Plan<L, false> then Plan<L, true>); else tw is the global table.
-template <int L, int B, int NT, bool TWS = false, class LD, class ST, class KW>
-__device__ __forceinline__ void pencil_conv(float2* smem, const LD& ld, const ST& st, const float* kss, int KH,
-                                            const float2* __restrict__ tw, int twstride, int P_other, int k_other,
-                                            bool fold_is_y, const KW& kw) {
-  // k along the pencil axis (length L = P_axis); the other folded axis index is
-  // fixed for the CTA.  fold_is_y: the pencil axis is y (K2'), else z (K3).
-  auto flags = [&](int k, bool& fy, bool& fz, int& kf) {
-    const bool fa = k > (L >> 1);
-    kf = fa ? L - k : k;
-    const bool fo = k_other > (P_other >> 1);
-    if (fold_is_y) {
-      fy = fa;
-      fz = false;
-    } else {
-      fy = fo;
-      fz = fa;
-    }
-  };
-  const ThreadMap<L, B, NT, true> tm;
-  static_assert(!TWS || ZPlan<L>::FUSE, "shared twiddle tables: fused plans only");
-  if constexpr (ZPlan<L>::FUSE) {
-    using PF = Pass<L, fft_npass(L) - 1, false, B, NT, true, 3>;
-    using PI = Pass<L, 0, true, B, NT, true, 3>;
-    static_assert(PF::R == PI::R && PF::UPT == 1 && PI::UPT == 1, "fused plan");
-    PF pf;
-    const float2* twi = TWS ? tw + Plan<L, false, 4>::TW_ELEMS : tw;
-    fft_to_regs<L, B, NT, true, 3, false, true, false, false, TWS>(tm, smem, ld, tw, twstride, pf);
-    kw();
-    __syncthreads();
-    PI pi;
-#pragma unroll
-    for (int r = 0; r < PF::R; ++r) {
-      const int k = PF::sb(tm) + PF::C2(0, r);
-      bool fy, fz;
-      int kf;
-      flags(k, fy, fz, kf);
-      float2 a = pf.v[0][0][r], b = pf.v[0][1][r], c = pf.v[0][2][r];
-      kmul_s(a, b, c, kss, KH, B, kf, tm.b, fy, fz);
-      pi.v[0][0][r] = a;
-      pi.v[0][1][r] = b;
-      pi.v[0][2][r] = c;
-    }
-    fft_from_regs<L, B, NT, true, 3, true, true, true, TWS>(tm, smem, st, twi, twstride, pi);
-  } else {
-    using T = TileIdx<L, B, true>;
-    fft_tile<L, B, NT, true, false, (L > 1), false, 3>(smem, ld, SmemSt<L, B, true>{smem}, tw, twstride);
-    kw();
-    __syncthreads();
-    for (int u = threadIdx.x; u < L * B; u += NT) {
-      const int k = u / B, b = u - k * B;
-      bool fy, fz;
-      int kf;
-      flags(k, fy, fz, kf);
-      float2* s0 = smem + T::at(b, k);
-      float2 a = s0[0], bb = s0[T::ELEMS], c = s0[2 * T::ELEMS];
-      kmul_s(a, bb, c, kss, KH, B, kf, b, fy, fz);
-      s0[0] = a;
-      s0[T::ELEMS] = bb;
-      s0[2 * T::ELEMS] = c;
-    }
-    __syncthreads();
-    fft_tile<L, B, NT, true, true, false, (L > 1), 3>(smem, SmemLd<L, B, true>{smem}, st, tw, twstride);
   }
 }
 
