@@ -298,8 +298,13 @@ static cudaError_t small_launch(const Geom& g, const SmallArgs& a0, cudaStream_t
 }
 
 // Which (LX, PY, C) instantiation serves this grid (0: none -> the pencil path).
+// Opt-in (GRACE_SMALL=1): measured slower than the graph-replayed pencil path on
+// one B200 (SP4 coarse 13.8 vs 10.9 us/step, refined 29.3 vs 14.1):
+// one cluster of 8-16 SMs at 4 warps each is compute-starved, while the pencil
+// path's four kernels spread each stage over the whole GPU.
 static int small_kind(const Geom& g) {
-  if (getenv("GRACE_NO_SMALL")) return 0;
+  const char* on = getenv("GRACE_SMALL");
+  if (!on || on[0] != '1') return 0;
   if (g.nz != 1 || g.Pz != 1 || g.kb != 0 || g.masked) return 0;
   const int LX = g.Px / 2;
   if (LX == 128 && g.Py == 64) return 1;   // SP4 coarse 100x25x1
