@@ -332,9 +332,10 @@ def run_own(args, w):
     # e2e through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        Mh = torch.empty(3 * Nloc, dtype=torch.float64, pin_memory=True)
-        Mh.copy_(torch.from_numpy(np.ascontiguousarray(Mloc).ravel()))
-        Mout = torch.empty(3 * Nloc, dtype=torch.float64, pin_memory=True)
+        # fp32 host buffers (the device state is fp32): 12 B/cell each way
+        Mh = torch.empty(3 * Nloc, dtype=torch.float32, pin_memory=True)
+        Mh.copy_(torch.from_numpy(np.ascontiguousarray(Mloc, dtype=np.float32).ravel()))
+        Mout = torch.empty(3 * Nloc, dtype=torch.float32, pin_memory=True)
         mh = Mh.numpy()
         mo = Mout.numpy()
         torch.cuda.synchronize()
@@ -342,12 +343,12 @@ def run_own(args, w):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        pb.grace_set_m(g.h, mh)
+        pb.grace_set_m_f32(g.h, mh)
         for _ in range(args.steps):
             g.set_hext(w.hext)
             g.step(1, w.dt)
             g.mavg()
-        pb.grace_get_m(g.h, mo)
+        pb.grace_get_m_f32(g.h, mo)
         e1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
@@ -358,9 +359,10 @@ def run_own(args, w):
             tms = float(t.item())
         K = args.steps
         e2e = {"value": (N if distributed else world * N) * K / (tms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": (24 * Nloc + 40 * K) / K, "d2h_bytes_per_step": (24 * Nloc + 32 * K) / K,
+               "h2d_bytes_per_step": (12 * Nloc + 40 * K) / K, "d2h_bytes_per_step": (12 * Nloc + 32 * K) / K,
                "ms_per_step": tms / K, "host_wall_s": wall,
-               "api": "grace_set_m(pinned) + K x (grace_set_hext, grace_step(1), grace_mavg) + grace_get_m(pinned)"}
+               "api": "grace_set_m_f32(pinned fp32 M) + K x (grace_set_hext, grace_step(1), grace_mavg -> host) + "
+                      "grace_get_m_f32(pinned)"}
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

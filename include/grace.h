@@ -101,6 +101,14 @@ int grace_set_stream(grace_ctx *h, void *cuda_stream);
 int grace_set_m_device(grace_ctx *h, const float *d_m);
 int grace_get_m_device(grace_ctx *h, float *d_m_out);
 
+/* Host fp32 variants of grace_set_m / grace_get_m (SoA [3][nz][ny][nx], A/m;
+ * the rank-local slab on the NCCL path): the device state is fp32, so these move
+ * 12 bytes per cell each way instead of 24 (pinned host memory gives full PCIe
+ * bandwidth).  set renormalises like grace_set_m (GRACE_EZEROCELL likewise);
+ * both return after the copy has completed. */
+int grace_set_m_f32(grace_ctx *h, const float *m);
+int grace_get_m_f32(grace_ctx *h, float *m_out);
+
 /* <M>/Ms (3 doubles) by a fixed-order two-stage reduction (deterministic). */
 int grace_mavg(grace_ctx *h, double *out3);
 

@@ -66,6 +66,8 @@ SIGNATURES = [
     ("grace_partition", _I, [_P, _PLL]),
     ("grace_set_geometry", _I, [_P, _P]),
     ("grace_step_adaptive", _I, [_P, _D, _PD, _D, ctypes.c_longlong, _PLL, _PLL]),
+    ("grace_set_m_f32", _I, [_P, _PF]),
+    ("grace_get_m_f32", _I, [_P, _PF]),
 ]
 
 _lib = None
@@ -172,6 +174,22 @@ def grace_set_m(h, m):
 
 def grace_get_m(h, out):
     _check(load().grace_get_m(h, _pd(out)))
+    return out
+
+
+def _pf(a):
+    if a.dtype != np.float32 or not a.flags["C_CONTIGUOUS"]:
+        raise ValueError("expected a C-contiguous float32 array")
+    return a.ctypes.data_as(_PF)
+
+
+def grace_set_m_f32(h, m):
+    """m: C-contiguous float32 [3][nz][ny][nx] host array (pinned for full PCIe speed)."""
+    _check(load().grace_set_m_f32(h, _pf(m)))
+
+
+def grace_get_m_f32(h, out):
+    _check(load().grace_get_m_f32(h, _pf(out)))
     return out
 
 

@@ -892,6 +892,33 @@ int grace_get_m(grace_ctx* h, double* out) {
   return GRACE_OK;
 }
 
+int grace_set_m_f32(grace_ctx* h, const float* m) {
+  if (!h || !m) return fail(GRACE_EINVAL, "NULL argument");
+  // stage the fp32 input in the A buffer, normalise into the spare M buffer
+  const int target = 1 - h->cur;
+  for (auto& rk : h->ranks) {
+    float* stage = reinterpret_cast<float*>(rk.A);
+    const size_t off = slab_offset(h, rk);
+    for (int c = 0; c < 3; ++c)
+      CUDA_OR(cudaMemcpyAsync(stage + c * rk.Nl, m + c * h->N + off, sizeof(float) * rk.Nl, cudaMemcpyHostToDevice,
+                              h->stream));
+    CUDA_OR(launch_set_m_f32(stage, rk.M[target], rk.Nl, (float)h->Ms, rk.mask, rk.flag + 1, h->stream));
+  }
+  return finish_set_m(h, target);
+}
+
+int grace_get_m_f32(grace_ctx* h, float* out) {
+  if (!h || !out) return fail(GRACE_EINVAL, "NULL argument");
+  for (auto& rk : h->ranks) {
+    const size_t off = slab_offset(h, rk);
+    for (int c = 0; c < 3; ++c)
+      CUDA_OR(cudaMemcpyAsync(out + c * h->N + off, rk.M[h->cur] + c * rk.Nl, sizeof(float) * rk.Nl,
+                              cudaMemcpyDeviceToHost, h->stream));
+  }
+  CUDA_OR(cudaStreamSynchronize(h->stream));
+  return GRACE_OK;
+}
+
 int grace_get_m_device(grace_ctx* h, float* d_out) {
   if (!h || !d_out) return fail(GRACE_EINVAL, "NULL argument");
   for (auto& rk : h->ranks) {

@@ -424,3 +424,22 @@ def test_heun_steps_match_oracle(n, d):
     with pytest.raises(pb.GraceError):
         g.set_integrator(7)
     g.close()
+
+
+def test_host_fp32_set_get_m():
+    """grace_set_m_f32 / grace_get_m_f32 (12 B/cell each way) = the fp64 calls."""
+    n = (33, 17, 5)
+    M = random_m(n, 8e5, seed=81)
+    g = pb.Grace(n, (1e-9,) * 3, 8e5, 1.3e-11, 0.0, 0.5, GAMMA0)
+    g.set_m(M)
+    a = g.get_m()
+    pb.grace_set_m_f32(g.h, np.ascontiguousarray(M, dtype=np.float32))
+    b = np.empty((3,) + n[::-1], dtype=np.float32)
+    pb.grace_get_m_f32(g.h, b)
+    assert np.abs(a - b).max() <= 1e-7 * 8e5
+    M32 = np.ascontiguousarray(M, dtype=np.float32)
+    M32[:, 1, 2, 3] = 0.0
+    with pytest.raises(pb.GraceError) as e:
+        pb.grace_set_m_f32(g.h, M32)
+    assert e.value.code == pb.GRACE_EZEROCELL
+    g.close()
