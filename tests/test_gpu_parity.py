@@ -436,7 +436,7 @@ def test_host_fp32_set_get_m():
     pb.grace_set_m_f32(g.h, np.ascontiguousarray(M, dtype=np.float32))
     b = np.empty((3,) + n[::-1], dtype=np.float32)
     pb.grace_get_m_f32(g.h, b)
-    assert np.abs(a - b).max() <= 1e-7 * 8e5
+    assert np.abs(a - b).max() <= 4e-7 * 8e5  # fp32 vs fp64 normalisation: a few ulps
     M32 = np.ascontiguousarray(M, dtype=np.float32)
     M32[:, 1, 2, 3] = 0.0
     with pytest.raises(pb.GraceError) as e:
