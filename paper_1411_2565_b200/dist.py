@@ -50,6 +50,71 @@ def partition(nx, nz, rank, nranks):
     return Slab(rank, nranks, nzl, rank * nzl, kb, cols)
 
 
+def xrow_layout(nx, ny, nz, nranks):
+    """Sizes of the destination-blocked x-row layout [P][3][nz/P][ny][Kb] complex that
+    K1 writes and the C1 transpose sends (grace_api.cu alltoall): elements per
+    block (one destination rank) and per component sub-block."""
+    s = partition(nx, nz, 0, nranks)
+    kb = s.kx_block if nranks > 1 else s.kx_columns
+    sub = s.nz_local * ny * kb
+    return {"kb": kb, "nz_local": s.nz_local, "block": 3 * sub, "sub": sub}
+
+
+def comm_schedule(nx, ny, nz, nranks, pipelined=True):
+    """The exchanges of one distributed step in issue order, as libgrace enqueues
+    them: (name, stream, bytes sent by one rank).  C3 = the two
+    one-plane halos of M (own communicator and stream), C1 = z slabs -> kx blocks
+    after K1, C2 = back after K4; pipelined: per magnetisation component."""
+    if nranks == 1:
+        return []
+    lay = xrow_layout(nx, ny, nz, nranks)
+    plane = 3 * ny * nx * 4
+    out = [("C3 halo", "halo", 2 * plane)]
+    per = 8 * lay["sub"] * (nranks - 1)  # one component's sub-block to every other rank
+    comps = range(3) if pipelined else [None]
+    for name in ("C1", "C2"):
+        for q in comps:
+            out.append((name if q is None else f"{name}[{q}]", "comm", per * (1 if q is not None else 3)))
+    return out
+
+
+def step_time_model(kernel_ms, cells, nranks, link_GBps=700.0, pipelined=True):
+    """Per-step time of the z-slab partition of a grid of `cells` from a
+    single-GPU kernel split (kernel_ms: K1..K6 in ms, e.g. the bench line's
+    `kernels`) and an all-to-all bandwidth per GPU.  Compute scales as 1/P; one
+    transpose sends 24 (P-1)/P^2 bytes per cell from each rank.
+    A two-stream event simulation in the order libgrace enqueues the step:
+    without pipelining both transposes sit on the critical path; with it C1(q)
+    overlaps K1(q+1) and K2(q-1), and C2(q) overlaps K4(q+1) and K5(q-1).  The
+    halo exchange (own stream and communicator) is taken as hidden.
+    Returns (ms per step, ms of exposed communication)."""
+    P = nranks
+    k = {n: kernel_ms[n] / P for n in ("K1", "K2", "K3", "K4", "K5", "K6")}
+    busy = sum(k.values())
+    if P == 1:
+        return busy, 0.0
+    tr = 24.0 * cells * (P - 1) / (P * P) / (link_GBps * 1e6)  # ms per transpose
+    if not pipelined:
+        return busy + 2 * tr, 2 * tr
+    comp = comm = 0.0  # the step stream's and the communication stream's clocks
+    landed = [0.0] * 3
+    for q in range(3):  # K1(q) -> C1(q)
+        comp += k["K1"] / 3
+        comm = max(comm, comp) + tr / 3
+        landed[q] = comm
+    for q in range(3):  # K2(q) waits for C1(q)
+        comp = max(comp, landed[q]) + k["K2"] / 3
+    comp += k["K3"]
+    for q in range(3):  # K4(q) -> C2(q)
+        comp += k["K4"] / 3
+        comm = max(comm, comp) + tr / 3
+        landed[q] = comm
+    for q in range(3):  # K5(q) waits for C2(q)
+        comp = max(comp, landed[q]) + k["K5"] / 3
+    comp += k["K6"]
+    return comp, comp - busy
+
+
 def env_ranks():
     """(rank, world_size, local_rank) from the torchrun environment (1 process if absent)."""
     return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
