@@ -549,9 +549,6 @@ struct Z3Tma {
   static constexpr size_t KSB16 = (KSB + 15) / 16 * 16;
   static constexpr int TWF = Plan<L, false, 4>::TW_ELEMS, TWI = Plan<L, true, 4>::TW_ELEMS;
   static constexpr size_t TWB = (size_t)(TWF + TWI) * 8;  // per-pass twiddles, forward then inverse plan
-#ifndef GRACE_K3_PERSIST
-#define GRACE_K3_PERSIST 1  // persistent staged K3 (k3_z_pers) for two-pass fused pencils
-#endif
 #ifndef GRACE_K3_L2PF
 #define GRACE_K3_L2PF 0  // L2 prefetch distance of the TMA K3 in SMs' worth of CTAs (0: off; 2-8 measured slower: K3 1.00 -> 1.39 ms)
 #endif
@@ -658,138 +655,6 @@ __global__ void __launch_bounds__(Z3Tma<L>::NT, MINB)
       }
       mbar_wait(bar + 1, 1);
       pencil_conv<L, B, NT, true>(work, SmemLd<L, B, true>{work}, st, kss, Z::KZH, tws, 1, g.Py, ky, false, kw);
-    }
-  }
-}
-
-// Persistent K3 (fused two-pass plans, L = 32 / 64): each CTA walks (kx tile,
-// ky') items; every pencil set (ky, then Py - ky) is read by TMA into ONE staging
-// buffer, and the next set's load -- the mirror pencils, or the next item's ky
-// pencils -- is issued as soon as the forward first pass has consumed it, so it
-// lands while this set's remaining passes, multiply and inverse run.  The next
-// item's KS slice is issued right after the current item's last multiply.  Only
-// the CTA's very first load is exposed (k3_z_tma exposes one per item).
-template <int L, int MINB>
-__global__ void __launch_bounds__(Z3Tma<L>::NT, MINB)
-    k3_z_pers(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-              float2* __restrict__ X2, const float2* __restrict__ tw, Geom g) {
-  using Z = Z3Tma<L>;
-  constexpr int B = Z::B, NT = Z::NT, H = Z::H;
-  constexpr int NP = fft_npass(L);
-  static_assert(NP == 2 && ZPlan<L>::FUSE, "two-pass fused plans");
-  constexpr unsigned TXP = 3u * H * B * 8;
-  extern __shared__ __align__(128) unsigned char smraw[];
-  float2* work = reinterpret_cast<float2*>(smraw);
-  float2* stage = reinterpret_cast<float2*>(smraw + Z::WORK);
-  float* kss = reinterpret_cast<float*>(smraw + Z::WORK + Z::STAGE);
-  float2* tws = reinterpret_cast<float2*>(smraw + Z::WORK + Z::STAGE + Z::KSB16);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + Z::WORK + Z::STAGE + Z::KSB16 + Z::TWB);  // KS, stage
-  const int ntx = (g.Kc + B - 1) / B;
-  const int nitems = ntx * g.Kyh;
-  const size_t zstride = (size_t)g.Py * g.pitch2;
-  const size_t cstride = (size_t)g.nz * zstride;
-  auto nky_of = [&](int kyf) { return (kyf == 0 || 2 * kyf == g.Py) ? 1 : 2; };
-  auto issue_set = [&](int it, int rep) {  // pencils of item it, rep 0: ky', 1: Py - ky'
-    const int kyf = it / ntx, kx0 = (it - kyf * ntx) * B;
-    const int ky = rep == 0 ? kyf : g.Py - kyf;
-    mbar_expect_tx(bar + 1, TXP);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) tma_load_4d(stage + c * H * B, &xmap, bar + 1, kx0, ky, 0, c);
-  };
-  auto issue_ks = [&](int it) {
-    const int kyf = it / ntx, kx0 = (it - kyf * ntx) * B;
-    mbar_expect_tx(bar, (unsigned)Z::KSB);
-    tma_load_4d(kss, &kmap, bar, kx0, kyf, 0, 0);
-  };
-  pdl_trigger();
-  int it = blockIdx.x;
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
-    mbar_fence_init();
-    if (it < nitems) issue_ks(it);  // KS is constant: before the PDL wait
-  }
-  fill_pass_twiddles<Plan<L, false, 4>, L>(tws, tw, g.Lmax / L, threadIdx.x, NT);
-  fill_pass_twiddles<Plan<L, true, 4>, L>(tws + Z::TWF, tw, g.Lmax / L, threadIdx.x, NT);
-  __syncthreads();
-  pdl_wait();  // X2 comes from K2
-  if (threadIdx.x == 0 && it < nitems) issue_set(it, 0);
-  struct StageLd {
-    __device__ static constexpr bool kSmem() { return false; }
-    const float2* s;
-    __device__ float2 operator()(int b, int c, int ib, int Cc) const { return s[(c * H + ib + Cc) * B + b]; }
-  };
-  struct St {
-    __device__ static constexpr bool kSmem() { return false; }
-    float2* p;
-    size_t zs, cs;
-    int nz, nvalid;
-    __device__ void operator()(int b, int c, int ib, int Cc, float2 v) const {
-      const int i = ib + Cc;
-      if (i < nz && b < nvalid) p[c * cs + (b + i * zs)] = v;
-    }
-  };
-  struct None {
-    __device__ static constexpr bool kSmem() { return true; }
-    __device__ void operator()(int, int, int, int, float2) const {}
-  };
-  using PF = Pass<L, NP - 1, false, B, NT, true, 3>;
-  using PI = Pass<L, 0, true, B, NT, true, 3>;
-  static_assert(PF::R == PI::R && PF::UPT == 1 && PI::UPT == 1, "fused plan");
-  constexpr int IFACE0 = TileIdx<L, B, true, Plan<L, false, 4>::R(0)>::PAD ? kPad : kLin;
-  const ThreadMap<L, B, NT, true> tm;
-  const float2* twi = tws + Z::TWF;
-  unsigned ph_set = 0, ph_ks = 0;
-  for (; it < nitems; it += gridDim.x) {
-    const int kyf = it / ntx, kx0 = (it - kyf * ntx) * B;
-    const int nky = nky_of(kyf);
-    const int nvalid = g.Kc - kx0;
-    const int nxt = it + (int)gridDim.x;
-    for (int rep = 0; rep < nky; ++rep) {
-      const int ky = rep == 0 ? kyf : g.Py - kyf;
-          const St st{X2 + (size_t)ky * g.pitch2 + kx0, zstride, cstride, g.nz, nvalid};
-      mbar_wait(bar + 1, ph_set);
-      ph_set ^= 1;
-      // forward first pass: staged pencils -> work tile
-      fft_head<L, 0, NP - 1, false, B, NT, true, 3, false, true, true>(tm, work, StageLd{stage}, None{}, tws, 1);
-      __syncthreads();  // the stage buffer is consumed: load the next pencil set into it
-      if (threadIdx.x == 0) {
-        fence_proxy_async();
-        if (rep + 1 < nky) issue_set(it, rep + 1);
-        else if (nxt < nitems) issue_set(nxt, 0);
-      }
-      PF pf;
-      if (PF::active(tm)) {
-        pf.template load_smem<PF::R, IFACE0 == kPad>(tm, work);
-        pf.template compute<false, false, false, true>(tm, tws, 1);
-      }
-      if (rep == 0) {
-        mbar_wait(bar, ph_ks);
-        ph_ks ^= 1;
-      }
-      __syncthreads();
-      PI pi;
-#pragma unroll
-      for (int r = 0; r < PF::R; ++r) {
-        const int k = PF::sb(tm) + PF::C2(0, r);
-        const bool fz = k > (L >> 1);
-        const int kf = fz ? L - k : k;
-        const bool fy = ky > (g.Py >> 1);
-        float2 a = pf.v[0][0][r], b = pf.v[0][1][r], c = pf.v[0][2][r];
-        kmul_s(a, b, c, kss, Z::KZH, B, kf, tm.b, fy, fz);
-        pi.v[0][0][r] = a;
-        pi.v[0][1][r] = b;
-        pi.v[0][2][r] = c;
-      }
-      if (rep + 1 == nky) {  // the item's last multiply: the KS slice is free
-        __syncthreads();
-        if (threadIdx.x == 0 && nxt < nitems) {
-          fence_proxy_async();
-          issue_ks(nxt);
-        }
-      }
-      fft_from_regs<L, B, NT, true, 3, true, true, true, true>(tm, work, st, twi, 1, pi);
-      __syncthreads();  // the work tile is free
     }
   }
 }
@@ -1750,18 +1615,6 @@ static cudaError_t k3_launch(const Geom& g, float2* X2, const float* KS, const f
       CUtensorMap xm, km;
       memcpy(&xm, xmap->b, sizeof xm);
       memcpy(&km, kmap->b, sizeof km);
-      if constexpr (GRACE_K3_PERSIST && fft_npass(L) == 2 && Z::PRE) {
-        constexpr int MB = (L == 64 ? GRACE_MINB_Z3T64 : C::MINB);
-        auto kp = k3_z_pers<L, MB>;
-        cudaError_t e = prep(kp, Z::SMEM);
-        if (e != cudaSuccess) return e;
-        int per_sm = 0;
-        GRACE_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, Z::NT, Z::SMEM));
-        const int nitems = ((g.Kc + Z::B - 1) / Z::B) * g.Kyh;
-        const int cap = g.nsm * (per_sm > 0 ? per_sm : 1);
-        GRACE_TRY(launch_k(4, kp, nitems < cap ? nitems : cap, Z::NT, Z::SMEM, st, xm, km, X2, tw, g));
-        return cudaGetLastError();
-      }
       auto kern = k3_z_tma<L, (L == 64 ? GRACE_MINB_Z3T64 : C::MINB)>;
       cudaError_t e = prep(kern, Z::SMEM);
       if (e != cudaSuccess) return e;
