@@ -9,7 +9,8 @@
 //             halo exchanges are cudaMemcpyAsync between the ranks' buffers
 //             (exercises the partition logic against the single path).
 //   nccl    - this process's rank of P (one GPU per process); the exchanges are
-//             ncclAlltoAll and grouped ncclSend/ncclRecv over NVLink.
+//             grouped ncclSend/ncclRecv over NVLink (the all-to-all transposes,
+//             pipelined per component; the halos on a split communicator).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -813,7 +814,7 @@ int grace_create_dist(int nx, int ny, int nz, double dx, double dy, double dz, d
                       double alpha, double gamma, int rank, int nranks, const void* nccl_id, grace_ctx** out) {
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(GRACE_EINVAL, "bad rank %d of %d", rank, nranks);
   // One rank is the single-GPU context, unless GRACE_FORCE_NCCL is set: then the
-  // NCCL path runs with P = 1 (distributed layouts, ncclAllToAll / ncclAllReduce on
+  // NCCL path runs with P = 1 (distributed layouts, grouped send/recv / ncclAllReduce on
   // a one-rank communicator) -- how its host and device plumbing is exercised on a
   // one-GPU machine (tests/test_gpu_dist.py).
   if (nranks == 1 && !getenv("GRACE_FORCE_NCCL")) return grace_create(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma, out);

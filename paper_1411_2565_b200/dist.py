@@ -3,7 +3,8 @@
 One process per GPU, launched by torchrun.  torch.distributed is used only for
 the plumbing: reading RANK/WORLD_SIZE/LOCAL_RANK, broadcasting libgrace's NCCL
 unique id from rank 0, barriers and max-over-ranks timing.  The exchanges of
-the step itself (ncclAlltoAll transposes, halo send/recv) run inside libgrace.
+the step itself (all-to-all transposes as grouped ncclSend/ncclRecv, halo
+send/recv on a split communicator) run inside libgrace.
 
 ``partition`` restates the slab / kx-block arithmetic of libgrace's
 ``rank_geom`` (grace_api.cu) so the launcher can hand every rank its slab of a

@@ -129,8 +129,11 @@ def main(rnd, rep, launches, bench):
                          f"{bk.get('ms_per_launch', float('nan')):.3f} | {bk.get('share', float('nan')):.3f} |")
     lines += ["", f"Bench line: {b['ms_per_step']:.3f} ms/step, {b['value'] / 1e9:.2f} Gcell-updates/s, dominant kernel "
               f"{b['roofline']['kernel']} at {b['roofline']['achieved']:.0f} GB/s = {b['roofline']['frac']:.3f} of "
-              f"{b['roofline']['peak']} GB/s; step {b['roofline'].get('step_GBps_per_gpu', b['roofline'].get('step_GBps')):.0f} GB/s = "
-              f"{b['roofline']['step_frac']:.3f} of the measured HBM copy peak."]
+              f"{b['roofline']['peak']} GB/s; step fraction {b['roofline']['step_frac']:.3f} of the measured HBM copy "
+              f"peak on SURVEY 8(d)'s design bytes ({b['roofline'].get('step_bytes_design', 0) / 1e9:.2f} GB), "
+              f"{b['roofline'].get('step_frac_moved', float('nan')):.3f} on the bytes this build moves "
+              f"({b['roofline'].get('step_bytes_moved', 0) / 1e9:.2f} GB); e2e (C-ABI, host fp32 in/out) "
+              f"{(b.get('e2e') or {}).get('ms_per_step', float('nan')):.3f} ms/step."]
     open(os.path.join(PROF, f"{rnd}_ncu_summary.md"), "w").write("\n".join(lines) + "\n")
     text = open(launches).read().splitlines()
     start = next(i for i, ln in enumerate(text) if ln.startswith('"ID"'))

@@ -104,7 +104,7 @@ def test_virtual_ranks_heun_matches_single():
 
 
 def test_nccl_path_one_rank_matches_single(monkeypatch):
-    """The real NCCL path (dlopen'd libnccl, unique id, communicator, ncclAllToAll
+    """The real NCCL path (dlopen'd libnccl, unique id, communicator, grouped send/recv
     for both transposes, ncclAllReduce for <M> and the diagnostics, destination-
     blocked layouts) on a one-rank communicator (GRACE_FORCE_NCCL): same results
     as the single-GPU context.  Multi-rank NCCL runs need more GPUs than this
