@@ -699,26 +699,18 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
   cudaGetLastError();
   h->N = (mode == grace_ctx::kNccl) ? h->ranks[0].Nl : (long long)nx * ny * nz;
 
-  // setup: fp64 octant -> fp64 padded spectrum -> fp32 folded KS (S1..S5), once;
-  // each rank's table receives only its kx columns (no full-width copy).  The
-  // transient scratch is the fp64 octant (48 B/cell) plus one component's padded
-  // complex grid (16 B per padded point), for the whole grid on every rank.
-  const long long Ng = (long long)nx * ny * nz;
-  double* oct = nullptr;
-  double2* work = nullptr;
-  const size_t octb = sizeof(double) * 6 * (size_t)Ng;
-  const size_t workb = sizeof(double2) * (size_t)g0.Px * g0.Py * g0.Pz;
-  if (cudaMalloc(&oct, octb) != cudaSuccess || cudaMalloc(&work, workb) != cudaSuccess) {
-    cudaGetLastError();
-    if (oct) cudaFree(oct);
-    if (work) cudaFree(work);
-    return bail(fail(GRACE_ENOMEM, "setup needs %zu bytes of fp64 scratch", octb + workb));
-  }
+  // setup: fp64 octant -> fp64 padded spectrum -> fp32 folded KS (S1..S5), once,
+  // one tensor component at a time; each rank's table receives only its kx
+  // columns and only those columns are carried through the y and z transforms.
   std::vector<KsOut> kso;
   for (auto& rk : h->ranks)
     if (rk.g.Kc > 0 || !dlay) kso.push_back(KsOut{rk.KS, dlay ? rk.r * rk.g.kb : 0, rk.g.Kc, rk.g.KSp});
-  cudaError_t e = tensor_octant_device(nx, ny, nz, dx, dy, dz, oct, s);
-  if (e == cudaSuccess) e = kernel_spectrum_device(g0, oct, work, (int)kso.size(), kso.data(), s);
+  size_t scratch = 0;
+  cudaError_t e = kernel_spectrum_device(g0, dx, dy, dz, (int)kso.size(), kso.data(), &scratch, s);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return bail(fail(GRACE_ENOMEM, "tensor setup needs %zu bytes of fp64 scratch", scratch));
+  }
   if (e == cudaSuccess) e = launch_twiddles(h->tw, g0.Lmax, s);
   for (auto& rk : h->ranks) {
     if (e == cudaSuccess) e = launch_fill_uniform_x(rk.M[0], rk.Nl, (float)Ms, s);
@@ -726,8 +718,6 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
   }
   if (e == cudaSuccess) e = h->upload_params(1e-15);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  cudaFree(oct);
-  cudaFree(work);
   if (e != cudaSuccess) return bail(fail(GRACE_ECUDA, "tensor setup: %s", cudaGetErrorString(e)));
   // Dry run of one step (M[0] -> M[1], the spare buffer) so every kernel's
   // shared-memory attribute is set before any graph capture; then restore the

@@ -128,14 +128,16 @@ cudaError_t launch_widen(const float* src, double* dst, long long n, cudaStream_
 // Real-space octant [6][nz][ny][nx] into device memory `oct` (bit-exact with the oracle).
 cudaError_t tensor_octant_device(int nx, int ny, int nz, double dx, double dy, double dz, double* oct,
                                  cudaStream_t st);
-// Spectral table KS [6][Kzh][Kyh][KSp] fp32 = -Re(FFT(circulant N))/(Px Py Pz), from the octant,
-// written for each output's kx columns [kx0, kx0 + ncol) (a rank's kx block; the
-// single-GPU table is kx0 = 0, ncol = Kx).  `work` must hold Px*Py*Pz double2.
+// Spectral table KS [6][Kzh][Kyh][KSp] fp32 = -Re(FFT(circulant N))/(Px Py Pz), written for
+// each output's kx columns [kx0, kx0 + ncol) (a rank's kx block; the single-GPU table is
+// kx0 = 0, ncol = Kx).  Lean: one octant component at a time (8 B/cell), the x lines
+// in chunks of padded z planes, and only the union of the requested kx columns kept
+// for the y and z lines; the transient device memory is reported in *scratch_bytes.
 struct KsOut {
   float* KS;
   int kx0, ncol, KSp;
 };
-cudaError_t kernel_spectrum_device(const Geom& g, const double* oct, double2* work, int nout, const KsOut* out,
-                                   cudaStream_t st);
+cudaError_t kernel_spectrum_device(const Geom& g, double dx, double dy, double dz, int nout, const KsOut* out,
+                                   size_t* scratch_bytes, cudaStream_t st);
 
 }  // namespace grace

@@ -19,6 +19,7 @@
 //   S5  k_fold     : KS = -Re / (Px Py Pz) on the folded octant, rounded to fp32
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 
@@ -192,13 +193,14 @@ __global__ void k_nodes(double* lat, int LI, int LJ, int LK, double dx, double d
 __device__ __forceinline__ double sgn(int v) { return (double)((v > 0) - (v < 0)); }
 
 // S2: one octant entry per thread.
+// Components c0 .. c0 + nc - 1 into oct[(c - c0) * N + ...].
 __global__ void k_octant(double* oct, const double* lat, int LI, int LJ, int LK, int nx, int ny, int nz, double dx,
-                         double dy, double dz) {
+                         double dy, double dz, int c0, int nc) {
   const long long N = (long long)nx * ny * nz;
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= 6 * N) return;
-  const int c = (int)(idx / N);
-  long long r = idx - c * N;
+  if (idx >= nc * N) return;
+  const int c = c0 + (int)(idx / N);
+  long long r = idx - (c - c0) * N;
   const int k = (int)(r / ((long long)nx * ny));
   r -= (long long)k * nx * ny;
   const int j = (int)(r / nx);
@@ -260,13 +262,15 @@ __device__ __forceinline__ int circ_index(int p, int P, int n, int& s) {
   }
   return -1;
 }
-__global__ void k_embed(double2* A, const double* oct_c, int c, int nx, int ny, int nz, int Px, int Py, int Pz) {
-  const long long tot = (long long)Px * Py * Pz;
+// Padded planes pz0 .. pz0 + npz - 1 into A [npz][Py][Px].
+__global__ void k_embed(double2* A, const double* oct_c, int c, int nx, int ny, int nz, int Px, int Py, int Pz,
+                        int pz0, int npz) {
+  const long long tot = (long long)Px * Py * npz;
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= tot) return;
   const int px = (int)(idx % Px);
   const int py = (int)((idx / Px) % Py);
-  const int pz = (int)(idx / ((long long)Px * Py));
+  const int pz = pz0 + (int)(idx / ((long long)Px * Py));
   int sx, sy, sz;
   const int ix = circ_index(px, Px, nx, sx), iy = circ_index(py, Py, ny, sy), iz = circ_index(pz, Pz, nz, sz);
   double v = 0.0;
@@ -314,8 +318,9 @@ __global__ void k_fft64(double2* A, int L, int logL, long long nlines, long long
 
 // S5: KS[c][kz'][ky'][kx - kx0] = -Re A[kz'][ky'][kx] / (Px Py Pz), rounded to fp32,
 // for the columns kx0 .. kx0 + ncol - 1 (one rank's kx block; pitch KSp, the
-// padding columns zero).
-__global__ void k_fold(float* KSc, const double2* A, Geom g, int kx0, int ncol, int KSp) {
+// padding columns zero).  A is the compact spectrum [Pz][Py][Kw] of the columns
+// kxlo .. kxlo + Kw - 1.
+__global__ void k_fold(float* KSc, const double2* A, Geom g, int kx0, int ncol, int KSp, int kxlo, int Kw) {
   const long long tot = (long long)g.Kzh * g.Kyh * KSp;
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= tot) return;
@@ -326,17 +331,28 @@ __global__ void k_fold(float* KSc, const double2* A, Geom g, int kx0, int ncol, 
   float v = 0.f;
   if (col < ncol && kx < g.Kx) {
     const double P = (double)g.Px * (double)g.Py * (double)g.Pz;
-    v = (float)(-A[((long long)kz * g.Py + ky) * g.Px + kx].x / P);
+    v = (float)(-A[((long long)kz * g.Py + ky) * Kw + (kx - kxlo)].x / P);
   }
   KSc[idx] = v;
+}
+
+// Columns kxlo .. kxlo + Kw - 1 of the x-transformed chunk [npz][Py][Px] -> compact [Pz][Py][Kw].
+__global__ void k_gather_cols(double2* dst, const double2* chunk, int Px, int Py, int pz0, int npz, int kxlo, int Kw) {
+  const long long tot = (long long)npz * Py * Kw;
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= tot) return;
+  const int kw = (int)(idx % Kw);
+  const long long row = idx / Kw;  // (pz - pz0) * Py + py
+  dst[((long long)pz0 * Py + row) * Kw + kw] = chunk[row * Px + kxlo + kw];
 }
 
 inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
 
 }  // namespace
 
-cudaError_t tensor_octant_device(int nx, int ny, int nz, double dx, double dy, double dz, double* oct,
-                                 cudaStream_t st) {
+// Node lattice of f/g values covering every near-field stencil node (S1).
+static cudaError_t node_lattice(int nx, int ny, int nz, double dx, double dy, double dz, double** lat, int* L3,
+                                cudaStream_t st) {
   // node box: near offsets satisfy |i| dx <= 30 diag, so |i| <= 30 diag/dx; +2 margin, capped by the grid.
   const double diag = std::sqrt((dx * dx + dy * dy) + dz * dz);
   auto ext = [&](int n, double d) {
@@ -344,19 +360,27 @@ cudaError_t tensor_octant_device(int nx, int ny, int nz, double dx, double dy, d
     const long long e = (lim > (double)n) ? (long long)n : (long long)lim;
     return (int)(e + 2);  // nodes 0 .. e+1
   };
-  const int LI = ext(nx, dx), LJ = ext(ny, dy), LK = ext(nz, dz);
-  double* lat = nullptr;
-  cudaError_t e = cudaMallocAsync(&lat, sizeof(double) * 6 * (size_t)LI * LJ * LK, st);
+  L3[0] = ext(nx, dx);
+  L3[1] = ext(ny, dy);
+  L3[2] = ext(nz, dz);
+  const long long nn = 6LL * L3[0] * L3[1] * L3[2];
+  cudaError_t e = cudaMallocAsync(lat, sizeof(double) * nn, st);
   if (e != cudaSuccess) return e;
-  const long long nn = 6LL * LI * LJ * LK;
-  k_nodes<<<(unsigned)cdiv(nn, 128), 128, 0, st>>>(lat, LI, LJ, LK, dx, dy, dz);
-  e = cudaGetLastError();
+  k_nodes<<<(unsigned)cdiv(nn, 128), 128, 0, st>>>(*lat, L3[0], L3[1], L3[2], dx, dy, dz);
+  return cudaGetLastError();
+}
+
+cudaError_t tensor_octant_device(int nx, int ny, int nz, double dx, double dy, double dz, double* oct,
+                                 cudaStream_t st) {
+  double* lat = nullptr;
+  int L3[3];
+  cudaError_t e = node_lattice(nx, ny, nz, dx, dy, dz, &lat, L3, st);
   if (e == cudaSuccess) {
     const long long no = 6LL * nx * ny * nz;
-    k_octant<<<(unsigned)cdiv(no, 256), 256, 0, st>>>(oct, lat, LI, LJ, LK, nx, ny, nz, dx, dy, dz);
+    k_octant<<<(unsigned)cdiv(no, 256), 256, 0, st>>>(oct, lat, L3[0], L3[1], L3[2], nx, ny, nz, dx, dy, dz, 0, 6);
     e = cudaGetLastError();
   }
-  cudaFreeAsync(lat, st);
+  if (lat) cudaFreeAsync(lat, st);
   return e;
 }
 
@@ -375,29 +399,65 @@ static cudaError_t fft64_axis(double2* A, int L, long long nlines, long long inn
   return cudaGetLastError();
 }
 
-cudaError_t kernel_spectrum_device(const Geom& g, const double* oct, double2* work, int nout, const KsOut* out,
-                                   cudaStream_t st) {
-  const long long tot = (long long)g.Px * g.Py * g.Pz;
+cudaError_t kernel_spectrum_device(const Geom& g, double dx, double dy, double dz, int nout, const KsOut* out,
+                                   size_t* scratch_bytes, cudaStream_t st) {
   const long long N = (long long)g.nx * g.ny * g.nz;
-  for (int c = 0; c < 6; ++c) {
-    k_embed<<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(work, oct + c * N, c, g.nx, g.ny, g.nz, g.Px, g.Py, g.Pz);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    // x lines: all (pz, py); y and z lines only for kx <= Px/2 (the half spectrum kept).
-    const long long kx = g.Px / 2 + 1 < g.Px ? g.Px / 2 + 1 : g.Px;
-    if ((e = fft64_axis(work, g.Px, (long long)g.Py * g.Pz, 1, g.Px, 1, st)) != cudaSuccess) return e;
-    if ((e = fft64_axis(work, g.Py, (long long)g.Pz * kx, kx, (long long)g.Py * g.Px, g.Px, st)) != cudaSuccess)
-      return e;
-    if ((e = fft64_axis(work, g.Pz, (long long)g.Py * kx, kx, g.Px, (long long)g.Px * g.Py, st)) != cudaSuccess)
-      return e;
-    for (int o = 0; o < nout; ++o) {
+  // the union of the requested kx columns: only these survive the x transform
+  int kxlo = g.Kx, kxhi = 0;
+  for (int o = 0; o < nout; ++o)
+    if (out[o].ncol > 0) {
+      kxlo = std::min(kxlo, out[o].kx0);
+      kxhi = std::max(kxhi, std::min(g.Kx, out[o].kx0 + out[o].ncol));
+    }
+  if (kxhi <= kxlo) return cudaSuccess;
+  const int Kw = kxhi - kxlo;
+  const long long plane = (long long)g.Px * g.Py;
+  // x transforms in chunks of padded z planes, at most the compact spectrum's size
+  int zc = (int)std::max<long long>(1, std::min<long long>(g.Pz, ((long long)g.Py * Kw * g.Pz) / plane));
+  const size_t need = sizeof(double) * N + sizeof(double2) * (size_t)plane * zc +
+                      sizeof(double2) * (size_t)g.Pz * g.Py * Kw;
+  if (scratch_bytes) *scratch_bytes = need;
+  double* lat = nullptr;
+  double* oct = nullptr;
+  double2* chunk = nullptr;
+  double2* A = nullptr;
+  int L3[3];
+  cudaError_t e = node_lattice(g.nx, g.ny, g.nz, dx, dy, dz, &lat, L3, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&oct, sizeof(double) * N, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&chunk, sizeof(double2) * (size_t)plane * zc, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&A, sizeof(double2) * (size_t)g.Pz * g.Py * Kw, st);
+  for (int c = 0; c < 6 && e == cudaSuccess; ++c) {
+    // S2 (component c), S3 + x lines per z chunk, kept columns -> compact A
+    k_octant<<<(unsigned)cdiv(N, 256), 256, 0, st>>>(oct, lat, L3[0], L3[1], L3[2], g.nx, g.ny, g.nz, dx, dy, dz, c,
+                                                     1);
+    e = cudaGetLastError();
+    for (int z0 = 0; z0 < g.Pz && e == cudaSuccess; z0 += zc) {
+      const int nz = std::min(zc, g.Pz - z0);
+      k_embed<<<(unsigned)cdiv(plane * nz, 256), 256, 0, st>>>(chunk, oct, c, g.nx, g.ny, g.nz, g.Px, g.Py, g.Pz, z0,
+                                                                nz);
+      e = cudaGetLastError();
+      if (e == cudaSuccess) e = fft64_axis(chunk, g.Px, (long long)g.Py * nz, 1, g.Px, 1, st);
+      if (e == cudaSuccess) {
+        k_gather_cols<<<(unsigned)cdiv((long long)nz * g.Py * Kw, 256), 256, 0, st>>>(A, chunk, g.Px, g.Py, z0, nz,
+                                                                                      kxlo, Kw);
+        e = cudaGetLastError();
+      }
+    }
+    // S4: y and z lines of the kept columns (the same line transforms as on the full array)
+    if (e == cudaSuccess) e = fft64_axis(A, g.Py, (long long)g.Pz * Kw, Kw, (long long)g.Py * Kw, Kw, st);
+    if (e == cudaSuccess) e = fft64_axis(A, g.Pz, (long long)g.Py * Kw, (long long)g.Py * Kw, 0, (long long)g.Py * Kw, st);
+    for (int o = 0; o < nout && e == cudaSuccess; ++o) {
       const long long kslen = (long long)g.Kzh * g.Kyh * out[o].KSp;
-      k_fold<<<(unsigned)cdiv(kslen, 256), 256, 0, st>>>(out[o].KS + c * kslen, work, g, out[o].kx0, out[o].ncol,
-                                                         out[o].KSp);
-      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      k_fold<<<(unsigned)cdiv(kslen, 256), 256, 0, st>>>(out[o].KS + c * kslen, A, g, out[o].kx0, out[o].ncol,
+                                                         out[o].KSp, kxlo, Kw);
+      e = cudaGetLastError();
     }
   }
-  return cudaSuccess;
+  if (A) cudaFreeAsync(A, st);
+  if (chunk) cudaFreeAsync(chunk, st);
+  if (oct) cudaFreeAsync(oct, st);
+  if (lat) cudaFreeAsync(lat, st);
+  return e;
 }
 
 }  // namespace grace
