@@ -248,6 +248,10 @@ struct YTma {
 #ifndef GRACE_YT_NB_INV
 #define GRACE_YT_NB_INV 1  // K4 tile buffers per CTA (1: two single-buffered CTAs per SM, 0.596 -> 0.585 ms; 2: double-buffered)
 #endif
+#ifndef GRACE_YT_EARLY
+#define GRACE_YT_EARLY 1  // single-buffered y tiles: issue the next load before the last pass
+#endif
+constexpr bool YT_EARLY = GRACE_YT_EARLY;
 template <int L, int NCOL, bool INV, int NB = 2>
 __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? 2 : GRACE_YT_MINB)
     k_y_tma(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, const float2* __restrict__ tw, Geom g,
@@ -329,7 +333,7 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? 2 : GRACE_YT_MINB
       }
       mbar_wait(bar + (k & 1), (k >> 1) & 1);
     } else {
-      if (threadIdx.x == 0) {
+      if (threadIdx.x == 0 && (k == 0 || !YT_EARLY)) {
         fence_proxy_async();
         issue(t, cur, bar);
 #if GRACE_YT_L2PF
@@ -344,6 +348,35 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? 2 : GRACE_YT_MINB
     const int kx0 = xt * NCOL;
     float2* o = out + (INV ? xrow_slab(g, slab) : (size_t)slab * g.Py * g.pitch2) + kx0;
     const int pitch = INV ? g.pitch1 : g.pitch2;
+    if constexpr (NB == 1 && YT_EARLY) {
+      // single buffer: the passes before the last run in place; once every thread
+      // holds its last-pass inputs in registers the buffer is free, so the next
+      // tile's TMA load is issued before the last pass computes and stores
+      constexpr int NP = fft_npass(L, 4);
+      constexpr int IFACE0 = TileIdx<L, NCOL, true, Plan<L, false, 4>::R(0)>::PAD ? kPad : kLin;
+      struct None {
+        __device__ static constexpr bool kSmem() { return true; }
+        __device__ void operator()(int, int, int, int, float2) const {}
+      };
+      const ThreadMap<L, NCOL, NT, true> tm;
+      fft_head<L, 0, NP - 1, false, NCOL, NT, true, 1, INV, !INV, true>(tm, cur, SmemLd<L, NCOL, true>{cur}, None{},
+                                                                       tws, 1);
+      __syncthreads();
+      using PS = Pass<L, NP - 1, false, NCOL, NT, true, 1>;
+      PS ps;
+      if (PS::active(tm)) ps.template load_smem<PS::R, NP == 2 && IFACE0 == kPad>(tm, cur);
+      __syncthreads();
+      if (threadIdx.x == 0 && t + (int)gridDim.x < ntiles) {
+        fence_proxy_async();
+        issue(t + gridDim.x, cur, bar);
+      }
+      if (PS::active(tm)) {
+        ps.template compute<INV, false, INV, true>(tm, tws, 1);
+        if (g.Kc - kx0 >= NCOL && n_out >= (INV ? L / 2 : L)) ps.template store_ext<INV ? PS::R / 2 : PS::R>(tm, StFull{o, pitch});
+        else ps.template store_ext<INV ? PS::R / 2 : PS::R>(tm, St{o, pitch, n_out, g.Kc - kx0});
+      }
+      continue;
+    }
     if (g.Kc - kx0 >= NCOL && n_out >= (INV ? L / 2 : L))
       fft_tile<L, NCOL, NT, true, INV, !INV, INV, 1, false, true>(cur, SmemLd<L, NCOL, true>{cur}, StFull{o, pitch},
                                                                    tws, 1);
@@ -366,13 +399,19 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? 2 : GRACE_YT_MINB
 #ifndef GRACE_YSTAGE_MINB
 #define GRACE_YSTAGE_MINB 1
 #endif
+#ifndef GRACE_YSTAGE_TWS
+#define GRACE_YSTAGE_TWS 1  // per-pass twiddle tables in smem when they fit beside the tiles
+#endif
 template <int L>
 struct YStage {
   static constexpr int NCOL = (L == 2048 && GRACE_YSTAGE_2048) ? GRACE_YSTAGE_2048 : 4;
   using T = TileIdx<L, NCOL, true>;
+  using PL = Plan<L, false, 4>;
   static constexpr int WB = ((T::ELEMS * 8 + 1023) / 1024) * 1024;  // work tile bytes
   static constexpr int SB = NCOL * (L / 2) * 8;                       // staging bytes
-  static constexpr size_t SMEM = (size_t)WB + SB + 64;
+  static constexpr int TWB = PL::TW_ELEMS * 8;                        // per-pass twiddle tables
+  static constexpr bool TWS = GRACE_YSTAGE_TWS && (size_t)WB + SB + TWB + 64 <= 232448;
+  static constexpr size_t SMEM = (size_t)WB + SB + (TWS ? TWB : 0) + 64;
   static constexpr int NT = NCOL * (L / 16);
   static constexpr int BR = 256;
 };
@@ -387,8 +426,12 @@ __global__ void __launch_bounds__(YStage<L>::NT, (L == 2048 ? GRACE_YSTAGE_MINB 
   extern __shared__ __align__(1024) unsigned char smraw[];
   float2* work = reinterpret_cast<float2*>(smraw);
   float2* stage = reinterpret_cast<float2*>(smraw + Y::WB);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + Y::WB + Y::SB);
+  float2* tws = reinterpret_cast<float2*>(smraw + Y::WB + Y::SB);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + Y::WB + Y::SB + (Y::TWS ? Y::TWB : 0));
   pdl_trigger();
+  if constexpr (Y::TWS) fill_pass_twiddles<typename Y::PL, L>(tws, tw, g.Lmax / L, threadIdx.x, NT);
+  const float2* twp = Y::TWS ? tws : tw;  // the passes' twiddle source
+  const int tws_stride = Y::TWS ? 1 : g.Lmax / L;
   const int ntx = (g.Kc + NCOL - 1) / NCOL;
   const int ntiles = ntx * g.nc * g.nz;  // components c0 .. c0 + nc - 1
   const int slab0 = g.c0 * g.nz;
@@ -430,15 +473,15 @@ __global__ void __launch_bounds__(YStage<L>::NT, (L == 2048 ? GRACE_YSTAGE_MINB 
     const int kx0 = xt * NCOL;
     const St st{out + (size_t)slab * g.Py * g.pitch2 + kx0, g.pitch2, g.Kc - kx0};
     // pass 0: staged rows (< L/2, the rest is the zero padding) -> work tile
-    fft_pass<L, 0, false, NCOL, NT, true, 1, false, true, false, kExt, IFACE0>(tm, StageLd{stage}, st, work, tw,
-                                                                              g.Lmax / L);
+    fft_pass<L, 0, false, NCOL, NT, true, 1, false, true, false, kExt, IFACE0, Y::TWS>(tm, StageLd{stage}, st, work,
+                                                                                       twp, tws_stride);
     __syncthreads();  // the staging buffer is free
     if (threadIdx.x == 0 && t + (int)gridDim.x < ntiles) {
       fence_proxy_async();
       issue(t + gridDim.x);
     }
-    fft_passes<L, 1, false, NCOL, NT, true, 1, false, true, false, kExt, kExt>(tm, work, StageLd{stage}, st, tw,
-                                                                                g.Lmax / L);
+    fft_passes<L, 1, false, NCOL, NT, true, 1, false, true, false, kExt, kExt, Y::TWS>(tm, work, StageLd{stage}, st,
+                                                                                         twp, tws_stride);
     __syncthreads();
   }
   (void)n_out;
