@@ -68,11 +68,24 @@ struct ZPlan {
   static constexpr int NT = B * TPC < 32 ? 32 : B * TPC;
 };
 
+template <int L>
+__host__ __device__ constexpr int pencil_tw_elems() {
+  return ZPlan<L>::FUSE ? Plan<L, false, 4>::TW_ELEMS + Plan<L, true, 4>::TW_ELEMS : Plan<L, false, 4>::TW_ELEMS;
+}
+// Fill the shared table pencil_conv<..., TWS = true> reads (threads [tid, nt)).
+template <int L>
+__device__ __forceinline__ void fill_pencil_twiddles(float2* dst, const float2* __restrict__ tw, int twstride, int tid,
+                                                     int nt) {
+  fill_pass_twiddles<Plan<L, false, 4>, L>(dst, tw, twstride, tid, nt);
+  if constexpr (ZPlan<L>::FUSE) fill_pass_twiddles<Plan<L, true, 4>, L>(dst + Plan<L, false, 4>::TW_ELEMS, tw, twstride, tid, nt);
+}
+
 // kw(): called before the multiply's barrier -- waits for this thread's part of
 // the KS slice (cp.async group or TMA mbarrier).
-// TWS (fused plans only): tw is a shared table holding the forward plan's per-pass
-// twiddles followed by the reversed (inverse) plan's (fill_pass_twiddles of
-// Plan<L, false> then Plan<L, true>); else tw is the global table.
+// TWS: tw is a shared table of per-pass twiddles (fill_pass_twiddles): for fused
+// plans the forward plan's followed by the reversed (inverse) plan's (Plan<L, false>
+// then Plan<L, true>), for unfused ones the forward plan's alone (both directions
+// run it); else tw is the global table.  pencil_tw_elems<L>() sizes it.
 template <int L, int B, int NT, bool TWS = false, class LD, class ST, class KW>
 __device__ __forceinline__ void pencil_conv(float2* smem, const LD& ld, const ST& st, const float* kss, int KH,
                                             const float2* __restrict__ tw, int twstride, int P_other, int k_other,
@@ -92,7 +105,6 @@ __device__ __forceinline__ void pencil_conv(float2* smem, const LD& ld, const ST
     }
   };
   const ThreadMap<L, B, NT, true> tm;
-  static_assert(!TWS || ZPlan<L>::FUSE, "shared twiddle tables: fused plans only");
   if constexpr (ZPlan<L>::FUSE) {
     using PF = Pass<L, fft_npass(L) - 1, false, B, NT, true, 3>;
     using PI = Pass<L, 0, true, B, NT, true, 3>;
@@ -118,7 +130,7 @@ __device__ __forceinline__ void pencil_conv(float2* smem, const LD& ld, const ST
     fft_from_regs<L, B, NT, true, 3, true, true, true, TWS>(tm, smem, st, twi, twstride, pi);
   } else {
     using T = TileIdx<L, B, true>;
-    fft_tile<L, B, NT, true, false, (L > 1), false, 3>(smem, ld, SmemSt<L, B, true>{smem}, tw, twstride);
+    fft_tile<L, B, NT, true, false, (L > 1), false, 3, false, TWS>(smem, ld, SmemSt<L, B, true>{smem}, tw, twstride);
     kw();
     __syncthreads();
     for (int u = threadIdx.x; u < L * B; u += NT) {
@@ -134,7 +146,7 @@ __device__ __forceinline__ void pencil_conv(float2* smem, const LD& ld, const ST
       s0[2 * T::ELEMS] = c;
     }
     __syncthreads();
-    fft_tile<L, B, NT, true, true, false, (L > 1), 3>(smem, SmemLd<L, B, true>{smem}, st, tw, twstride);
+    fft_tile<L, B, NT, true, true, false, (L > 1), 3, false, TWS>(smem, SmemLd<L, B, true>{smem}, st, tw, twstride);
   }
 }
 

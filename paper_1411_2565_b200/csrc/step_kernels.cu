@@ -248,10 +248,6 @@ struct YTma {
 #ifndef GRACE_YT_NB_INV
 #define GRACE_YT_NB_INV 1  // K4 tile buffers per CTA (1: two single-buffered CTAs per SM, 0.596 -> 0.585 ms; 2: double-buffered)
 #endif
-#ifndef GRACE_YT_EARLY
-#define GRACE_YT_EARLY 1  // single-buffered y tiles: issue the next load before the last pass
-#endif
-constexpr bool YT_EARLY = GRACE_YT_EARLY;
 template <int L, int NCOL, bool INV, int NB = 2>
 __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? 2 : GRACE_YT_MINB)
     k_y_tma(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, const float2* __restrict__ tw, Geom g,
@@ -333,7 +329,7 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? 2 : GRACE_YT_MINB
       }
       mbar_wait(bar + (k & 1), (k >> 1) & 1);
     } else {
-      if (threadIdx.x == 0 && (k == 0 || !YT_EARLY)) {
+      if (threadIdx.x == 0) {
         fence_proxy_async();
         issue(t, cur, bar);
 #if GRACE_YT_L2PF
@@ -348,35 +344,6 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? 2 : GRACE_YT_MINB
     const int kx0 = xt * NCOL;
     float2* o = out + (INV ? xrow_slab(g, slab) : (size_t)slab * g.Py * g.pitch2) + kx0;
     const int pitch = INV ? g.pitch1 : g.pitch2;
-    if constexpr (NB == 1 && YT_EARLY) {
-      // single buffer: the passes before the last run in place; once every thread
-      // holds its last-pass inputs in registers the buffer is free, so the next
-      // tile's TMA load is issued before the last pass computes and stores
-      constexpr int NP = fft_npass(L, 4);
-      constexpr int IFACE0 = TileIdx<L, NCOL, true, Plan<L, false, 4>::R(0)>::PAD ? kPad : kLin;
-      struct None {
-        __device__ static constexpr bool kSmem() { return true; }
-        __device__ void operator()(int, int, int, int, float2) const {}
-      };
-      const ThreadMap<L, NCOL, NT, true> tm;
-      fft_head<L, 0, NP - 1, false, NCOL, NT, true, 1, INV, !INV, true>(tm, cur, SmemLd<L, NCOL, true>{cur}, None{},
-                                                                       tws, 1);
-      __syncthreads();
-      using PS = Pass<L, NP - 1, false, NCOL, NT, true, 1>;
-      PS ps;
-      if (PS::active(tm)) ps.template load_smem<PS::R, NP == 2 && IFACE0 == kPad>(tm, cur);
-      __syncthreads();
-      if (threadIdx.x == 0 && t + (int)gridDim.x < ntiles) {
-        fence_proxy_async();
-        issue(t + gridDim.x, cur, bar);
-      }
-      if (PS::active(tm)) {
-        ps.template compute<INV, false, INV, true>(tm, tws, 1);
-        if (g.Kc - kx0 >= NCOL && n_out >= (INV ? L / 2 : L)) ps.template store_ext<INV ? PS::R / 2 : PS::R>(tm, StFull{o, pitch});
-        else ps.template store_ext<INV ? PS::R / 2 : PS::R>(tm, St{o, pitch, n_out, g.Kc - kx0});
-      }
-      continue;
-    }
     if (g.Kc - kx0 >= NCOL && n_out >= (INV ? L / 2 : L))
       fft_tile<L, NCOL, NT, true, INV, !INV, INV, 1, false, true>(cur, SmemLd<L, NCOL, true>{cur}, StFull{o, pitch},
                                                                    tws, 1);
@@ -514,6 +481,11 @@ __device__ __forceinline__ void stage_ks(float* kss, const float* __restrict__ b
   }
 }
 
+#ifndef GRACE_PENCIL_TWS
+#define GRACE_PENCIL_TWS 1  // K3 (LDG) and K2': per-pass twiddle tables in shared memory
+#endif
+constexpr bool PENCIL_TWS = GRACE_PENCIL_TWS;
+
 // K3: z pencils of the three components for one ky' (and its mirror Py - ky'):
 // forward z-FFT (nz of L nonzero), H~ = KS . M~, inverse z-FFT, keep z < nz.
 // Processing ky and Py-ky in one CTA reads each folded KS slice once; the slice
@@ -530,9 +502,14 @@ __global__ void __launch_bounds__(NT, MINB) k3_z(float2* __restrict__ X2, const 
   const int nvalid = g.Kc - kx0;
   const int nky = (kyf == 0 || 2 * kyf == g.Py) ? 1 : 2;
   float* kss = reinterpret_cast<float*>(smem + 3 * TileIdx<L, B, true>::ELEMS);
+  float2* tws = reinterpret_cast<float2*>(kss + 6 * KZH * B);  // per-pass twiddles (GRACE_PENCIL_TWS)
   pdl_trigger();
   stage_ks<B, NT>(kss, KS + (size_t)kyf * g.KSp + kx0, (size_t)g.Kzh * g.Kyh * g.KSp, (size_t)g.Kyh * g.KSp, KZH,
                   g.KSp - kx0);
+  if constexpr (PENCIL_TWS) {
+    fill_pencil_twiddles<L>(tws, tw, g.Lmax / L, threadIdx.x, NT);
+    __syncthreads();
+  }
   pdl_wait();  // the KS slice is constant; X2 comes from K2
   for (int rep = 0; rep < nky; ++rep) {
     const int ky = rep == 0 ? kyf : g.Py - kyf;
@@ -560,9 +537,10 @@ __global__ void __launch_bounds__(NT, MINB) k3_z(float2* __restrict__ X2, const 
       }
     } st{base, zstride, cstride, g.nz, nvalid};
     if (rep) __syncthreads();
-    pencil_conv<L, B, NT>(smem, ld, st, kss, KZH, tw, g.Lmax / L, g.Py, ky, false, [&] {
-      if (rep == 0) cp_async_wait_all();
-    });
+    pencil_conv<L, B, NT, PENCIL_TWS>(smem, ld, st, kss, KZH, PENCIL_TWS ? tws : tw, PENCIL_TWS ? 1 : g.Lmax / L,
+                                      g.Py, ky, false, [&] {
+                                        if (rep == 0) cp_async_wait_all();
+                                      });
   }
 }
 
@@ -738,7 +716,6 @@ template <int L, int B, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k2f_y_fused(float2* __restrict__ X1, const float* __restrict__ KS,
                                                         const float2* __restrict__ tw, Geom g) {
   pdl_trigger();
-  pdl_wait();
   extern __shared__ float2 smem[];
   constexpr int KYH = L / 2 + 1;
   const int kx0 = blockIdx.x * B;
@@ -746,7 +723,13 @@ __global__ void __launch_bounds__(NT, MINB) k2f_y_fused(float2* __restrict__ X1,
   const size_t cstride = (size_t)g.ny * g.pitch1;
   float2* base = X1 + kx0;
   float* kss = reinterpret_cast<float*>(smem + 3 * TileIdx<L, B, true>::ELEMS);
+  float2* tws = reinterpret_cast<float2*>(kss + 6 * KYH * B);
+  if constexpr (PENCIL_TWS) {
+    fill_pencil_twiddles<L>(tws, tw, g.Lmax / L, threadIdx.x, NT);
+    __syncthreads();
+  }
   stage_ks<B, NT>(kss, KS + kx0, (size_t)g.Kzh * g.Kyh * g.KSp, (size_t)g.KSp, KYH, g.KSp - kx0);
+  pdl_wait();
   struct Ld {
     __device__ static constexpr bool kSmem() { return false; }
     const float2* p;
@@ -767,7 +750,8 @@ __global__ void __launch_bounds__(NT, MINB) k2f_y_fused(float2* __restrict__ X1,
       if (i < ny && b < nvalid) p[c * cs + (b + i * pitch)] = v;
     }
   } st{base, cstride, g.pitch1, g.ny, nvalid};
-  pencil_conv<L, B, NT>(smem, ld, st, kss, KYH, tw, g.Lmax / L, 1, 0, true, [] { cp_async_wait_all(); });
+  pencil_conv<L, B, NT, PENCIL_TWS>(smem, ld, st, kss, KYH, PENCIL_TWS ? tws : tw, PENCIL_TWS ? 1 : g.Lmax / L, 1, 0,
+                                    true, [] { cp_async_wait_all(); });
 }
 
 // ---------------------------------------------------------------------------
@@ -1321,7 +1305,8 @@ struct ZCfg {  // K3 and K2'
                                 : L == 512 ? GRACE_MINB_Z512
                                 : L == 1024 ? GRACE_MINB_Z1024
                                 : (NT <= 256 ? GRACE_MINB_Z : (NT <= 512 ? 2 : 1)));
-  static constexpr size_t SMEM = (size_t)3 * TileIdx<L, B, true>::ELEMS * 8 + (size_t)6 * (L / 2 + 1) * B * 4;
+  static constexpr size_t SMEM = (size_t)3 * TileIdx<L, B, true>::ELEMS * 8 + (size_t)6 * (L / 2 + 1) * B * 4 +
+                                 (PENCIL_TWS ? (size_t)pencil_tw_elems<L>() * 8 : 0);
 };
 
 #define GRACE_TRY(x)                       \
