@@ -482,7 +482,7 @@ __device__ __forceinline__ void stage_ks(float* kss, const float* __restrict__ b
 }
 
 #ifndef GRACE_PENCIL_TWS
-#define GRACE_PENCIL_TWS 1  // K3 (LDG) and K2': per-pass twiddle tables in shared memory
+#define GRACE_PENCIL_TWS 0  // K3 (LDG) and K2': per-pass twiddles in smem (off: the block's Pz = 128 K3 drops to 2 CTAs/SM, 11.9 -> 12.6 ms; SP4 unchanged)
 #endif
 constexpr bool PENCIL_TWS = GRACE_PENCIL_TWS;
 
@@ -912,8 +912,9 @@ __global__ void __launch_bounds__(XBulk<L>::NT, GRACE_XB_MINB)
   pdl_trigger();
 #endif
   fill_pass_twiddles<typename X::PL, L>(tws, tw, g.Lmax / L, threadIdx.x, NT);
-  if constexpr (FWD)
-    for (int kk = threadIdx.x; kk < X::PPE; kk += NT) twp[kk] = __ldg(tw + kk * (g.Lmax / (2 * L)));
+  // w^k = exp(-2 pi i k / Px), k = 0 .. L/2 (K1's post-process; K5's pre-process
+  // takes k > L/2 as w^k = -conj w^(L-k))
+  for (int kk = threadIdx.x; kk < X::PPE; kk += NT) twp[kk] = __ldg(tw + kk * (g.Lmax / (2 * L)));
   const int nrows = g.nzl * g.ny;
   const int total = g.nc * nrows;  // rows of components c0 .. c0 + nc - 1
   const size_t rowoff = (size_t)g.c0 * nrows;
@@ -948,7 +949,6 @@ __global__ void __launch_bounds__(XBulk<L>::NT, GRACE_XB_MINB)
   if (FWD && bump != nullptr && blockIdx.x == 0 && threadIdx.x == 0) bump->step += 1;
   int t = blockIdx.x;
   if (issuer && t < ntiles) issue(t, smraw, bar);
-  const int twpx = g.Lmax / (2 * L);
   if (t + (int)gridDim.x >= ntiles) pdl_trigger();
   for (int k = 0; t < ntiles; ++k, t += gridDim.x) {
     float2* cur = reinterpret_cast<float2*>(smraw + (k & 1) * X::TB);
@@ -1008,19 +1008,24 @@ __global__ void __launch_bounds__(XBulk<L>::NT, GRACE_XB_MINB)
       struct Ld {
         __device__ static constexpr bool kSmem() { return true; }
         const float2* s;
-        const float2* tw;
-        int twpx;
+        const float2* twp;  // w^k, k <= L/2, in smem
         __device__ float2 operator()(int b, int, int ib, int C) const {
           const int kk = ib + C;
           const float2 a = s[b * T::ROWS + kk];
           const float2 m = s[b * T::ROWS + (L - kk)];
           const float2 S = make_float2(a.x + m.x, a.y - m.y);  // X[k] + conj X[L-k]
           const float2 D = make_float2(a.x - m.x, a.y + m.y);  // X[k] - conj X[L-k]
-          const float2 w = __ldg(tw + kk * twpx);                // exp(-2 pi i k/Px)
+          float2 w;                                              // exp(-2 pi i k/Px)
+          if (kk <= L / 2) {
+            w = twp[kk];
+          } else {
+            const float2 u = twp[L - kk];
+            w = make_float2(-u.x, u.y);
+          }
           const float2 wD = cmulc(D, w);
           return make_float2(S.x - wD.y, S.y + wD.x);  // S + i w^-k D
         }
-      } ld{cur, tw, twpx};
+      } ld{cur, twp};
       float* H = static_cast<float*>(out) + (rowoff + (size_t)r0) * g.nx;
       if (nv == RB && g.nx == L)  // the pruned last pass produces exactly the nx outputs
         fft_tile<L, RB, NT, false, true, false, true, 1, false, true>(cur, ld, XbSt<false>{H, g.nx, nv}, tws, 1);
