@@ -79,19 +79,6 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-// L2 prefetch of a tensor-map box (no shared-memory destination, no completion):
-// warms L2 for a tile this or another CTA loads with TMA a little later.
-__device__ __forceinline__ void tma_prefetch_5d(const CUtensorMap* map, int c0, int c1, int c2, int c3, int c4) {
-  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];\n" ::"l"(map), "r"(c0),
-               "r"(c1), "r"(c2), "r"(c3), "r"(c4)
-               : "memory");
-}
-__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
-  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];\n" ::"l"(map), "r"(c0),
-               "r"(c1), "r"(c2), "r"(c3)
-               : "memory");
-}
-
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
                                             int c3) {
   asm volatile(
@@ -242,9 +229,6 @@ struct YTma {
 #ifndef GRACE_YT_MINB
 #define GRACE_YT_MINB 1
 #endif
-#ifndef GRACE_YT_L2PF
-#define GRACE_YT_L2PF 0  // single-buffered y tiles: prefetch the CTA's next tile into L2 (measured slower: K4 0.596 -> 0.656 ms)
-#endif
 #ifndef GRACE_YT_NB_INV
 #define GRACE_YT_NB_INV 1  // K4 tile buffers per CTA (1: two single-buffered CTAs per SM, 0.596 -> 0.585 ms; 2: double-buffered)
 #endif
@@ -282,18 +266,6 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? 2 : GRACE_YT_MINB
 #pragma unroll
     for (int nb = 0; nb < NBOX; ++nb) tma_load_5d(dst + nb * BR * NCOL, &tin, b, xt * NCOL, nb * BR, c2, c, c4);
   };
-  auto prefetch = [&](int t) {
-    const int slab = slab0 + t / ntx, xt = t - (t / ntx) * ntx;
-    const int c = slab / g.nz, z = slab - c * g.nz;
-    int c2 = z, c4 = 0;
-    if (!INV) {
-      c4 = z / g.nzl;
-      c2 = z - c4 * g.nzl;
-    }
-#pragma unroll
-    for (int nb = 0; nb < NBOX; ++nb) tma_prefetch_5d(&tin, xt * NCOL, nb * BR, c2, c, c4);
-  };
-  (void)prefetch;
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
@@ -332,11 +304,6 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? 2 : GRACE_YT_MINB
       if (threadIdx.x == 0) {
         fence_proxy_async();
         issue(t, cur, bar);
-#if GRACE_YT_L2PF
-        // single buffer: the next tile's boxes go to L2 now, so its TMA load after
-        // this tile's passes is an L2 hit instead of an HBM round trip
-        if (t + (int)gridDim.x < ntiles) prefetch(t + gridDim.x);
-#endif
       }
       mbar_wait(bar, k & 1);
     }
@@ -570,9 +537,6 @@ struct Z3Tma {
   static constexpr size_t KSB16 = (KSB + 15) / 16 * 16;
   static constexpr int TWF = Plan<L, false, 4>::TW_ELEMS, TWI = Plan<L, true, 4>::TW_ELEMS;
   static constexpr size_t TWB = (size_t)(TWF + TWI) * 8;  // per-pass twiddles, forward then inverse plan
-#ifndef GRACE_K3_L2PF
-#define GRACE_K3_L2PF 0  // L2 prefetch distance of the TMA K3 in SMs' worth of CTAs (0: off; 2-8 measured slower: K3 1.00 -> 1.39 ms)
-#endif
 #ifndef GRACE_K3_PRE
 #define GRACE_K3_PRE 1  // prefetch the mirror pencils where 4 CTAs/SM still fit
 #endif
@@ -624,21 +588,6 @@ __global__ void __launch_bounds__(Z3Tma<L>::NT, MINB)
   if (threadIdx.x == 0) {
     issue(work, kyf, bar + 1, Z::T::ELEMS);
     if (Z::PRE && nky == 2) issue(stage, g.Py - kyf, bar + 2, H * B);
-#if GRACE_K3_L2PF
-    // warm L2 for the CTA launched about one resident wave later (CTAs start in
-    // linear block order), so its first pencil load is an L2 hit
-    const int nxb = (int)gridDim.x;
-    const long long nb = (long long)blockIdx.y * nxb + blockIdx.x + (long long)GRACE_K3_L2PF * g.nsm;
-    if (nb < (long long)nxb * gridDim.y) {
-      const int pky = (int)(nb / nxb), pkx = (int)(nb - (long long)pky * nxb) * B;
-      tma_prefetch_4d(&kmap, pkx, pky, 0, 0);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        tma_prefetch_4d(&xmap, pkx, pky, 0, c);
-        if (pky != 0 && 2 * pky != g.Py) tma_prefetch_4d(&xmap, pkx, g.Py - pky, 0, c);
-      }
-    }
-#endif
   }
   struct StageLd {  // staged mirror pencils [c][z][b] (a different buffer: no in-place hazard)
     __device__ static constexpr bool kSmem() { return false; }
