@@ -218,8 +218,11 @@ int grace_kernel_times(grace_ctx *h, double *ms, long long *launches, int *nk, i
  * K2 starts on q once it has landed; likewise C2 against K4 / K5 (GRACE_NO_PIPE
  * turns this off).  C3 runs on its own stream and, on the NCCL path, its own
  * communicator (ncclCommSplit).  The step is captured into CUDA graphs like the
- * single-GPU step (GRACE_DIST_EAGER: eager launches).  Results are identical to
- * the single-GPU path (same per-pencil arithmetic).
+ * single-GPU step (GRACE_DIST_EAGER: eager launches).  Opt-in fused transposes
+ * (GRACE_P2P=1 on every rank, P <= 8): K1 and K4 store their destination blocks
+ * straight into the peers' receive buffers over NVLink (CUDA IPC handles exchanged
+ * at create), and each all-to-all shrinks to a one-float all-reduce barrier.
+ * Results are identical to the single-GPU path (same per-pencil arithmetic).
  *
  * Collective calls on the NCCL path (call them on every rank, in the same order):
  * grace_create_dist, grace_step, grace_heff, grace_mavg, grace_energy,
@@ -243,10 +246,10 @@ int grace_nccl_unique_id(void *out128);
 int grace_create_dist(int nx, int ny, int nz, double dx, double dy, double dz, double Ms, double A, double Ku,
                       double alpha, double gamma, int rank, int nranks, const void *nccl_id, grace_ctx **out);
 
-/* out[0..10] = P, rank, nz_local, z_offset, kx_block, kx_columns_here, pitch1, pitch2,
+/* out[0..11] = P, rank, nz_local, z_offset, kx_block, kx_columns_here, pitch1, pitch2,
  * transposes pipelined per component (0/1), step captured into graphs (0/1), halo on
- * its own NCCL communicator (0/1). */
-int grace_partition(grace_ctx *h, long long *out11);
+ * its own NCCL communicator (0/1), fused P2P transposes (0/1). */
+int grace_partition(grace_ctx *h, long long *out12);
 
 #ifdef __cplusplus
 }

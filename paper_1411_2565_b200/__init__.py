@@ -156,10 +156,10 @@ def grace_create_dist(nx, ny, nz, dx, dy, dz, Ms, A, Ku, alpha, gamma, rank, nra
 
 
 def grace_partition(h):
-    out = (ctypes.c_longlong * 11)()
+    out = (ctypes.c_longlong * 12)()
     _check(load().grace_partition(h, out))
     keys = ("P", "rank", "nz_local", "z_offset", "kx_block", "kx_columns", "pitch1", "pitch2", "pipelined",
-            "graphs", "halo_comm")
+            "graphs", "halo_comm", "p2p")
     return dict(zip(keys, list(out)))
 
 

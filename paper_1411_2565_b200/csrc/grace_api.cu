@@ -72,7 +72,7 @@ typedef int ncclResult_t;
 struct ncclUniqueId {
   char internal[128];
 };
-enum { kNcclUint32 = 3, kNcclUint64 = 5, kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0, kNcclMax = 2, kNcclMin = 3 };
+enum { kNcclUint8 = 1, kNcclUint32 = 3, kNcclUint64 = 5, kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0, kNcclMax = 2, kNcclMin = 3 };
 struct Nccl {
   void* h = nullptr;
   ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
@@ -80,6 +80,7 @@ struct Nccl {
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*commSplit)(ncclComm_t, int, int, ncclComm_t*, void*) = nullptr;  // optional (NCCL >= 2.18)
   ncclResult_t (*allReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*groupStart)() = nullptr;
@@ -109,12 +110,14 @@ struct Nccl {
     commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
     commSplit = (decltype(commSplit))dlsym(h, "ncclCommSplit");
     allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+    allGather = (decltype(allGather))dlsym(h, "ncclAllGather");
     send = (decltype(send))dlsym(h, "ncclSend");
     recv = (decltype(recv))dlsym(h, "ncclRecv");
     groupStart = (decltype(groupStart))dlsym(h, "ncclGroupStart");
     groupEnd = (decltype(groupEnd))dlsym(h, "ncclGroupEnd");
     errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
-    return getUniqueId && commInitRank && commDestroy && allReduce && send && recv && groupStart && groupEnd && errStr;
+    return getUniqueId && commInitRank && commDestroy && allReduce && allGather && send && recv && groupStart &&
+           groupEnd && errStr;
   }
 };
 Nccl g_nccl;
@@ -181,6 +184,14 @@ struct grace_ctx {
   cudaEvent_t evk[3] = {nullptr, nullptr, nullptr};  // component q computed (K1 / K4)
   cudaEvent_t evc[3] = {nullptr, nullptr, nullptr};  // component q transposed (C1 / C2)
   bool dist_graphs = true;                    // distributed step captured into graphs (else eager)
+  // Fused transposes (GRACE_P2P=1): K1 / K4 store into the peers' receive
+  // buffers directly (CUDA IPC over NVLink on the NCCL path); the exchanges
+  // shrink to a barrier (a one-float ncclAllReduce) after each.
+  bool p2p = false;
+  float2* peerA[8] = {};  // rank q's A (K4's destination) and B (K1's destination)
+  float2* peerB[8] = {};
+  std::vector<void*> ipc_open;  // handles opened with cudaIpcOpenMemHandle
+  float* p2p_bar = nullptr;     // device float of the barrier all-reduce
   cudaGraphExec_t g1[2] = {nullptr, nullptr}, gc[2] = {nullptr, nullptr};
   ncclComm_t comm = nullptr;
   ncclComm_t comm_halo = nullptr;  // C3's own communicator (NCCL orders work per communicator)
@@ -260,6 +271,79 @@ struct grace_ctx {
     bad |= g_nccl.groupEnd() != 0;
     return bad ? cudaErrorUnknown : cudaSuccess;
   }
+  // rank rk's geometry with the fused-transpose destinations
+  Geom p2p_geom(const Rank& rk, float2* const* peers) const {
+    Geom g = rk.g;
+    g.p2p = 1;
+    g.rank = rk.r;
+    for (int q = 0; q < P; ++q) g.peer[q] = peers[q];
+    return g;
+  }
+  // every rank's K1 (or K4) stores have landed: stream order on the virtual path,
+  // a one-float all-reduce (all ranks reach it after their kernel) on the NCCL path
+  cudaError_t p2p_barrier(cudaStream_t s) {
+    if (mode != kNccl) return cudaSuccess;
+    return g_nccl.allReduce(p2p_bar, p2p_bar, 1, kNcclFloat32, kNcclSum, comm, s) == 0 ? cudaSuccess
+                                                                                      : cudaErrorUnknown;
+  }
+  // Set up the fused transposes: peer buffer tables (IPC handles exchanged with
+  // ncclAllGather on the NCCL path).  The ranks agree on the outcome (min-reduce).
+  cudaError_t setup_p2p() {
+    if (mode == kSingle || P > 8) return cudaSuccess;
+    bool ok = true;
+    for (auto& rk : ranks) ok = ok && p2p_ok(rk.g) && (rk.g.Kc == 0 || rk.tma);
+    if (mode == kVirtual) {
+      if (!ok) return cudaSuccess;
+      for (int q = 0; q < P; ++q) {
+        peerA[q] = ranks[q].A;
+        peerB[q] = ranks[q].B;
+      }
+      p2p = true;
+      return cudaSuccess;
+    }
+    Rank& rk = ranks[0];
+    CE(cudaMalloc(&p2p_bar, 2 * sizeof(cudaIpcMemHandle_t) * (P + 1)));
+    unsigned char* dev = reinterpret_cast<unsigned char*>(p2p_bar) + 64;  // handle exchange scratch after the float
+    const size_t hb = 2 * sizeof(cudaIpcMemHandle_t);
+    std::vector<unsigned char> hs(hb * P, 0), mine(hb, 0);
+    if (ok) {
+      cudaIpcMemHandle_t h2[2];
+      ok = cudaIpcGetMemHandle(&h2[0], rk.A) == cudaSuccess && cudaIpcGetMemHandle(&h2[1], rk.B) == cudaSuccess;
+      if (ok) std::memcpy(mine.data(), h2, hb);
+    }
+    cudaGetLastError();
+    CE(cudaMemcpy(dev, mine.data(), hb, cudaMemcpyHostToDevice));
+    if (g_nccl.allGather(dev, dev + hb, hb, kNcclUint8, comm, stream) != 0) return cudaErrorUnknown;
+    CE(cudaMemcpyAsync(hs.data(), dev + hb, hb * P, cudaMemcpyDeviceToHost, stream));
+    CE(cudaStreamSynchronize(stream));
+    for (int q = 0; q < P && ok; ++q) {
+      if (q == myrank) {
+        peerA[q] = rk.A;
+        peerB[q] = rk.B;
+        continue;
+      }
+      cudaIpcMemHandle_t h2[2];
+      std::memcpy(h2, hs.data() + hb * q, hb);
+      void* pa = nullptr;
+      void* pb = nullptr;
+      ok = cudaIpcOpenMemHandle(&pa, h2[0], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+      if (ok) ipc_open.push_back(pa);
+      ok = ok && cudaIpcOpenMemHandle(&pb, h2[1], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+      if (ok) ipc_open.push_back(pb);
+      peerA[q] = static_cast<float2*>(pa);
+      peerB[q] = static_cast<float2*>(pb);
+    }
+    cudaGetLastError();
+    // agree: every rank uses the fused transposes or none does
+    float v = ok ? 0.f : 1.f;
+    CE(cudaMemcpy(p2p_bar, &v, sizeof v, cudaMemcpyHostToDevice));
+    if (g_nccl.allReduce(p2p_bar, p2p_bar, 1, kNcclFloat32, kNcclSum, comm, stream) != 0) return cudaErrorUnknown;
+    CE(cudaMemcpyAsync(&v, p2p_bar, sizeof v, cudaMemcpyDeviceToHost, stream));
+    CE(cudaStreamSynchronize(stream));
+    p2p = v == 0.f;
+    return cudaSuccess;
+  }
+
   // component q of rank rk's geometry (K1, K2, K4, K5 on one component)
   static Geom comp_geom(const Rank& rk, int q) {
     Geom g = rk.g;
@@ -348,6 +432,18 @@ struct grace_ctx {
       return cudaSuccess;
     }
     CE(halo_start(c, s));  // C3: one M plane to each neighbour, overlapped
+    if (p2p) {  // fused transposes: K1 / K4 store into the peers' buffers
+      for (auto& rk : ranks) CE(launch_k1(p2p_geom(rk, peerB), rk.M[c], rk.A, tw, bump ? rk.prm : nullptr, s));
+      CE(p2p_barrier(s));
+      for (auto& rk : ranks) {
+        if (rk.g.Kc > 0) {
+          CE(launch_k2(rk.g, rk.B, rk.X2, tw, s, rk.tma ? &rk.k2map : nullptr));
+          CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s, rk.tma3 ? &rk.k3x : nullptr, rk.tma3 ? &rk.k3k : nullptr));
+          CE(launch_k4(p2p_geom(rk, peerA), rk.X2, rk.B, tw, s, rk.tma ? &rk.k4map : nullptr));
+        }
+      }
+      return p2p_barrier(s);
+    }
     if (!pipe) {
       for (auto& rk : ranks) CE(launch_k1(rk.g, rk.M[c], rk.A, tw, bump ? rk.prm : nullptr, s));
       CE(alltoall(&Rank::A, &Rank::B, s));  // C1: z slabs -> kx blocks
@@ -521,6 +617,8 @@ struct grace_ctx {
     if (evM) cudaEventDestroy(evM);
     if (evH) cudaEventDestroy(evH);
     if (cs) cudaStreamDestroy(cs);
+    for (void* p : ipc_open) cudaIpcCloseMemHandle(p);
+    if (p2p_bar) cudaFree(p2p_bar);
     for (int q = 0; q < 3; ++q) {
       if (evk[q]) cudaEventDestroy(evk[q]);
       if (evc[q]) cudaEventDestroy(evc[q]);
@@ -698,6 +796,13 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
     }
   cudaGetLastError();
   h->N = (mode == grace_ctx::kNccl) ? h->ranks[0].Nl : (long long)nx * ny * nz;
+  if (dlay) {  // fused transposes (opt-in; collective on the NCCL path: set GRACE_P2P on every rank)
+    const char* pe = getenv("GRACE_P2P");
+    if (pe && pe[0] == '1') {
+      if (h->setup_p2p() != cudaSuccess) return bail(fail(GRACE_ECUDA, "fused-transpose (P2P) setup failed"));
+      if (h->p2p) h->pipe = false;
+    }
+  }
 
   // setup: fp64 octant -> fp64 padded spectrum -> fp32 folded KS (S1..S5), once,
   // one tensor component at a time; each rank's table receives only its kx
@@ -1340,10 +1445,10 @@ int grace_geometry(grace_ctx* h, long long* o) {
 int grace_partition(grace_ctx* h, long long* o) {
   if (!h || !o) return fail(GRACE_EINVAL, "NULL argument");
   const Geom& g = h->ranks[0].g;
-  const long long v[11] = {h->P,      h->ranks[0].r, g.nzl,    (long long)h->ranks[0].r * g.nzl,
+  const long long v[12] = {h->P,      h->ranks[0].r, g.nzl,    (long long)h->ranks[0].r * g.nzl,
                            g.kb,      g.Kc,          g.pitch1, g.pitch2,
                            h->pipe,   (h->mode == grace_ctx::kSingle || h->dist_graphs) ? 1 : 0,
-                           h->comm_halo != nullptr};
+                           h->comm_halo != nullptr, h->p2p};
   std::memcpy(o, v, sizeof v);
   return GRACE_OK;
 }

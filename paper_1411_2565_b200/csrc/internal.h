@@ -56,6 +56,12 @@ struct Geom {
   int masked;          // geometry mask set (grace_set_geometry): M = 0 marks an empty cell (reading Q26)
   int c0, nc;          // components c0 .. c0 + nc - 1 handled by K1, K2, K4, K5 (default 0, 3; the
                        // distributed step runs them per component to pipeline the transposes)
+  // Fused transposes (GRACE_P2P, distributed path): K1 / K4 store x-row block q
+  // straight into rank q's receive buffer peer[q] (block `rank` of it) instead of
+  // their own send buffer -- peer memory over NVLink (CUDA IPC) on the NCCL path,
+  // the other ranks' buffers on the virtual path.  0: off.
+  int p2p, rank;
+  float2* peer[8];
   float cx, cy, cz; // exchange 2A/(mu0 Ms^2 d^2) per axis (0 for a singleton axis)
   float ck;         // anisotropy 2Ku/(mu0 Ms^2)
   float Ms;
@@ -95,6 +101,7 @@ cudaError_t launch_k6(const Geom& g, int mode, const float* Hd, const float* M, 
                       const float* Hhi, unsigned* aerr = nullptr);
 bool fused_y_path(const Geom& g);  // nz == 1 and the y-pencils of 3 components fit one CTA
 bool comp_split_ok(const Geom& g); // K1 .. K5 can run per component (bulk-copy x kernels)
+bool p2p_ok(const Geom& g);        // K1 / K4 can store into peers' buffers (bulk-copy K1, TMA K4)
 void set_pdl_blocked(bool b);      // this thread's next launches without programmatic dependent launch
 int kernel_count(const Geom& g);   // kernels per step
 

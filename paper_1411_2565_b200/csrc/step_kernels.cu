@@ -171,6 +171,14 @@ __device__ __forceinline__ size_t xrow_slab(const Geom& g, int slab) {
   const int q = z / g.nzl, zl = z - q * g.nzl;
   return ((size_t)(q * 3 + c) * g.nzl + zl) * g.ny * g.pitch1;
 }
+// K4's destination for that slab: its own buffer (then the C2 transpose), or with
+// fused transposes block `rank` of the owning rank q's buffer (peer memory).
+__device__ __forceinline__ float2* xrow_dst(const Geom& g, float2* out, int slab) {
+  if (!g.p2p) return out + xrow_slab(g, slab);
+  const int c = slab / g.nz, z = slab - c * g.nz;
+  const int q = z / g.nzl, zl = z - q * g.nzl;
+  return g.peer[q] + ((size_t)(g.rank * 3 + c) * g.nzl + zl) * g.ny * g.pitch1;
+}
 
 // ---------------------------------------------------------------------------
 // K2 / K4: y pencils.  Columns (kx) are contiguous; a CTA owns NCOL columns of one
@@ -309,7 +317,7 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? 2 : GRACE_YT_MINB
     }
     const int slab = slab0 + t / ntx, xt = t - (t / ntx) * ntx;
     const int kx0 = xt * NCOL;
-    float2* o = out + (INV ? xrow_slab(g, slab) : (size_t)slab * g.Py * g.pitch2) + kx0;
+    float2* o = (INV ? xrow_dst(g, out, slab) : out + (size_t)slab * g.Py * g.pitch2) + kx0;
     const int pitch = INV ? g.pitch1 : g.pitch2;
     if (g.Kc - kx0 >= NCOL && n_out >= (INV ? L / 2 : L))
       fft_tile<L, NCOL, NT, true, INV, !INV, INV, 1, false, true>(cur, SmemLd<L, NCOL, true>{cur}, StFull{o, pitch},
@@ -925,12 +933,13 @@ __global__ void __launch_bounds__(XBulk<L>::NT, GRACE_XB_MINB)
       if (b < nv) {
         float2* X1 = static_cast<float2*>(out);
         const size_t gr = rowoff + (size_t)(r0 + b);
-        auto at = [&](int kk) -> size_t {
-          if constexpr (DIST) {
+        auto at = [&](int kk) -> float2* {
+          if constexpr (DIST) {  // destination-blocked: kx block q goes to rank q
             const int q = kk / g.kb;
-            return q * g.blk1 + gr * g.pitch1 + (kk - q * g.kb);
+            if (g.p2p) return g.peer[q] + g.rank * g.blk1 + gr * g.pitch1 + (kk - q * g.kb);  // fused transpose
+            return X1 + q * g.blk1 + gr * g.pitch1 + (kk - q * g.kb);
           } else {
-            return gr * g.pitch1 + kk;
+            return X1 + gr * g.pitch1 + kk;
           }
         };
         const float2* z = cur + b * T::ROWS;
@@ -945,12 +954,12 @@ __global__ void __launch_bounds__(XBulk<L>::NT, GRACE_XB_MINB)
           const int kk = jb + i * TPC;
           const float2 w = twp[kk];
           const float2 Zk = z[kk], Zn = z[(L - kk) & (L - 1)];
-          X1[at(kk)] = post(Zk, Zn, w);
-          X1[at(L - kk)] = post(Zn, Zk, make_float2(-w.x, w.y));
+          *at(kk) = post(Zk, Zn, w);
+          *at(L - kk) = post(Zn, Zk, make_float2(-w.x, w.y));
         }
         if (jb == 0) {  // k = L/2 pairs with itself
           const float2 Zk = z[L / 2];
-          X1[at(L / 2)] = post(Zk, Zk, twp[L / 2]);
+          *at(L / 2) = post(Zk, Zk, twp[L / 2]);
         }
       }
     } else {
@@ -1630,6 +1639,8 @@ bool fused_y_path(const Geom& g) { return g.Pz == 1 && g.Py <= 512; }
 // K1 and K5 take the persistent bulk-copy kernels (which, like K2 and K4, can run
 // on a range of components): the distributed step may then pipeline the
 // transposes per component.
+bool p2p_ok(const Geom& g) { return comp_split_ok(g) && g.Py >= kTmaMinL; }
+
 bool comp_split_ok(const Geom& g) {
   if (g.Px < 2 || fused_y_path(g)) return false;
 #define CASE(v) case v: return (v >= kXBulkMinL && v <= kXBulkMaxL) && xbulk_ok<(v >= kXBulkMinL && v <= kXBulkMaxL ? v : kXBulkMinL)>(g, true) && xbulk_ok<(v >= kXBulkMinL && v <= kXBulkMaxL ? v : kXBulkMinL)>(g, false);

@@ -221,3 +221,58 @@ def test_nccl_one_rank_graphs_pipeline_and_agreed_nonfinite(monkeypatch):
     assert res[0][1] == res[1][1]
     pb.grace_destroy(h)
     ref.close()
+
+
+@pytest.mark.parametrize("n,P", [((128, 64, 16), 4), ((100, 20, 4), 2)])
+def test_fused_p2p_transposes_bitwise(n, P, monkeypatch):
+    """GRACE_P2P: K1 / K4 store their destination blocks straight into the other
+    ranks' receive buffers (no separate all-to-all): bitwise the pipelined NCCL-style
+    exchange path and the single-GPU step."""
+    d = (1e-9, 1e-9, 1e-9)
+    M = random_m(n, 1e6, seed=62)
+    out = []
+    for p2p in (True, False):
+        if p2p:
+            monkeypatch.setenv("GRACE_P2P", "1")
+        else:
+            monkeypatch.delenv("GRACE_P2P", raising=False)
+        g = pb.Grace(n, d, 1e6, 1e-11, 6.2832e4, 0.5, GAMMA0, virtual_ranks=P)
+        part = pb.grace_partition(g.h)
+        assert part["p2p"] == (1 if p2p else 0)
+        assert part["pipelined"] == (0 if p2p else 1)
+        g.set_m(M)
+        g.step(19, 1e-15)
+        out.append((g.get_m(), g.heff()))
+        g.close()
+    monkeypatch.delenv("GRACE_P2P", raising=False)
+    ref = pb.Grace(n, d, 1e6, 1e-11, 6.2832e4, 0.5, GAMMA0)
+    ref.set_m(M)
+    ref.step(19, 1e-15)
+    out.append((ref.get_m(), ref.heff()))
+    ref.close()
+    for Mo, Ho in out[1:]:
+        assert np.array_equal(out[0][0], Mo)
+        assert np.array_equal(out[0][1], Ho)
+
+
+def test_fused_p2p_nccl_one_rank(monkeypatch):
+    """The fused transposes on the NCCL path (one rank: its own buffers as the peer
+    table; the barrier all-reduce captured into the step graphs)."""
+    monkeypatch.setenv("GRACE_FORCE_NCCL", "1")
+    monkeypatch.setenv("GRACE_P2P", "1")
+    n, d, Ms = (64, 20, 8), (2e-9, 2e-9, 3e-9), 8e5
+    M = random_m(n, Ms, seed=58)
+    h = pb.grace_create_dist(*n, *d, Ms, 1.3e-11, 2e4, 0.3, GAMMA0, 0, 1, pb.grace_nccl_unique_id())
+    assert pb.grace_partition(h)["p2p"] == 1
+    monkeypatch.delenv("GRACE_P2P")
+    ref = pb.Grace(n, d, Ms, 1.3e-11, 2e4, 0.3, GAMMA0)
+    res = []
+    for hh in (h, ref.h):
+        pb.grace_set_m(hh, M.ravel().copy())
+        pb.grace_step(hh, 20, 2e-14)
+        Mo = np.empty(3 * M[0].size)
+        pb.grace_get_m(hh, Mo)
+        res.append(Mo)
+    assert np.array_equal(res[0], res[1])
+    pb.grace_destroy(h)
+    ref.close()
