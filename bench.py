@@ -373,7 +373,10 @@ def run_own(args, w):
                    "alpha": w.alpha, "dt": w.dt, "gamma0": w.gamma0,
                    "l2": f"inputs larger than L2 ({(pb.grace_device_bytes(g.h)) / 1e9:.2f} GB resident vs 126 MB L2); no flush",
                    "parallelism": "single GPU" if world == 1 else
-                   (f"z-slab x{world}: NCCL send/recv transposes pipelined per component + halo planes (one grid)" if distributed
+                   (f"z-slab x{world}: " + ("fused P2P transposes (K1/K4 store into peers over NVLink)"
+                                            if os.environ.get("GRACE_P2P") == "1" else
+                                            "NCCL send/recv transposes pipelined per component")
+                    + " + halo planes (one grid)" if distributed
                     else f"{world} independent replicas (nz not divisible by {world})"),
                    "step": " | ".join(STEP_DESC[k] for k in names),
                    "timing": "timed region 1 (value, ms_per_step): K steps of CUDA-graph replay with programmatic "

@@ -302,9 +302,10 @@ struct grace_ctx {
       return cudaSuccess;
     }
     Rank& rk = ranks[0];
-    CE(cudaMalloc(&p2p_bar, 2 * sizeof(cudaIpcMemHandle_t) * (P + 1)));
-    unsigned char* dev = reinterpret_cast<unsigned char*>(p2p_bar) + 64;  // handle exchange scratch after the float
-    const size_t hb = 2 * sizeof(cudaIpcMemHandle_t);
+    const size_t hb = 2 * sizeof(cudaIpcMemHandle_t);  // this rank's (A, B) handles
+    // [barrier float | pad to 64 B | own handles | every rank's handles]
+    CE(cudaMalloc(&p2p_bar, 64 + hb * (P + 1)));
+    unsigned char* dev = reinterpret_cast<unsigned char*>(p2p_bar) + 64;
     std::vector<unsigned char> hs(hb * P, 0), mine(hb, 0);
     if (ok) {
       cudaIpcMemHandle_t h2[2];
