@@ -108,3 +108,25 @@ def test_slab_graph_pdl_step_bitwise_equals_eager():
     diff = np.flatnonzero(a.ravel() != b.ravel())
     assert diff.size == 0, (diff.size, diff[:5])
     g.close()
+
+
+def test_film_full_grid_heff_and_step():
+    """BASELINE configs[2] (film 512x512x8 at 5x5x3 nm) at full size: the whole H_eff
+    (rel-L2 <= 1e-5) and one Euler step cell by cell against the oracle."""
+    w = WORKLOADS["film_512x512x8"]
+    op = DemagFFT(tensor_octant(*w.n, *w.d))
+    M = random_m(w.n, w.Ms, seed=33)
+    hext = (1e3, 2e3, -5e2)
+    g = pb.Grace(w.n, w.d, w.Ms, w.A, w.Ku, w.alpha, GAMMA0)
+    g.set_m(M)
+    g.set_hext(hext)
+    Hg = g.heff()
+    Ho = oracle_heff(M, op, w.A, w.Ms, w.Ku, w.d, hext)
+    assert float(np.linalg.norm(Hg - Ho) / np.linalg.norm(Ho)) <= 1e-5
+    M0 = g.get_m()
+    g.step(1, w.dt)
+    Mg = g.get_m()
+    g.close()
+    sim = Sim(M0, op, w.Ms, w.A, w.Ku, w.alpha, GAMMA0, w.d, hext)
+    sim.euler_step(w.dt)
+    assert np.abs(Mg - sim.M).max() <= 2e-5 * w.Ms
