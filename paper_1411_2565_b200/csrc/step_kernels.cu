@@ -543,8 +543,11 @@ struct Z3Tma {
   static constexpr size_t STAGE = 3 * (size_t)H * B * 8;
   static constexpr size_t KSB = 6 * (size_t)KZH * B * 4;
   static constexpr size_t KSB16 = (KSB + 15) / 16 * 16;
-  static constexpr int TWF = Plan<L, false, 4>::TW_ELEMS, TWI = Plan<L, true, 4>::TW_ELEMS;
-  static constexpr size_t TWB = (size_t)(TWF + TWI) * 8;  // per-pass twiddles, forward then inverse plan
+  // per-pass twiddles in smem, forward then inverse plan (fused plans; unfused
+  // long pencils keep the global table so the CTA count per SM is unchanged)
+  static constexpr bool TWS = ZPlan<L>::FUSE;
+  static constexpr int TWF = TWS ? Plan<L, false, 4>::TW_ELEMS : 0, TWI = TWS ? Plan<L, true, 4>::TW_ELEMS : 0;
+  static constexpr size_t TWB = (size_t)(TWF + TWI) * 8;
 #ifndef GRACE_K3_PRE
 #define GRACE_K3_PRE 1  // prefetch the mirror pencils where 4 CTAs/SM still fit
 #endif
@@ -584,8 +587,12 @@ __global__ void __launch_bounds__(Z3Tma<L>::NT, MINB)
   }
   // per-pass twiddle tables in smem (the global table's lines would miss the
   // minimal L1 of a shared-memory-carveout kernel)
-  fill_pass_twiddles<Plan<L, false, 4>, L>(tws, tw, g.Lmax / L, threadIdx.x, NT);
-  fill_pass_twiddles<Plan<L, true, 4>, L>(tws + Z::TWF, tw, g.Lmax / L, threadIdx.x, NT);
+  if constexpr (Z::TWS) {
+    fill_pass_twiddles<Plan<L, false, 4>, L>(tws, tw, g.Lmax / L, threadIdx.x, NT);
+    fill_pass_twiddles<Plan<L, true, 4>, L>(tws + Z::TWF, tw, g.Lmax / L, threadIdx.x, NT);
+  }
+  const float2* twp = Z::TWS ? tws : tw;  // the passes' twiddle source and stride
+  const int twstr = Z::TWS ? 1 : g.Lmax / L;
   __syncthreads();
   pdl_wait();  // X2 comes from K2
   auto issue = [&](float2* dst, int ky, uint64_t* b, int cstep) {
@@ -620,11 +627,11 @@ __global__ void __launch_bounds__(Z3Tma<L>::NT, MINB)
     };
     if (rep == 0) {
       mbar_wait(bar + 1, 0);
-      pencil_conv<L, B, NT, true>(work, SmemLd<L, B, true>{work}, st, kss, Z::KZH, tws, 1, g.Py, ky, false, kw);
+      pencil_conv<L, B, NT, Z::TWS>(work, SmemLd<L, B, true>{work}, st, kss, Z::KZH, twp, twstr, g.Py, ky, false, kw);
     } else if constexpr (Z::PRE) {
       __syncthreads();  // the work tile is free
       mbar_wait(bar + 2, 0);
-      pencil_conv<L, B, NT, true>(work, StageLd{stage}, st, kss, Z::KZH, tws, 1, g.Py, ky, false, kw);
+      pencil_conv<L, B, NT, Z::TWS>(work, StageLd{stage}, st, kss, Z::KZH, twp, twstr, g.Py, ky, false, kw);
     } else {
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -632,7 +639,7 @@ __global__ void __launch_bounds__(Z3Tma<L>::NT, MINB)
         issue(work, ky, bar + 1, Z::T::ELEMS);
       }
       mbar_wait(bar + 1, 1);
-      pencil_conv<L, B, NT, true>(work, SmemLd<L, B, true>{work}, st, kss, Z::KZH, tws, 1, g.Py, ky, false, kw);
+      pencil_conv<L, B, NT, Z::TWS>(work, SmemLd<L, B, true>{work}, st, kss, Z::KZH, twp, twstr, g.Py, ky, false, kw);
     }
   }
 }
@@ -1561,8 +1568,12 @@ cudaError_t make_ky_tmaps(const Geom& g, const float2* k2_in, const float2* x2, 
 #define GRACE_K3_TMA_MINL 32  // shortest z pencil fed by TMA (L = 16 keeps k3_z: 2 CTAs/SM of 77 KB either way)
 #endif
 template <int L>
+#ifndef GRACE_K3_TMA_MAXL
+#define GRACE_K3_TMA_MAXL 128  // longest z pencil fed by TMA (block Pz = 128: K3 11.4 -> 10.5 ms; 256 neutral)
+#endif
 constexpr bool k3_tma_ok() {
-  return ZPlan<L>::FUSE && L >= GRACE_K3_TMA_MINL && L >= 16;
+  return L >= GRACE_K3_TMA_MINL && L >= 16 && L <= GRACE_K3_TMA_MAXL && !TileIdx<L, ZPlan<L>::B, true>::PAD &&
+         ZPlan<L>::B * 8 >= 16;
 }
 
 // K3 tensor maps: X2 [3][nz][Py][pitch2] complex as 4-D {kx < Kc, ky, z, c}, box

@@ -68,6 +68,11 @@ WORKLOADS = {
 }
 
 
+for _N in (128, 256):  # Table-1 sizes as bench workloads (table1_cube below)
+    WORKLOADS[f"cube_{_N}"] = Workload(f"cube_{_N}", (_N, _N, _N), (1e-9, 1e-9, 1e-9), BENCH_MS, BENCH_A, BENCH_KU,
+                                       0.5, 1e-15, note="paper Table 1 size")
+
+
 def table1_cube(N):
     """Paper Table 1 workload: N^3 cube, Sec. 4 material, 1 nm cells."""
     return Workload(f"cube_{N}", (N, N, N), (1e-9, 1e-9, 1e-9), BENCH_MS, BENCH_A, BENCH_KU,
