@@ -241,7 +241,7 @@ struct YTma {
 #define GRACE_YT_NB_INV 1  // K4 tile buffers per CTA (1: two single-buffered CTAs per SM, 0.596 -> 0.585 ms; 2: double-buffered)
 #endif
 template <int L, int NCOL, bool INV, int NB = 2>
-__global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? 2 : GRACE_YT_MINB)
+__global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? (YTma<L, NCOL>::NT <= 512 ? 2 : 1) : GRACE_YT_MINB)
     k_y_tma(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, const float2* __restrict__ tw, Geom g,
             int n_out) {
   using Y = YTma<L, NCOL, NB>;
@@ -1422,7 +1422,7 @@ static cudaError_t ky_tma_launch(const Geom& g, float2* out, const float2* tw, c
   cudaError_t e = prep(kern, Y::SMEM);
   if (e != cudaSuccess) return e;
   const int ntiles = ((g.Kc + NCOL - 1) / NCOL) * g.nc * g.nz;
-  const int want = NB == 1 ? 2 : GRACE_YT_MINB;
+  const int want = NB == 1 ? (Y::NT <= 512 ? 2 : 1) : GRACE_YT_MINB;
   const int per_sm = (int)(220 * 1024 / Y::SMEM) < want ? (int)(220 * 1024 / Y::SMEM) : want;
   const int cap = g.nsm * (per_sm > 0 ? per_sm : 1);
   const int grid = ntiles < cap ? ntiles : cap;
