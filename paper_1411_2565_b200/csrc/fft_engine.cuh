@@ -64,7 +64,15 @@ __host__ __device__ constexpr int fft_rmax(int L, int RB = 4) { return L <= 1 ? 
 #ifndef GRACE_RB_ROWS3
 #define GRACE_RB_ROWS3 4
 #endif
-__host__ __device__ constexpr int rb_for(bool colmode, int V) { return (!colmode && V == 3) ? GRACE_RB_ROWS3 : 4; }
+// Column-mode three-component 16-point pencils (the film's and 8^3 cubes' z axis):
+// radix 4 x 4 (four threads per pencil, 12 complex values each) instead of one
+// radix-16 pass (one thread per pencil holding 48: 168 registers, 8 warps/SM).
+#ifndef GRACE_RB_Z16
+#define GRACE_RB_Z16 2
+#endif
+__host__ __device__ constexpr int rb_for(bool colmode, int V, int L = 0) {
+  return (!colmode && V == 3) ? GRACE_RB_ROWS3 : ((colmode && V == 3 && L == 16) ? GRACE_RB_Z16 : 4);
+}
 
 // x * exp(-+2 pi i K/16) for compile-time K (forward sign -, INV conjugates).
 template <bool INV, int K>
@@ -283,7 +291,7 @@ __device__ __forceinline__ float2 tw_lds(const float2* p) {
 // first pass, all in registers).
 template <int L, int P, bool REV, int NCOL, int NT, bool COLMODE, int V>
 struct Pass {
-  static constexpr int RB = rb_for(COLMODE, V);
+  static constexpr int RB = rb_for(COLMODE, V, L);
   using PL = Plan<L, REV, RB>;
   using TM = ThreadMap<L, NCOL, NT, COLMODE>;
   using T = TileIdx<L, NCOL, COLMODE, PL::R(0)>;
@@ -419,7 +427,7 @@ template <int L, int P, bool REV, int NCOL, int NT, bool COLMODE, int V, bool IN
           int DSTN, bool TWS = false, class LD, class ST>
 __device__ __forceinline__ void fft_passes(const ThreadMap<L, NCOL, NT, COLMODE>& tm, float2* s, const LD& ld,
                                            const ST& st, const float2* __restrict__ tw, int twstride) {
-  constexpr int RB = rb_for(COLMODE, V);
+  constexpr int RB = rb_for(COLMODE, V, L);
   constexpr int NP = fft_npass(L, RB);
   constexpr bool first = (P == 0), last = (P == NP - 1);
   constexpr int IFACE0 = TileIdx<L, NCOL, COLMODE, Plan<L, REV, RB>::R(0)>::PAD ? kPad : kLin;
@@ -447,7 +455,7 @@ template <int L, int P, int NH, bool REV, int NCOL, int NT, bool COLMODE, int V,
 __device__ __forceinline__ void fft_head(const ThreadMap<L, NCOL, NT, COLMODE>& tm, float2* s, const LD& ld,
                                          const ST& none, const float2* __restrict__ tw, int twstride) {
   if constexpr (P < NH) {
-    constexpr int RB = rb_for(COLMODE, V);
+    constexpr int RB = rb_for(COLMODE, V, L);
     constexpr int IFACE0 = TileIdx<L, NCOL, COLMODE, Plan<L, REV, RB>::R(0)>::PAD ? kPad : kLin;
     if constexpr (P == 0) {
       fft_pass<L, 0, REV, NCOL, NT, COLMODE, V, INV, HIN, false, kExt, IFACE0, TWS>(tm, ld, none, s, tw, twstride);
@@ -468,7 +476,7 @@ template <int L, int NCOL, int NT, bool COLMODE, int V, bool INV, bool HIN, bool
           class LD, class PS>
 __device__ __forceinline__ void fft_to_regs(const ThreadMap<L, NCOL, NT, COLMODE>& tm, float2* s, const LD& ld,
                                             const float2* __restrict__ tw, int twstride, PS& ps) {
-  constexpr int RB = rb_for(COLMODE, V);
+  constexpr int RB = rb_for(COLMODE, V, L);
   constexpr int NP = fft_npass(L, RB);
   constexpr int IFACE0 = TileIdx<L, NCOL, COLMODE, Plan<L, REV, RB>::R(0)>::PAD ? kPad : kLin;
   if constexpr (NP == 1) {
@@ -498,7 +506,7 @@ template <int L, int NCOL, int NT, bool COLMODE, int V, bool INV, bool HOUT, boo
           class PS>
 __device__ __forceinline__ void fft_from_regs(const ThreadMap<L, NCOL, NT, COLMODE>& tm, float2* s, const ST& st,
                                               const float2* __restrict__ tw, int twstride, PS& ps) {
-  constexpr int RB = rb_for(COLMODE, V);
+  constexpr int RB = rb_for(COLMODE, V, L);
   constexpr int NP = fft_npass(L, RB);
   constexpr int IFACE0 = TileIdx<L, NCOL, COLMODE, Plan<L, REV, RB>::R(0)>::PAD ? kPad : kLin;
   struct None {

@@ -49,12 +49,13 @@ __device__ __forceinline__ void kmul_s(float2& a, float2& b, float2& c, const fl
 template <int L>
 struct ZPlan {
   static constexpr bool FUSE = L >= 2 && L <= 64;
-  static constexpr int RLAST = L <= 1 ? 1 : 1 << fft_pass_bits(L, fft_npass(L) - 1);
+  static constexpr int RB = rb_for(true, 3, L);  // radix bits of the three-component pencil plans
+  static constexpr int RLAST = L <= 1 ? 1 : 1 << fft_pass_bits(L, fft_npass(L, RB) - 1, RB);
   // threads per column, unfused: L / R for the plan's largest radix R up to
   // L = 512, so no pass leaves threads idle (L / 8 idled half of them in the
   // radix-16 passes: 128^3 cube K3 0.32 -> 0.17 ms, block 17.9 -> 12.1 ms);
   // L / 8 for L = 1024 (16.8.8: more threads beat the idle pass, 20.7 vs 23.0 ms)
-  static constexpr int R0 = L <= 1 ? 1 : 1 << fft_pass_bits(L, 0);
+  static constexpr int R0 = L <= 1 ? 1 : 1 << fft_pass_bits(L, 0, RB);
   static constexpr int TPC = L <= 1 ? 1 : (FUSE ? L / RLAST : (L <= 512 ? L / R0 : L / 8));
   // fused (short) pencils: at least GRACE_Z_MINNT threads per CTA; unfused:
   // GRACE_Z_ELEMS values per component per CTA (smem: 3 components resident)
@@ -70,14 +71,17 @@ struct ZPlan {
 
 template <int L>
 __host__ __device__ constexpr int pencil_tw_elems() {
-  return ZPlan<L>::FUSE ? Plan<L, false, 4>::TW_ELEMS + Plan<L, true, 4>::TW_ELEMS : Plan<L, false, 4>::TW_ELEMS;
+  constexpr int RB = ZPlan<L>::RB;
+  return ZPlan<L>::FUSE ? Plan<L, false, RB>::TW_ELEMS + Plan<L, true, RB>::TW_ELEMS : Plan<L, false, RB>::TW_ELEMS;
 }
 // Fill the shared table pencil_conv<..., TWS = true> reads (threads [tid, nt)).
 template <int L>
 __device__ __forceinline__ void fill_pencil_twiddles(float2* dst, const float2* __restrict__ tw, int twstride, int tid,
                                                      int nt) {
-  fill_pass_twiddles<Plan<L, false, 4>, L>(dst, tw, twstride, tid, nt);
-  if constexpr (ZPlan<L>::FUSE) fill_pass_twiddles<Plan<L, true, 4>, L>(dst + Plan<L, false, 4>::TW_ELEMS, tw, twstride, tid, nt);
+  constexpr int RB = ZPlan<L>::RB;
+  fill_pass_twiddles<Plan<L, false, RB>, L>(dst, tw, twstride, tid, nt);
+  if constexpr (ZPlan<L>::FUSE)
+    fill_pass_twiddles<Plan<L, true, RB>, L>(dst + Plan<L, false, RB>::TW_ELEMS, tw, twstride, tid, nt);
 }
 
 // kw(): called before the multiply's barrier -- waits for this thread's part of
@@ -106,11 +110,11 @@ __device__ __forceinline__ void pencil_conv(float2* smem, const LD& ld, const ST
   };
   const ThreadMap<L, B, NT, true> tm;
   if constexpr (ZPlan<L>::FUSE) {
-    using PF = Pass<L, fft_npass(L) - 1, false, B, NT, true, 3>;
+    using PF = Pass<L, fft_npass(L, ZPlan<L>::RB) - 1, false, B, NT, true, 3>;
     using PI = Pass<L, 0, true, B, NT, true, 3>;
     static_assert(PF::R == PI::R && PF::UPT == 1 && PI::UPT == 1, "fused plan");
     PF pf;
-    const float2* twi = TWS ? tw + Plan<L, false, 4>::TW_ELEMS : tw;
+    const float2* twi = TWS ? tw + Plan<L, false, ZPlan<L>::RB>::TW_ELEMS : tw;
     fft_to_regs<L, B, NT, true, 3, false, true, false, false, TWS>(tm, smem, ld, tw, twstride, pf);
     kw();
     __syncthreads();

@@ -546,7 +546,8 @@ struct Z3Tma {
   // per-pass twiddles in smem, forward then inverse plan (fused plans; unfused
   // long pencils keep the global table so the CTA count per SM is unchanged)
   static constexpr bool TWS = ZPlan<L>::FUSE;
-  static constexpr int TWF = TWS ? Plan<L, false, 4>::TW_ELEMS : 0, TWI = TWS ? Plan<L, true, 4>::TW_ELEMS : 0;
+  static constexpr int TWF = TWS ? Plan<L, false, ZPlan<L>::RB>::TW_ELEMS : 0;
+  static constexpr int TWI = TWS ? Plan<L, true, ZPlan<L>::RB>::TW_ELEMS : 0;
   static constexpr size_t TWB = (size_t)(TWF + TWI) * 8;
 #ifndef GRACE_K3_PRE
 #define GRACE_K3_PRE 1  // prefetch the mirror pencils where 4 CTAs/SM still fit
@@ -588,8 +589,8 @@ __global__ void __launch_bounds__(Z3Tma<L>::NT, MINB)
   // per-pass twiddle tables in smem (the global table's lines would miss the
   // minimal L1 of a shared-memory-carveout kernel)
   if constexpr (Z::TWS) {
-    fill_pass_twiddles<Plan<L, false, 4>, L>(tws, tw, g.Lmax / L, threadIdx.x, NT);
-    fill_pass_twiddles<Plan<L, true, 4>, L>(tws + Z::TWF, tw, g.Lmax / L, threadIdx.x, NT);
+    fill_pass_twiddles<Plan<L, false, ZPlan<L>::RB>, L>(tws, tw, g.Lmax / L, threadIdx.x, NT);
+    fill_pass_twiddles<Plan<L, true, ZPlan<L>::RB>, L>(tws + Z::TWF, tw, g.Lmax / L, threadIdx.x, NT);
   }
   const float2* twp = Z::TWS ? tws : tw;  // the passes' twiddle source and stride
   const int twstr = Z::TWS ? 1 : g.Lmax / L;
@@ -772,7 +773,7 @@ __global__ void __launch_bounds__(NT, MINB) k5_inv_x(const float2* __restrict__ 
         return make_float2(S.x - wD.y, S.y + wD.x);            // S + i w^-k D
       }
     } ld{X1, tw, cstrideX, row0, nrows, g.pitch1, twpx, g.kb, g.blk1};
-    using PS = Pass<L, fft_npass(L, rb_for(false, 3)) - 1, false, B, NT, false, 3>;
+    using PS = Pass<L, fft_npass(L, rb_for(false, 3, L)) - 1, false, B, NT, false, 3>;
     const ThreadMap<L, B, NT, false> tm;
     PS ps;
     fft_to_regs<L, B, NT, false, 3, true, false, true, false>(tm, smem, ld, tw, g.Lmax / L, ps);
@@ -1216,7 +1217,7 @@ __global__ void __launch_bounds__(256, GRACE_K6_MINB) k6_llg(const float* __rest
 #define GRACE_MINB_Z1024 1  // 512^3 K3 20.7 -> 15.6 ms (2: 648 B of spills)
 #endif
 #ifndef GRACE_MINB_Z16
-#define GRACE_MINB_Z16 3  // scripts/sweep_z16.sh: film K3 0.084 -> 0.074 ms (4: 128 registers with spills; 2: 0.086 ms)
+#define GRACE_MINB_Z16 8  // radix-4x4 plan (GRACE_RB_Z16): film K3 0.0765 -> 0.064 ms at 8 CTAs/SM (6: 0.0686; radix 16 at 3: 0.0765)
 #endif
 #ifndef GRACE_EPT_Y
 #define GRACE_EPT_Y 16
