@@ -70,8 +70,13 @@ __host__ __device__ constexpr int fft_rmax(int L, int RB = 4) { return L <= 1 ? 
 #ifndef GRACE_RB_Z16
 #define GRACE_RB_Z16 2
 #endif
+#ifndef GRACE_RB_Z64
+#define GRACE_RB_Z64 4
+#endif
 __host__ __device__ constexpr int rb_for(bool colmode, int V, int L = 0) {
-  return (!colmode && V == 3) ? GRACE_RB_ROWS3 : ((colmode && V == 3 && L == 16) ? GRACE_RB_Z16 : 4);
+  return (!colmode && V == 3) ? GRACE_RB_ROWS3
+                              : ((colmode && V == 3 && L == 16) ? GRACE_RB_Z16
+                                                                : ((colmode && V == 3 && L == 64) ? GRACE_RB_Z64 : 4));
 }
 
 // x * exp(-+2 pi i K/16) for compile-time K (forward sign -, INV conjugates).

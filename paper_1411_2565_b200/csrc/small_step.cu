@@ -34,7 +34,7 @@ namespace grace {
 
 template <int LX, int PY, int C>
 struct Small {
-  static constexpr int NT = 128;
+  static constexpr int NT = ZPlan<PY>::NT;  // the chunk tiles' pencil plan sets the CTA size
   static constexpr int B = 16;   // kx columns per chunk
   static constexpr int RT = 16;  // component rows per x tile
   static constexpr int KX = LX + 1;
@@ -44,7 +44,7 @@ struct Small {
   using TX = TileIdx<LX, RT, false>;
   using TY = TileIdx<PY, B, true>;
   static_assert(!TY::PAD, "chunk tiles in the linear column layout");
-  static_assert(ZPlan<PY>::B == B && ZPlan<PY>::NT == NT, "pencil_conv plan of the chunk tiles");
+  static_assert(ZPlan<PY>::B == B && NT % RT == 0, "pencil_conv plan of the chunk tiles");
   static constexpr int YT = 3 * TY::ELEMS;   // float2 per chunk tile
   static constexpr int KSS = 6 * KYH * B;    // floats per chunk KS slice
   // dynamic smem for rmax rows per CTA (bytes)
@@ -64,7 +64,7 @@ struct SmallArgs {
 };
 
 template <int LX, int PY, int C>
-__global__ void __launch_bounds__(128, 1) k_small_step(Geom g, SmallArgs a) {
+__global__ void __launch_bounds__(Small<LX, PY, C>::NT, 1) k_small_step(Geom g, SmallArgs a) {
   using S = Small<LX, PY, C>;
   constexpr int NT = S::NT, B = S::B, RT = S::RT;
   using TX = typename S::TX;
