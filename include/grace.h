@@ -78,9 +78,12 @@ int grace_set_hext(grace_ctx *h, double hx, double hy, double hz);
 int grace_heff(grace_ctx *h, double *h_out);
 
 /* Advance n >= 0 explicit Euler steps of size dt > 0 seconds, entirely on the
- * device (CUDA-graph replay; no host round trip inside).  After the n steps one 8-byte
- * flag is read back: a non-finite M returns GRACE_ENONFINITE (the first failing step
- * and cell are kept for grace_last_nonfinite; M then holds non-finite values). */
+ * device (replay of CUDA graphs instantiated in grace_create: 16-step chunks, then
+ * single steps; no host round trip inside).  After the n steps one 8-byte flag is
+ * read back: a non-finite M returns GRACE_ENONFINITE (the first failing step and
+ * cell are kept for grace_last_nonfinite; M then holds non-finite values).  With
+ * GRACE_SMALL=1 an SP4-sized nz = 1 grid runs the whole call in one cluster kernel
+ * (small_step.cu; measured slower, opt-in). */
 int grace_step(grace_ctx *h, int n, double dt);
 
 /* Thread-local text of the last failure on this thread ("" if none). */
@@ -200,9 +203,15 @@ int grace_tensor_octant(int nx, int ny, int nz, double dx, double dy, double dz,
 /* Copy the fp32 spectral table KS [6][Kzh][Kyh][KSp] to the host (6*Kzh*Kyh*KSp floats). */
 int grace_kernel_spectrum(grace_ctx *h, float *out);
 
+/* The same table before its fp32 rounding: -Re FFT(circulant N) / (Px Py Pz) in fp64
+ * (S4-S5 of the setup, exactly as grace_create computes it), [6][Kzh][Kyh][KSp]
+ * doubles with Kzh, Kyh, KSp as grace_geometry reports them.  Standalone (no context);
+ * for checking the fp64 spectrum against the oracle at 1e-12. */
+int grace_kernel_spectrum_f64(int nx, int ny, int nz, double dx, double dy, double dz, double *out);
+
 /* Per-kernel timing.  grace_set_profiling(h, 1) makes grace_step launch the kernels
  * eagerly with a CUDA event pair around each; grace_kernel_times returns, per kernel
- * of the step (order K1, K2, K3, K4, K5 or K1, K2', K5), the summed milliseconds and
+ * of the step (order K1, K2, K3, K4, K5, K6 or K1, K2', K5, K6), the summed milliseconds and
  * the launch count since the last reset (reset = 1 clears after reading).  nk in:
  * capacity of ms[]/launches[]; out: number of kernels per step. */
 int grace_set_profiling(grace_ctx *h, int on);

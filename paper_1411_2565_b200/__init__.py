@@ -66,6 +66,7 @@ SIGNATURES = [
     ("grace_partition", _I, [_P, _PLL]),
     ("grace_set_geometry", _I, [_P, _P]),
     ("grace_step_adaptive", _I, [_P, _D, _PD, _D, ctypes.c_longlong, _PLL, _PLL]),
+    ("grace_kernel_spectrum_f64", _I, [_I, _I, _I, _D, _D, _D, _PD]),
     ("grace_set_m_f32", _I, [_P, _PF]),
     ("grace_get_m_f32", _I, [_P, _PF]),
 ]
@@ -309,6 +310,26 @@ def grace_kernel_spectrum(h):
     g = grace_geometry(h)
     out = np.empty((6, g["Kzh"], g["Kyh"], g["KSp"]), dtype=np.float32)
     _check(load().grace_kernel_spectrum(h, out.ctypes.data_as(_PF)))
+    return out
+
+
+def grace_kernel_spectrum_f64(nx, ny, nz, dx, dy, dz):
+    """fp64 folded spectrum [6][Kzh][Kyh][KSp] before the fp32 rounding (standalone)."""
+    def pad(n):
+        if n == 1:
+            return 1
+        p = 1
+        while p < 2 * n - 1:
+            p <<= 1
+        return p
+
+    px, py, pz = pad(nx), pad(ny), pad(nz)
+    kx = 1 if px == 1 else px // 2 + 1
+    kyh = 1 if py == 1 else py // 2 + 1
+    kzh = 1 if pz == 1 else pz // 2 + 1
+    ksp = (kx + 31) // 32 * 32
+    out = np.empty((6, kzh, kyh, ksp), dtype=np.float64)
+    _check(load().grace_kernel_spectrum_f64(nx, ny, nz, dx, dy, dz, _pd(out)))
     return out
 
 

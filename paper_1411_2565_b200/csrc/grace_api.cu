@@ -1487,6 +1487,28 @@ int grace_kernel_spectrum(grace_ctx* h, float* out) {
   return GRACE_OK;
 }
 
+int grace_kernel_spectrum_f64(int nx, int ny, int nz, double dx, double dy, double dz, double* out) {
+  if (!out) return fail(GRACE_EINVAL, "NULL argument");
+  if (nx < 1 || ny < 1 || nz < 1) return fail(GRACE_EINVAL, "cell counts must be >= 1");
+  if (!finite_pos(dx) || !finite_pos(dy) || !finite_pos(dz)) return fail(GRACE_EINVAL, "cell sizes must be > 0");
+  Geom g{};
+  int rc = make_geom(nx, ny, nz, dx, dy, dz, 1.0, 0.0, 0.0, &g);
+  if (rc) return rc;
+  const size_t n = (size_t)6 * g.Kzh * g.Kyh * g.KSp;
+  double* d = nullptr;
+  if (cudaMalloc(&d, sizeof(double) * n) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(GRACE_ENOMEM, "needs %zu bytes", sizeof(double) * n);
+  }
+  KsOut o{nullptr, 0, g.Kx, g.KSp, d};
+  size_t scratch = 0;
+  cudaError_t e = kernel_spectrum_device(g, dx, dy, dz, 1, &o, &scratch, 0);
+  if (e == cudaSuccess) e = cudaMemcpy(out, d, sizeof(double) * n, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(GRACE_ECUDA, "kernel spectrum: %s", cudaGetErrorString(e));
+  return GRACE_OK;
+}
+
 int grace_set_profiling(grace_ctx* h, int on) {
   if (!h) return fail(GRACE_EINVAL, "NULL context");
   h->profiling = on != 0;

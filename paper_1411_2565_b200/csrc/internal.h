@@ -143,6 +143,7 @@ cudaError_t tensor_octant_device(int nx, int ny, int nz, double dx, double dy, d
 struct KsOut {
   float* KS;
   int kx0, ncol, KSp;
+  double* KS64 = nullptr;  // optional: the fp64 values before rounding (same layout)
 };
 cudaError_t kernel_spectrum_device(const Geom& g, double dx, double dy, double dz, int nout, const KsOut* out,
                                    size_t* scratch_bytes, cudaStream_t st);

@@ -320,7 +320,9 @@ __global__ void k_fft64(double2* A, int L, int logL, long long nlines, long long
 // for the columns kx0 .. kx0 + ncol - 1 (one rank's kx block; pitch KSp, the
 // padding columns zero).  A is the compact spectrum [Pz][Py][Kw] of the columns
 // kxlo .. kxlo + Kw - 1.
-__global__ void k_fold(float* KSc, const double2* A, Geom g, int kx0, int ncol, int KSp, int kxlo, int Kw) {
+// KS64 (optional): the same values before the fp32 rounding (grace_kernel_spectrum_f64).
+__global__ void k_fold(float* KSc, double* KS64c, const double2* A, Geom g, int kx0, int ncol, int KSp, int kxlo,
+                       int Kw) {
   const long long tot = (long long)g.Kzh * g.Kyh * KSp;
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= tot) return;
@@ -328,12 +330,13 @@ __global__ void k_fold(float* KSc, const double2* A, Geom g, int kx0, int ncol, 
   const int ky = (int)((idx / KSp) % g.Kyh);
   const int kz = (int)(idx / ((long long)KSp * g.Kyh));
   const int kx = kx0 + col;
-  float v = 0.f;
+  double v = 0.0;
   if (col < ncol && kx < g.Kx) {
     const double P = (double)g.Px * (double)g.Py * (double)g.Pz;
-    v = (float)(-A[((long long)kz * g.Py + ky) * Kw + (kx - kxlo)].x / P);
+    v = -A[((long long)kz * g.Py + ky) * Kw + (kx - kxlo)].x / P;
   }
-  KSc[idx] = v;
+  if (KSc) KSc[idx] = (float)v;
+  if (KS64c) KS64c[idx] = v;
 }
 
 // Columns kxlo .. kxlo + Kw - 1 of the x-transformed chunk [npz][Py][Px] -> compact [Pz][Py][Kw].
@@ -448,8 +451,9 @@ cudaError_t kernel_spectrum_device(const Geom& g, double dx, double dy, double d
     if (e == cudaSuccess) e = fft64_axis(A, g.Pz, (long long)g.Py * Kw, (long long)g.Py * Kw, 0, (long long)g.Py * Kw, st);
     for (int o = 0; o < nout && e == cudaSuccess; ++o) {
       const long long kslen = (long long)g.Kzh * g.Kyh * out[o].KSp;
-      k_fold<<<(unsigned)cdiv(kslen, 256), 256, 0, st>>>(out[o].KS + c * kslen, A, g, out[o].kx0, out[o].ncol,
-                                                         out[o].KSp, kxlo, Kw);
+      k_fold<<<(unsigned)cdiv(kslen, 256), 256, 0, st>>>(out[o].KS ? out[o].KS + c * kslen : nullptr,
+                                                         out[o].KS64 ? out[o].KS64 + c * kslen : nullptr, A, g,
+                                                         out[o].kx0, out[o].ncol, out[o].KSp, kxlo, Kw);
       e = cudaGetLastError();
     }
   }

@@ -76,6 +76,28 @@ def test_kernel_spectrum_matches_oracle_rfftn(n, d):
     g.close()
 
 
+@pytest.mark.parametrize("n,d", [((7, 5, 3), (1e-9, 2e-9, 3e-9)), ((100, 25, 1), (5e-9, 5e-9, 3e-9)),
+                                 ((12, 1, 9), (1e-9, 1e-9, 1e-9)), ((33, 17, 20), (1e-9, 1.5e-9, 2e-9))])
+def test_kernel_spectrum_fp64_matches_oracle_1e12(n, d):
+    """the fp64 spectrum (before its fp32 rounding) against the oracle's
+    rfftn of its own bit-identical octant at the GPU padding, within 1e-12 of the
+    largest entry (different FFT algorithms: not bitwise)."""
+    K64 = pb.grace_kernel_spectrum_f64(*n, *d)
+    _, Kzh, Kyh, _ = K64.shape
+    g = pb.Grace(n, d, 8e5, 1.3e-11, 0.0, 0.5, GAMMA0)
+    geo = g.geometry
+    KS = pb.grace_kernel_spectrum(g.h)
+    g.close()
+    P = (geo["Pz"], geo["Py"], geo["Px"])
+    spec = kernel_spectrum(tensor_octant(*n, *d), P)
+    want = -spec.real[:, :Kzh, :Kyh, :] / (P[0] * P[1] * P[2])
+    got = K64[:, :, :, : geo["Kx"]]
+    scale = np.abs(want).max()
+    assert np.abs(got - want).max() <= 1e-12 * scale
+    # the fp32 table is this fp64 table rounded once
+    assert np.array_equal(KS[:, :, :, : geo["Kx"]], got.astype(np.float32))
+
+
 # ---------------------------------------------------------------- H_eff
 
 HEFF_CASES = [
