@@ -5,6 +5,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "fft_engine.cuh"
 
 namespace grace {
@@ -21,6 +23,24 @@ __device__ __forceinline__ void kmul_s(float2& a, float2& b, float2& c, const fl
   const float nxy = fy ? -p[cs] : p[cs];
   const float nxz = fz ? -p[2 * cs] : p[2 * cs];
   const float nyz = (fy != fz) ? -p[4 * cs] : p[4 * cs];
+  const float2 mx = a, my = b, mz = c;
+  a = make_float2(nxx * mx.x + nxy * my.x + nxz * mz.x, nxx * mx.y + nxy * my.y + nxz * mz.y);
+  b = make_float2(nxy * mx.x + nyy * my.x + nyz * mz.x, nxy * mx.y + nyy * my.y + nyz * mz.y);
+  c = make_float2(nxz * mx.x + nyz * my.x + nzz * mz.x, nxz * mx.y + nyz * my.y + nzz * mz.y);
+}
+
+// The same multiply with the fold signs known at compile time (the fused
+// pencils' last-pass element index decides the pencil-axis fold per register;
+// the other axis' fold is uniform per call): the negations fold into the FMAs.
+template <bool FY, bool FZ>
+__device__ __forceinline__ void kmul_c(float2& a, float2& b, float2& c, const float* kss, int KH, int B, int kf,
+                                       int bcol) {
+  const int cs = KH * B;
+  const float* p = kss + kf * B + bcol;
+  const float nxx = p[0], nyy = p[3 * cs], nzz = p[5 * cs];
+  const float nxy = FY ? -p[cs] : p[cs];
+  const float nxz = FZ ? -p[2 * cs] : p[2 * cs];
+  const float nyz = (FY != FZ) ? -p[4 * cs] : p[4 * cs];
   const float2 mx = a, my = b, mz = c;
   a = make_float2(nxx * mx.x + nxy * my.x + nxz * mz.x, nxx * mx.y + nxy * my.y + nxz * mz.y);
   b = make_float2(nxy * mx.x + nyy * my.x + nyz * mz.x, nxy * mx.y + nyy * my.y + nyz * mz.y);
@@ -119,18 +139,34 @@ __device__ __forceinline__ void pencil_conv(float2* smem, const LD& ld, const ST
     kw();
     __syncthreads();
     PI pi;
+    // The last forward pass leaves element k = jb + r NS in register r (jb < NS =
+    // L / R), so k > L/2 exactly for r > R/2, and for r = R/2 except at k = L/2,
+    // the Nyquist index, where folding maps kf to itself and the odd components
+    // of the spectrum vanish (their circulant sequences are odd): the fold of the
+    // pencil axis is r >= R/2, known at compile time once the loop is unrolled.
+    static_assert(PF::NS == PF::TPC || PF::NS == 1, "fused last pass: one element per register and NS");
+    auto mul = [&](auto fo_tag) {
+      constexpr bool FO = decltype(fo_tag)::value;
 #pragma unroll
-    for (int r = 0; r < PF::R; ++r) {
-      const int k = PF::sb(tm) + PF::C2(0, r);
-      bool fy, fz;
-      int kf;
-      flags(k, fy, fz, kf);
-      float2 a = pf.v[0][0][r], b = pf.v[0][1][r], c = pf.v[0][2][r];
-      kmul_s(a, b, c, kss, KH, B, kf, tm.b, fy, fz);
-      pi.v[0][0][r] = a;
-      pi.v[0][1][r] = b;
-      pi.v[0][2][r] = c;
-    }
+      for (int r = 0; r < PF::R; ++r) {
+        const int k = PF::sb(tm) + PF::C2(0, r);
+        const bool fa = r >= PF::R / 2;
+        const int kf = fa ? L - k : k;
+        float2 a = pf.v[0][0][r], b = pf.v[0][1][r], c = pf.v[0][2][r];
+        if (fold_is_y) {
+          if (fa) kmul_c<true, false>(a, b, c, kss, KH, B, kf, tm.b);
+          else kmul_c<false, false>(a, b, c, kss, KH, B, kf, tm.b);
+        } else {
+          if (fa) kmul_c<FO, true>(a, b, c, kss, KH, B, kf, tm.b);
+          else kmul_c<FO, false>(a, b, c, kss, KH, B, kf, tm.b);
+        }
+        pi.v[0][0][r] = a;
+        pi.v[0][1][r] = b;
+        pi.v[0][2][r] = c;
+      }
+    };
+    if (!fold_is_y && k_other > (P_other >> 1)) mul(std::true_type{});
+    else mul(std::false_type{});
     fft_from_regs<L, B, NT, true, 3, true, true, true, TWS>(tm, smem, st, twi, twstride, pi);
   } else {
     using T = TileIdx<L, B, true>;
