@@ -150,6 +150,7 @@ struct Rank {
   TmapBlob k2map{}, k4map{};
   bool tma3 = false;                   // TMA descriptors of the K3 pencils and KS slices built
   TmapBlob k3x{}, k3k{};
+  float2* tw3 = nullptr;               // K3's twiddle tables in their smem layout
 };
 
 struct grace_ctx {
@@ -424,7 +425,7 @@ struct grace_ctx {
         CE(launch_k2(rk.g, rk.A, rk.X2, tw, s, rk.tma ? &rk.k2map : nullptr));
         rec(3);
         rec(4);
-        CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s, rk.tma3 ? &rk.k3x : nullptr, rk.tma3 ? &rk.k3k : nullptr));
+        CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s, rk.tma3 ? &rk.k3x : nullptr, rk.tma3 ? &rk.k3k : nullptr, rk.tw3));
         rec(5);
         rec(6);
         CE(launch_k4(rk.g, rk.X2, rk.A, tw, s, rk.tma ? &rk.k4map : nullptr));
@@ -439,7 +440,7 @@ struct grace_ctx {
       for (auto& rk : ranks) {
         if (rk.g.Kc > 0) {
           CE(launch_k2(rk.g, rk.B, rk.X2, tw, s, rk.tma ? &rk.k2map : nullptr));
-          CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s, rk.tma3 ? &rk.k3x : nullptr, rk.tma3 ? &rk.k3k : nullptr));
+          CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s, rk.tma3 ? &rk.k3x : nullptr, rk.tma3 ? &rk.k3k : nullptr, rk.tw3));
           CE(launch_k4(p2p_geom(rk, peerA), rk.X2, rk.B, tw, s, rk.tma ? &rk.k4map : nullptr));
         }
       }
@@ -451,7 +452,7 @@ struct grace_ctx {
       for (auto& rk : ranks) {
         if (rk.g.Kc > 0) {
           CE(launch_k2(rk.g, rk.B, rk.X2, tw, s, rk.tma ? &rk.k2map : nullptr));
-          CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s, rk.tma3 ? &rk.k3x : nullptr, rk.tma3 ? &rk.k3k : nullptr));
+          CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s, rk.tma3 ? &rk.k3x : nullptr, rk.tma3 ? &rk.k3k : nullptr, rk.tw3));
           CE(launch_k4(rk.g, rk.X2, rk.B, tw, s, rk.tma ? &rk.k4map : nullptr));
         }
       }
@@ -480,7 +481,7 @@ struct grace_ctx {
     set_pdl_blocked(false);
     for (auto& rk : ranks)
       if (rk.g.Kc > 0)
-        CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s, rk.tma3 ? &rk.k3x : nullptr, rk.tma3 ? &rk.k3k : nullptr));
+        CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s, rk.tma3 ? &rk.k3x : nullptr, rk.tma3 ? &rk.k3k : nullptr, rk.tw3));
     // K4(q) | C2(q) on cs while K4(q+1); k5_stage consumes component q once C2(q) landed
     for (int q = 0; q < 3; ++q) {
       for (auto& rk : ranks)
@@ -604,7 +605,7 @@ struct grace_ctx {
     for (auto e : ev) cudaEventDestroy(e);
     for (auto& rk : ranks) {
       void* ptrs[] = {rk.M[0], rk.M[1], rk.A,   rk.B,    rk.X2,  rk.KS,   rk.Hlo, rk.Hhi,
-                      rk.prm,  rk.flag, rk.red, rk.Hbuf, rk.Hd,  rk.dred, rk.F,   rk.mask, rk.aerr};
+                      rk.prm,  rk.flag, rk.red, rk.Hbuf, rk.Hd,  rk.dred, rk.F,   rk.mask, rk.aerr, rk.tw3};
       for (void* p : ptrs)
         if (p) cudaFree(p);
     }
@@ -818,6 +819,8 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
     return bail(fail(GRACE_ENOMEM, "tensor setup needs %zu bytes of fp64 scratch", scratch));
   }
   if (e == cudaSuccess) e = launch_twiddles(h->tw, g0.Lmax, s);
+  for (auto& rk : h->ranks)
+    if (e == cudaSuccess && rk.tma3) e = make_k3_twiddles(rk.g, h->tw, &rk.tw3, s);
   for (auto& rk : h->ranks) {
     if (e == cudaSuccess) e = launch_fill_uniform_x(rk.M[0], rk.Nl, (float)Ms, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(rk.flag, 0xff, 2 * sizeof(unsigned long long), s);

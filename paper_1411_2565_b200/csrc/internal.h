@@ -86,8 +86,11 @@ cudaError_t launch_k2(const Geom& g, const float2* X1, float2* X2, const float2*
 // K3 tensor maps (X2 pencils, KS slices) for the TMA-fed kernel; cudaErrorNotSupported
 // where K3 takes the LDG kernel (unfused long pencils, short L, nz == 1).
 cudaError_t make_k3_tmaps(const Geom& g, const float2* X2, const float* KS, TmapBlob* xmap, TmapBlob* kmap);
+// tw3: the TMA K3's twiddle tables in their smem layout (make_k3_twiddles; nullptr:
+// each CTA builds them from tw).
 cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* tw, cudaStream_t st,
-                      const TmapBlob* xmap = nullptr, const TmapBlob* kmap = nullptr);
+                      const TmapBlob* xmap = nullptr, const TmapBlob* kmap = nullptr, const float2* tw3 = nullptr);
+cudaError_t make_k3_twiddles(const Geom& g, const float2* tw, float2** out, cudaStream_t st);
 cudaError_t launch_k4(const Geom& g, const float2* X2, float2* X1, const float2* tw, cudaStream_t st,
                       const TmapBlob* tmap = nullptr);
 cudaError_t launch_k2f(const Geom& g, float2* X1, const float* KS, const float2* tw, cudaStream_t st);

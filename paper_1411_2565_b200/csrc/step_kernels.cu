@@ -79,6 +79,17 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// expect tx bytes on the barrier's current phase without arriving
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
                                             int c3) {
   asm volatile(
@@ -561,7 +572,7 @@ struct Z3Tma {
 template <int L, int MINB>
 __global__ void __launch_bounds__(Z3Tma<L>::NT, MINB)
     k3_z_tma(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-             float2* __restrict__ X2, const float2* __restrict__ tw, Geom g) {
+             float2* __restrict__ X2, const float2* __restrict__ tw, const float2* __restrict__ tw3, Geom g) {
   using Z = Z3Tma<L>;
   constexpr int B = Z::B, NT = Z::NT, H = Z::H;
   constexpr unsigned TXP = 3u * H * B * 8;  // bytes of one pencil set
@@ -589,8 +600,15 @@ __global__ void __launch_bounds__(Z3Tma<L>::NT, MINB)
   // per-pass twiddle tables in smem (the global table's lines would miss the
   // minimal L1 of a shared-memory-carveout kernel)
   if constexpr (Z::TWS) {
-    fill_pass_twiddles<Plan<L, false, ZPlan<L>::RB>, L>(tws, tw, g.Lmax / L, threadIdx.x, NT);
-    fill_pass_twiddles<Plan<L, true, ZPlan<L>::RB>, L>(tws + Z::TWF, tw, g.Lmax / L, threadIdx.x, NT);
+    if (tw3 != nullptr) {  // the tables precomputed in this layout (k3_twiddle_tables): one bulk copy
+      if (threadIdx.x == 0) {
+        mbar_expect_tx_only(bar + 1, (unsigned)Z::TWB);
+        bulk_load(tws, tw3, (unsigned)Z::TWB, bar + 1);
+      }
+    } else {
+      fill_pass_twiddles<Plan<L, false, ZPlan<L>::RB>, L>(tws, tw, g.Lmax / L, threadIdx.x, NT);
+      fill_pass_twiddles<Plan<L, true, ZPlan<L>::RB>, L>(tws + Z::TWF, tw, g.Lmax / L, threadIdx.x, NT);
+    }
   }
   const float2* twp = Z::TWS ? tws : tw;  // the passes' twiddle source and stride
   const int twstr = Z::TWS ? 1 : g.Lmax / L;
@@ -812,12 +830,6 @@ __global__ void __launch_bounds__(NT, MINB) k5_inv_x(const float2* __restrict__ 
 //              -> C2R pre-process -> H_demag rows (nx floats)
 // Requires nx % 4 == 0 (16-byte row copies); the launchers fall back to the
 // non-persistent kernels otherwise.
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
 
 // K1 loader: packed pairs z[i] = (x[2i], x[2i+1]) of raw row b (nh = nx/2 of them).
 template <int ROWS, bool GUARD>
@@ -1608,9 +1620,39 @@ cudaError_t make_k3_tmaps(const Geom& g, const float2* X2, const float* KS, Tmap
 #undef CASE
 }
 
+// The TMA K3's per-pass twiddle tables in its shared-memory layout, built once
+// per context so each CTA brings them in with one bulk copy.
+template <int L>
+__global__ void k_k3_twiddles(float2* dst, const float2* tw, int twstride) {
+  constexpr int RB = ZPlan<L>::RB;
+  fill_pass_twiddles<Plan<L, false, RB>, L>(dst, tw, twstride, threadIdx.x, blockDim.x);
+  fill_pass_twiddles<Plan<L, true, RB>, L>(dst + Plan<L, false, RB>::TW_ELEMS, tw, twstride, threadIdx.x, blockDim.x);
+}
+
+template <int L>
+static cudaError_t k3_tables(const Geom& g, const float2* tw, float2** out, cudaStream_t st) {
+  *out = nullptr;
+  if constexpr (k3_tma_ok<L>()) {
+    if constexpr (Z3Tma<L>::TWS && Z3Tma<L>::TWB > 0) {
+      GRACE_TRY(cudaMalloc(out, Z3Tma<L>::TWB));
+      k_k3_twiddles<L><<<1, 256, 0, st>>>(*out, tw, g.Lmax / L);
+      return cudaGetLastError();
+    }
+  }
+  return cudaSuccess;
+}
+
+cudaError_t make_k3_twiddles(const Geom& g, const float2* tw, float2** out, cudaStream_t st) {
+  *out = nullptr;
+  if (g.Pz < 2 || fused_y_path(g)) return cudaSuccess;
+#define CASE(v) case v: return (v >= 2 && v <= 1024) ? k3_tables<(v >= 2 && v <= 1024 ? v : 2)>(g, tw, out, st) : cudaSuccess;
+  GRACE_L_SWITCH(g.Pz, CASE)
+#undef CASE
+}
+
 template <int L>
 static cudaError_t k3_launch(const Geom& g, float2* X2, const float* KS, const float2* tw, cudaStream_t st,
-                             const TmapBlob* xmap, const TmapBlob* kmap) {
+                             const TmapBlob* xmap, const TmapBlob* kmap, const float2* tw3) {
   using C = ZCfg<L>;
   if constexpr (k3_tma_ok<L>()) {
     if (xmap != nullptr && kmap != nullptr && !getenv("GRACE_NO_K3_TMA")) {
@@ -1622,7 +1664,7 @@ static cudaError_t k3_launch(const Geom& g, float2* X2, const float* KS, const f
       cudaError_t e = prep(kern, Z::SMEM);
       if (e != cudaSuccess) return e;
       dim3 grid((g.Kc + Z::B - 1) / Z::B, g.Kyh);
-      GRACE_TRY(launch_k(4, kern, grid, Z::NT, Z::SMEM, st, xm, km, X2, tw, g));
+      GRACE_TRY(launch_k(4, kern, grid, Z::NT, Z::SMEM, st, xm, km, X2, tw, tw3, g));
       return cudaGetLastError();
     }
   }
@@ -1635,13 +1677,13 @@ static cudaError_t k3_launch(const Geom& g, float2* X2, const float* KS, const f
 }
 
 cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* tw, cudaStream_t st,
-                      const TmapBlob* xmap, const TmapBlob* kmap) {
+                      const TmapBlob* xmap, const TmapBlob* kmap, const float2* tw3) {
   if (g.Pz == 1) {
     dim3 grid((g.Kc + 127) / 128, g.Py);
     GRACE_TRY(launch_k(4, k_mul_plane, grid, 128, 0, st, X2, KS, g));
     return cudaGetLastError();
   }
-#define CASE(v) case v: return (v >= 2 && v <= 1024) ? k3_launch<(v >= 2 && v <= 1024 ? v : 2)>(g, X2, KS, tw, st, xmap, kmap) : cudaErrorInvalidValue;
+#define CASE(v) case v: return (v >= 2 && v <= 1024) ? k3_launch<(v >= 2 && v <= 1024 ? v : 2)>(g, X2, KS, tw, st, xmap, kmap, tw3) : cudaErrorInvalidValue;
   GRACE_L_SWITCH(g.Pz, CASE)
 #undef CASE
 }
