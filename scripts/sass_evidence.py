@@ -36,7 +36,7 @@ print("# SASS evidence (`cuobjdump -sass paper_1411_2565_b200/libgrace.so`, stat
 print("sm_100a: TMA tensor loads are `UTMALDG`, 1-D bulk copies `UBLKCP`, mbarrier waits `SYNCS*`, "
       "programmatic dependent launch `ACQBULK` (griddepcontrol.wait) / `PREEXIT` (launch_dependents); `LDGSTS` is "
       "cp.async (K3's KS slice).  No tensor-core instructions by design (no dense contraction on this path).  "
-      "Rows: the slab step's kernels (K1 = k_x_bulk<1024, true>, K2 = k_y_stage<2048>, K3 = k3_z<64, ...>, "
+      "Rows: the slab step's kernels (K1 = k_x_bulk<1024, true>, K2 = k_y_stage<2048>, K3 = k3_z_tma<64, 4>, "
       "K4 = k_y_tma<2048, 4, true>, K5 = k_x_bulk<1024, false>, K6 = k6_llg), SP4's K2', the tensor setup and the "
       "diagnostics reduction.\n")
 print("| kernel | " + " | ".join(WATCH) + " |")
