@@ -53,7 +53,7 @@ def algorithmic_bytes(geo, names):
     x2 = 3 * nz * Py * Kx * 8
     m = 12 * N
     ks = 6 * Kzh * Kyh * Kx * 4 if geo["Pz"] > 1 else 4 * Kyh * Kx * 4
-    b = {"K1": m + x1, "K2f": 2 * x1 + ks, "K2": x1 + x2, "K3": 2 * x2 + ks, "K4": x2 + x1,
+    b = {"K1": m + x1, "K2f": 2 * x1 + ks, "KP": 2 * x1 + ks, "K2": x1 + x2, "K3": 2 * x2 + ks, "K4": x2 + x1,
          "K5": x1 + m, "K6": 3 * m}
     return {k: b[k] for k in names}
 
@@ -62,14 +62,22 @@ def design_step_bytes(geo):
     """SURVEY §8(d)'s per-step compulsory bytes (349 B/cell at the slab): the
     same FFT stages with the C2R and the LLG update in one pass (x1 + 2m)."""
     nx, ny, nz = geo["nx"], geo["ny"], geo["nz"]
-    names = KERNEL_NAMES[geo["kernels"]]
+    names = kernel_names(geo)
     ab = algorithmic_bytes(geo, names)
     return sum(ab.values()) - 2 * 12 * nx * ny * nz
 
 
-STEP_DESC = {"K1": "K1 x-R2C", "K2": "K2 y-FFT (TMA)", "K2f": "K2' y-FFT*N*iFFT", "K3": "K3 z-FFT*N*iFFT",
+STEP_DESC = {"K1": "K1 x-R2C", "K2": "K2 y-FFT (TMA)", "K2f": "K2' y-FFT*N*iFFT",
+             "KP": "KP plane-fused y-FFT*z-FFT*N*iFFT*iFFT", "K3": "K3 z-FFT*N*iFFT",
              "K4": "K4 y-iFFT (TMA)", "K5": "K5 x-C2R -> H_demag", "K6": "K6 exch+anis+Zeeman+LLG+Euler stencil"}
 KERNEL_NAMES = {4: ["K1", "K2f", "K5", "K6"], 6: ["K1", "K2", "K3", "K4", "K5", "K6"]}
+
+
+def kernel_names(geo):
+    """The step's kernels: four with nz = 1 (K2') or on the thin-film plane path (KP), else six."""
+    if geo["kernels"] == 4 and geo["Pz"] > 1:
+        return ["K1", "KP", "K5", "K6"]
+    return KERNEL_NAMES[geo["kernels"]]
 
 
 def read_peaks():
@@ -265,7 +273,7 @@ def run_own(args, w):
     pb.grace_set_m_device(g.h, M0.data_ptr())
     g.set_hext(w.hext)
     geo = g.geometry
-    names = KERNEL_NAMES[geo["kernels"]]
+    names = kernel_names(geo)
     g.step(args.warmup, w.dt)
     # Timed region 1 (the headline): K steps of the product path, CUDA-graph
     # replay with programmatic dependent launch, CUDA events on the library stream.
@@ -326,8 +334,10 @@ def run_own(args, w):
                 "step_bytes_design": design_bytes, "step_bytes_moved": step_bytes,
                 "step_frac": design_bytes / div / (ms_step / 1e3) / 1e9 / peak,
                 "step_frac_moved": step_bytes / div / (ms_step / 1e3) / 1e9 / peak,
-                "step_frac_note": "step_frac: SURVEY 8(d) design bytes (349 B/cell at the slab) / ms_step / peak; "
-                                  "step_frac_moved: the bytes this build's kernels move (K5/K6 split: +24 B/cell)"}
+                "step_frac_note": "step_frac: the compulsory bytes of this step's design (SURVEY 8(d): 349 B/cell "
+                                  "at the slab; the KP plane path of thin films: K1 + KP + one C2R+LLG pass) "
+                                  "/ ms_step / peak; step_frac_moved: the bytes this build's kernels move "
+                                  "(K5/K6 split: +24 B/cell)"}
 
     # e2e through the public API with pinned host buffers
     e2e = None

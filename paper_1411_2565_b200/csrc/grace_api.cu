@@ -135,6 +135,7 @@ struct Rank {
   float2* B = nullptr;   // dist: R1 / S2 [P][3][nzl][ny][Kb]
   float2* X2 = nullptr;  // [3][nz][Py][pitch2] (absent on the fused nz = 1 path)
   float* KS = nullptr;
+  float* KSP = nullptr;  // plane-ordered KS [kx][6][Kzh][Kyh] (KP path only)
   float* Hlo = nullptr;  // halo planes [3][ny][nx]
   float* Hhi = nullptr;
   StepParams* prm = nullptr;
@@ -169,6 +170,7 @@ struct grace_ctx {
   double nmag = 0;  // magnetic cells of the whole grid under the geometry mask (0: no mask)
   int cur = 0;
   bool fused = false;
+  bool plane = false;  // KP replaces K2..K4 (thin films, single GPU)
   Geom g0{};  // global geometry
   std::vector<Rank> ranks;
   float2* tw = nullptr;
@@ -420,6 +422,10 @@ struct grace_ctx {
         rec(2);
         CE(launch_k2f(rk.g, rk.A, rk.KS, tw, s));
         rec(3);
+      } else if (plane) {
+        rec(2);
+        CE(launch_kplane(rk.g, rk.A, rk.KSP, tw, s));
+        rec(3);
       } else {
         rec(2);
         CE(launch_k2(rk.g, rk.A, rk.X2, tw, s, rk.tma ? &rk.k2map : nullptr));
@@ -605,7 +611,7 @@ struct grace_ctx {
     for (auto e : ev) cudaEventDestroy(e);
     for (auto& rk : ranks) {
       void* ptrs[] = {rk.M[0], rk.M[1], rk.A,   rk.B,    rk.X2,  rk.KS,   rk.Hlo, rk.Hhi,
-                      rk.prm,  rk.flag, rk.red, rk.Hbuf, rk.Hd,  rk.dred, rk.F,   rk.mask, rk.aerr, rk.tw3};
+                      rk.prm,  rk.flag, rk.red, rk.Hbuf, rk.Hd,  rk.dred, rk.F,   rk.mask, rk.aerr, rk.tw3, rk.KSP};
       for (void* p : ptrs)
         if (p) cudaFree(p);
     }
@@ -722,6 +728,8 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
   h->P = P;
   h->myrank = first_rank;
   h->g0 = g0;
+  h->g0.plane = mode == grace_ctx::kSingle && !fused_y_path(g0) && plane_ok(g0);
+  h->plane = h->g0.plane;
   h->dx = dx;
   h->dy = dy;
   h->dz = dz;
@@ -767,17 +775,18 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
   for (int i = 0; i < nranks_here; ++i) {
     Rank& rk = h->ranks[i];
     rk.r = first_rank + i;
-    rk.g = rank_geom(g0, rk.r, P, dlay);
+    rk.g = rank_geom(h->g0, rk.r, P, dlay);
     const Geom& g = rk.g;
     rk.Nl = (long long)g.nzl * ny * nx;
     const size_t mb = sizeof(float) * 3 * (size_t)rk.Nl;
     const size_t ab = !dlay ? sizeof(float2) * 3 * (size_t)nz * ny * g.Kxp : sizeof(float2) * (size_t)P * g.blk1;
-    const size_t x2 = h->fused ? 0 : sizeof(float2) * 3 * (size_t)nz * g.Py * g.pitch2;
+    const size_t x2 = (h->fused || h->plane) ? 0 : sizeof(float2) * 3 * (size_t)nz * g.Py * g.pitch2;
     const size_t ks = sizeof(float) * 6 * (size_t)g.Kzh * g.Kyh * g.KSp;
     const size_t hb = sizeof(float) * 3 * (size_t)ny * nx;
     if ((rc = h->alloc((void**)&rk.M[0], mb)) || (rc = h->alloc((void**)&rk.M[1], mb)) ||
         (rc = h->alloc((void**)&rk.A, ab)) || (dlay && (rc = h->alloc((void**)&rk.B, ab))) ||
         (x2 && (rc = h->alloc((void**)&rk.X2, x2))) || (rc = h->alloc((void**)&rk.KS, ks)) ||
+        (h->plane && (rc = h->alloc((void**)&rk.KSP, sizeof(float) * plane_ks_floats(g)))) ||
         (g.has_lo && (rc = h->alloc((void**)&rk.Hlo, hb))) || (g.has_hi && (rc = h->alloc((void**)&rk.Hhi, hb))) ||
         (rc = h->alloc((void**)&rk.prm, sizeof(StepParams))) ||
         (rc = h->alloc((void**)&rk.flag, 3 * sizeof(unsigned long long))) ||
@@ -791,7 +800,7 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
     for (auto& rk : h->ranks) h->pipe = h->pipe && comp_split_ok(rk.g);
   }
   // TMA descriptors for the y-pencil kernels (K2 reads the x-row layout, K4 reads X2)
-  if (!h->fused && !getenv("GRACE_NO_TMA"))
+  if (!h->fused && !h->plane && !getenv("GRACE_NO_TMA"))
     for (auto& rk : h->ranks) {
       rk.tma = make_ky_tmaps(rk.g, dlay ? rk.B : rk.A, rk.X2, &rk.k2map, &rk.k4map) == cudaSuccess;
       rk.tma3 = rk.X2 && make_k3_tmaps(rk.g, rk.X2, rk.KS, &rk.k3x, &rk.k3k) == cudaSuccess;
@@ -819,6 +828,8 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
     return bail(fail(GRACE_ENOMEM, "tensor setup needs %zu bytes of fp64 scratch", scratch));
   }
   if (e == cudaSuccess) e = launch_twiddles(h->tw, g0.Lmax, s);
+  for (auto& rk : h->ranks)
+    if (e == cudaSuccess && rk.KSP) e = launch_plane_ks(rk.g, rk.KSP, rk.KS, s);
   for (auto& rk : h->ranks)
     if (e == cudaSuccess && rk.tma3) e = make_k3_twiddles(rk.g, h->tw, &rk.tw3, s);
   for (auto& rk : h->ranks) {

@@ -62,6 +62,7 @@ struct Geom {
   // the other ranks' buffers on the virtual path.  0: off.
   int p2p, rank;
   float2* peer[8];
+  int plane;           // KP plane-fused y.z.y pass replaces K2..K4 (single GPU, thin films)
   float cx, cy, cz; // exchange 2A/(mu0 Ms^2 d^2) per axis (0 for a singleton axis)
   float ck;         // anisotropy 2Ku/(mu0 Ms^2)
   float Ms;
@@ -102,7 +103,14 @@ cudaError_t launch_k5(const Geom& g, const float2* X1, float* Hd, const float2* 
 cudaError_t launch_k6(const Geom& g, int mode, const float* Hd, const float* M, float* Mn, float* Hout,
                       const StepParams* prm, unsigned long long* flag, cudaStream_t st, const float* Hlo,
                       const float* Hhi, unsigned* aerr = nullptr);
-bool fused_y_path(const Geom& g);  // nz == 1 and the y-pencils of 3 components fit one CTA
+bool fused_y_path(const Geom& g);
+// KP (plane-fused y.z.y, nz >= 2 with Pz <= 16, single GPU): in place on X1 [3][nz][ny][pitch1]
+// with KSP, the plane-ordered spectrum [kx][6][Kzh][Kyh] (plane_ks_floats floats, filled
+// from KS by launch_plane_ks).
+bool plane_ok(const Geom& g);
+size_t plane_ks_floats(const Geom& g);
+cudaError_t launch_plane_ks(const Geom& g, float* KSP, const float* KS, cudaStream_t st);
+cudaError_t launch_kplane(const Geom& g, float2* X1, const float* KSP, const float2* tw, cudaStream_t st);  // nz == 1 and the y-pencils of 3 components fit one CTA
 bool comp_split_ok(const Geom& g); // K1 .. K5 can run per component (bulk-copy x kernels)
 bool p2p_ok(const Geom& g);        // K1 / K4 can store into peers' buffers (bulk-copy K1, TMA K4)
 void set_pdl_blocked(bool b);      // this thread's next launches without programmatic dependent launch

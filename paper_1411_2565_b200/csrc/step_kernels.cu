@@ -738,6 +738,160 @@ __global__ void __launch_bounds__(NT, MINB) k2f_y_fused(float2* __restrict__ X1,
 }
 
 // ---------------------------------------------------------------------------
+// KP: plane-fused y.z.y pass for thin films.  One CTA holds a
+// whole kx plane of the three components in shared memory and runs, between one
+// read and one write of its X1 column, the forward y-FFT, the z-FFT, H~ = KS.M~
+// (P:L55's convolution theorem), the inverse z-FFT and the inverse y-FFT, so
+// K2, K3 and K4 (and X2) drop out of the step: 24 + 24 B/cell of X1 plus the
+// plane's KS slice instead of K2..K4's ~267 B/cell.  The plane of the y spectra
+// is Py x 3 HZ complex (HZ = Pz/2 >= nz z rows, the rows z >= nz zero), which
+// fits the 227 KB of one CTA for Pz <= 16 (thin films; Py <= 1024 at Pz = 16).
+//   y stage : rows-mode tile, column b = c HZ + z (component c, z row), LY = Py
+//             points with the ny < LY/2 nonzero inputs read straight from X1
+//             (HIN); outputs in the tile's linear layout (b, ky) at b ROWS + ky.
+//   z stage : pencil ky, two adjacent lanes per pencil, lane h = the kz = 2m + h
+//             half of the pruned Pz-point transform: with a[n] = 0 for n >= Pz/2,
+//             M~[2m + h] = DFT_{Pz/2}(a[n] w_Pz^{hn})[m], and the inverse
+//             keeping n < nz is the sum over h of w_Pz^{-hn} IDFT_{Pz/2}(H~_h)[n]
+//             (one shuffle).  In registers, no shared-memory passes; consecutive
+//             pencils on consecutive lanes read consecutive words.
+//   KS      : the plane-ordered copy KSP [kx][6][Kzh][Kyh] (contiguous per kx,
+//             prefetched into L2 by one bulk prefetch before the PDL wait).
+template <int PZ>
+struct PlaneCfgZ {
+  static_assert(PZ == 4 || PZ == 8 || PZ == 16, "plane path: Pz in {4, 8, 16}");
+  static constexpr int HZ = PZ / 2;
+  static constexpr int NCOL = 3 * HZ;
+};
+#ifndef GRACE_PLANE_NT
+#define GRACE_PLANE_NT 768
+#endif
+template <int LY, int PZ>
+struct PlaneCfg : PlaneCfgZ<PZ> {
+  using Z = PlaneCfgZ<PZ>;
+  static constexpr int TPC0 = GRACE_PLANE_NT / Z::NCOL;
+  static constexpr int TPC1 = TPC0 >= 128 ? 128 : (TPC0 >= 64 ? 64 : (TPC0 >= 32 ? 32 : 16));
+  static constexpr int TPC = TPC1 < LY / 16 ? TPC1 : LY / 16;  // <= the first pass' butterflies per column
+  static constexpr int NT = Z::NCOL * TPC;
+  using T = TileIdx<LY, Z::NCOL, false>;
+  static constexpr size_t SMEM = (size_t)T::ELEMS * sizeof(float2);
+  static_assert(NT % 32 == 0 && (2 * LY) % 32 == 0, "whole warps in the z stage");
+};
+__host__ __device__ constexpr long long plane_ks_stride(int Kzh, int Kyh) { return ((6LL * Kzh * Kyh + 31) / 32) * 32; }
+
+// a[N] *= w_PZ^{+-N} for N < HZ (compile-time twiddles)
+template <bool INV, int PZ, int HZ, int N = 0>
+__device__ __forceinline__ void tw_rows(float2* a) {
+  if constexpr (N < HZ) {
+    a[N] = tw16_mul<INV, N * (16 / PZ)>(a[N]);
+    tw_rows<INV, PZ, HZ, N + 1>(a);
+  }
+}
+
+template <int LY, int PZ>
+__global__ void __launch_bounds__(PlaneCfg<LY, PZ>::NT, 1)
+    k_plane(float2* __restrict__ X1, const float* __restrict__ KSP, const float2* __restrict__ tw, Geom g) {
+  using C = PlaneCfg<LY, PZ>;
+  using T = typename C::T;
+  constexpr int HZ = C::HZ, NCOL = C::NCOL, NT = C::NT;
+  extern __shared__ float2 smem[];
+  const int kx = blockIdx.x;
+  const long long kss = plane_ks_stride(g.Kzh, g.Kyh);
+  const float* ks = KSP + kx * kss;
+  pdl_trigger();
+  pdl_wait();
+  // the KS slice into L2 while the y stage runs.  After the PDL wait: issued
+  // before it (the slice is constant), the graph-replayed step read garbage
+  // (measured: non-finite M after one step; eager launches were correct).
+  if (threadIdx.x == 0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(ks), "r"((unsigned)(kss * 4)) : "memory");
+  const int nz = g.nz, ny = g.ny;
+  const size_t ps = g.pitch1;
+  struct Ld {  // column b = c HZ + z of X1 [3][nz][ny][pitch1] at this kx; rows y >= ny and z >= nz are zero
+    __device__ static constexpr bool kSmem() { return false; }
+    const float2* p;
+    size_t ps;
+    int nz, ny;
+    __device__ float2 operator()(int b, int, int ib, int Cc) const {
+      const int y = ib + Cc, c = b / HZ, z = b - c * HZ;
+      return (y < ny && z < nz) ? __ldg(p + ((size_t)(c * nz + z) * ny + y) * ps) : make_float2(0.f, 0.f);
+    }
+  } ld{X1 + kx, ps, nz, ny};
+  fft_tile<LY, NCOL, NT, false, false, true, false>(smem, ld, SmemSt<LY, NCOL, false>{smem}, tw, g.Lmax / LY);
+  __syncthreads();
+  // z stage: unit u = (pencil ky = u / 2, half h = u % 2)
+  const int Kyh = g.Kyh, Kzh = g.Kzh;
+  const size_t kcs = (size_t)Kzh * Kyh;
+  for (int u = threadIdx.x; u < 2 * LY; u += NT) {
+    const int ky = u >> 1, h = u & 1;
+    const bool fy = ky > (LY >> 1);
+    const int kyf = fy ? LY - ky : ky;
+    float2 a[3][HZ];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int n = 0; n < HZ; ++n) a[c][n] = smem[T::at(c * HZ + n, ky)];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      if (h) tw_rows<false, PZ, HZ>(a[c]);  // a[n] w_Pz^n
+      dft_inplace<HZ, false>(a[c]);
+    }
+#pragma unroll
+    for (int m = 0; m < HZ; ++m) {
+      const int kz = 2 * m + h;
+      const bool fz = kz > (PZ >> 1);
+      const int kzf = fz ? PZ - kz : kz;
+      const float* q = ks + (size_t)kzf * Kyh + kyf;
+      const float nxx = __ldg(q), nyy = __ldg(q + 3 * kcs), nzz = __ldg(q + 5 * kcs);
+      const float nxy = fy ? -__ldg(q + kcs) : __ldg(q + kcs);
+      const float nxz = fz ? -__ldg(q + 2 * kcs) : __ldg(q + 2 * kcs);
+      const float nyz = (fy != fz) ? -__ldg(q + 4 * kcs) : __ldg(q + 4 * kcs);
+      const float2 mx = a[0][m], my = a[1][m], mz = a[2][m];
+      a[0][m] = make_float2(nxx * mx.x + nxy * my.x + nxz * mz.x, nxx * mx.y + nxy * my.y + nxz * mz.y);
+      a[1][m] = make_float2(nxy * mx.x + nyy * my.x + nyz * mz.x, nxy * mx.y + nyy * my.y + nyz * mz.y);
+      a[2][m] = make_float2(nxz * mx.x + nyz * my.x + nzz * mz.x, nxz * mx.y + nyz * my.y + nzz * mz.y);
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      dft_inplace<HZ, true>(a[c]);
+      if (h) tw_rows<true, PZ, HZ>(a[c]);  // w_Pz^-n IDFT(H~_odd)[n]
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int n = 0; n < HZ; ++n) {
+        const float2 v = a[c][n];
+        const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, v.x, 1), __shfl_xor_sync(0xffffffffu, v.y, 1));
+        if ((n & 1) == h) smem[T::at(c * HZ + n, ky)] = cadd(v, o);  // rows n >= nz are never stored to X1
+      }
+  }
+  __syncthreads();
+  struct St {
+    __device__ static constexpr bool kSmem() { return false; }
+    float2* p;
+    size_t ps;
+    int nz, ny;
+    __device__ void operator()(int b, int, int ib, int Cc, float2 v) const {
+      const int y = ib + Cc, c = b / HZ, z = b - c * HZ;
+      if (y < ny && z < nz) p[((size_t)(c * nz + z) * ny + y) * ps] = v;
+    }
+  } st{X1 + kx, ps, nz, ny};
+  fft_tile<LY, NCOL, NT, false, true, false, true>(smem, SmemLd<LY, NCOL, false>{smem}, st, tw, g.Lmax / LY);
+}
+
+// KSP [kx][6][Kzh][Kyh] (stride plane_ks_stride per kx) from KS [6][Kzh][Kyh][KSp].
+__global__ void k_plane_ks(float* __restrict__ KSP, const float* __restrict__ KS, Geom g) {
+  const long long per = 6LL * g.Kzh * g.Kyh;
+  const long long kss = plane_ks_stride(g.Kzh, g.Kyh);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per * g.Kx;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int kx = (int)(i % g.Kx);
+    const long long r = i / g.Kx;  // (c, kzf, kyf) row of KS
+    KSP[kx * kss + r] = KS[r * g.KSp + kx];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K5: inverse x C2R of the three H~ rows -> H_demag (K6 then applies the local
 // terms and the update).  C2R of length Px = 2L from the half spectrum X[0..L]:
 //   Z[k] = (X[k] + conj X[L-k]) + i w^-k (X[k] - conj X[L-k]),  k < L,
@@ -1704,7 +1858,7 @@ bool comp_split_ok(const Geom& g) {
   }
 #undef CASE
 }
-int kernel_count(const Geom& g) { return (fused_y_path(g) ? 3 : 5) + 1; }
+int kernel_count(const Geom& g) { return (fused_y_path(g) || g.plane ? 3 : 5) + 1; }
 
 template <int HEUN, bool MASK>
 static cudaError_t k6_launch(const Geom& g, int mode, const float* Hd, const float* M, float* Mn, float* Hout,
@@ -1756,6 +1910,66 @@ cudaError_t launch_k2f(const Geom& g, float2* X1, const float* KS, const float2*
 #define CASE(v) case v: return (v <= 512) ? k2f_launch<(v <= 512 ? v : 512)>(g, X1, KS, tw, st) : cudaErrorInvalidValue;
   GRACE_L_SWITCH(g.Py, CASE)
 #undef CASE
+}
+
+// KP eligibility: single GPU (unblocked kx), 2 <= nz with Pz <= 16, Py an
+// instantiated length whose plane fits one CTA.
+template <int LY, int PZ>
+static constexpr bool plane_fits() {
+  return LY >= 256 && LY <= 4096 && PlaneCfg<LY, PZ>::SMEM <= 227 * 1024;
+}
+template <int PZ>
+static bool plane_fits_rt(int LY) {
+  switch (LY) {
+    case 256: return plane_fits<256, PZ>();
+    case 512: return plane_fits<512, PZ>();
+    case 1024: return plane_fits<1024, PZ>();
+    case 2048: return plane_fits<2048, PZ>();
+    case 4096: return plane_fits<4096, PZ>();
+    default: return false;
+  }
+}
+bool plane_ok(const Geom& g) {
+  if (getenv("GRACE_NO_PLANE") || g.kb != 0 || g.Kc != g.Kx || g.nz < 2 || g.Px < 2) return false;
+  if (g.Pz == 4) return plane_fits_rt<4>(g.Py);
+  if (g.Pz == 8) return plane_fits_rt<8>(g.Py);
+  if (g.Pz == 16) return plane_fits_rt<16>(g.Py);
+  return false;
+}
+size_t plane_ks_floats(const Geom& g) { return (size_t)plane_ks_stride(g.Kzh, g.Kyh) * g.Kx; }
+cudaError_t launch_plane_ks(const Geom& g, float* KSP, const float* KS, cudaStream_t st) {
+  k_plane_ks<<<4 * g.nsm, 256, 0, st>>>(KSP, KS, g);
+  return cudaGetLastError();
+}
+template <int LY, int PZ>
+static cudaError_t kplane_launch(const Geom& g, float2* X1, const float* KSP, const float2* tw, cudaStream_t st) {
+  if constexpr (plane_fits<LY, PZ>()) {
+    using C = PlaneCfg<LY, PZ>;
+    auto kern = k_plane<LY, PZ>;
+    cudaError_t e = prep(kern, C::SMEM);
+    if (e != cudaSuccess) return e;
+    GRACE_TRY(launch_k(2, kern, g.Kx, C::NT, C::SMEM, st, X1, KSP, tw, g));
+    return cudaGetLastError();
+  } else {
+    return cudaErrorInvalidValue;
+  }
+}
+template <int PZ>
+static cudaError_t kplane_launch_z(const Geom& g, float2* X1, const float* KSP, const float2* tw, cudaStream_t st) {
+  switch (g.Py) {
+    case 256: return kplane_launch<256, PZ>(g, X1, KSP, tw, st);
+    case 512: return kplane_launch<512, PZ>(g, X1, KSP, tw, st);
+    case 1024: return kplane_launch<1024, PZ>(g, X1, KSP, tw, st);
+    case 2048: return kplane_launch<2048, PZ>(g, X1, KSP, tw, st);
+    case 4096: return kplane_launch<4096, PZ>(g, X1, KSP, tw, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+cudaError_t launch_kplane(const Geom& g, float2* X1, const float* KSP, const float2* tw, cudaStream_t st) {
+  if (g.Pz == 4) return kplane_launch_z<4>(g, X1, KSP, tw, st);
+  if (g.Pz == 8) return kplane_launch_z<8>(g, X1, KSP, tw, st);
+  if (g.Pz == 16) return kplane_launch_z<16>(g, X1, KSP, tw, st);
+  return cudaErrorInvalidValue;
 }
 
 template <int L, bool DIST>

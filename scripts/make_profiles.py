@@ -37,6 +37,8 @@ def label(name):
         return "K3"
     if "k2f_y_fused" in name:
         return "K2f"
+    if "k_plane" in name:
+        return "KP"
     if "k5_inv_x" in name:
         return "K5"
     if "k6_llg" in name:
