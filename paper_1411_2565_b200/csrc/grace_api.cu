@@ -136,6 +136,7 @@ struct Rank {
   float2* X2 = nullptr;  // [3][nz][Py][pitch2] (absent on the fused nz = 1 path)
   float* KS = nullptr;
   float* KSP = nullptr;  // plane-ordered KS [kx][6][Kzh][Kyh] (KP path only)
+  TmapBlob kpmap{};      // KP's TMA map of X1
   float* Hlo = nullptr;  // halo planes [3][ny][nx]
   float* Hhi = nullptr;
   StepParams* prm = nullptr;
@@ -424,7 +425,7 @@ struct grace_ctx {
         rec(3);
       } else if (plane) {
         rec(2);
-        CE(launch_kplane(rk.g, rk.A, rk.KSP, tw, s));
+        CE(launch_kplane(rk.g, rk.A, rk.KSP, tw, s, &rk.kpmap));
         rec(3);
       } else {
         rec(2);
@@ -800,6 +801,9 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
     for (auto& rk : h->ranks) h->pipe = h->pipe && comp_split_ok(rk.g);
   }
   // TMA descriptors for the y-pencil kernels (K2 reads the x-row layout, K4 reads X2)
+  for (auto& rk : h->ranks)
+    if (h->plane && make_plane_tmap(rk.g, rk.A, &rk.kpmap) != cudaSuccess)
+      return bail(fail(GRACE_ECUDA, "plane path: TMA descriptor of X1 failed"));
   if (!h->fused && !h->plane && !getenv("GRACE_NO_TMA"))
     for (auto& rk : h->ranks) {
       rk.tma = make_ky_tmaps(rk.g, dlay ? rk.B : rk.A, rk.X2, &rk.k2map, &rk.k4map) == cudaSuccess;

@@ -110,7 +110,9 @@ bool fused_y_path(const Geom& g);
 bool plane_ok(const Geom& g);
 size_t plane_ks_floats(const Geom& g);
 cudaError_t launch_plane_ks(const Geom& g, float* KSP, const float* KS, cudaStream_t st);
-cudaError_t launch_kplane(const Geom& g, float2* X1, const float* KSP, const float2* tw, cudaStream_t st);  // nz == 1 and the y-pencils of 3 components fit one CTA
+cudaError_t make_plane_tmap(const Geom& g, const float2* X1, TmapBlob* map);
+cudaError_t launch_kplane(const Geom& g, float2* X1, const float* KSP, const float2* tw, cudaStream_t st,
+                          const TmapBlob* map);  // nz == 1 and the y-pencils of 3 components fit one CTA
 bool comp_split_ok(const Geom& g); // K1 .. K5 can run per component (bulk-copy x kernels)
 bool p2p_ok(const Geom& g);        // K1 / K4 can store into peers' buffers (bulk-copy K1, TMA K4)
 void set_pdl_blocked(bool b);      // this thread's next launches without programmatic dependent launch

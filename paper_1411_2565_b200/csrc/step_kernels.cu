@@ -90,6 +90,14 @@ __device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, unsigned byte
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
                                             int c3) {
   asm volatile(
@@ -757,28 +765,34 @@ __global__ void __launch_bounds__(NT, MINB) k2f_y_fused(float2* __restrict__ X1,
 //             pencils on consecutive lanes read consecutive words.
 //   KS      : the plane-ordered copy KSP [kx][6][Kzh][Kyh] (contiguous per kx,
 //             prefetched into L2 by one bulk prefetch before the PDL wait).
-template <int PZ>
-struct PlaneCfgZ {
+// largest divisor d of ncol with d <= cap and d * tpc a multiple of 32
+__host__ __device__ constexpr int plane_ncolg(int ncol, int cap, int tpc, int d = 0) {
+  return d == 0 ? plane_ncolg(ncol, cap, tpc, ncol)
+                : (d == 1 || (ncol % d == 0 && d <= cap && (d * tpc) % 32 == 0) ? d : plane_ncolg(ncol, cap, tpc, d - 1));
+}
+template <int LY, int PZ>
+struct PlaneCfg {
   static_assert(PZ == 4 || PZ == 8 || PZ == 16, "plane path: Pz in {4, 8, 16}");
   static constexpr int HZ = PZ / 2;
   static constexpr int NCOL = 3 * HZ;
-};
-#ifndef GRACE_PLANE_NT
-#define GRACE_PLANE_NT 768
-#endif
-template <int LY, int PZ>
-struct PlaneCfg : PlaneCfgZ<PZ> {
-  using Z = PlaneCfgZ<PZ>;
-  static constexpr int TPC0 = GRACE_PLANE_NT / Z::NCOL;
-  static constexpr int TPC1 = TPC0 >= 128 ? 128 : (TPC0 >= 64 ? 64 : (TPC0 >= 32 ? 32 : 16));
-  static constexpr int TPC = TPC1 < LY / 16 ? TPC1 : LY / 16;  // <= the first pass' butterflies per column
-  static constexpr int NT = Z::NCOL * TPC;
-  using T = TileIdx<LY, Z::NCOL, false>;
-  static constexpr size_t SMEM = (size_t)T::ELEMS * sizeof(float2);
+  // the y stage runs in G column groups of NCOLG columns, LY/16 threads per
+  // column (at most 16 complex values per thread in any pass) and at most 512
+  // threads (128 registers: the z stage holds 3 x HZ complex values per thread)
+  static constexpr int NCOLG = plane_ncolg(NCOL, 8192 / LY, LY / 16);
+  static constexpr int G = NCOL / NCOLG;
+  static constexpr int TPC = LY / 16;
+  static constexpr int NT = NCOLG * TPC;
+  using T = TileIdx<LY, NCOLG, false>;
+  static constexpr int ROWS = T::ROWS;  // rows-mode tiles: per-column region, the same for every group size
+  static constexpr int TILE = NCOL * ROWS;  // float2
+  static constexpr int BY = 256;            // TMA box rows (y)
+  using PL = Plan<LY, false, rb_for(false, 1, LY)>;  // the y transforms' radix plan (rows mode, V = 1)
+  static constexpr int TWE = PL::TW_ELEMS;               // per-pass twiddle tables (fill_pass_twiddles)
+  static constexpr size_t SMEM = (size_t)(TILE + TWE) * sizeof(float2) + 16;
   static_assert(NT % 32 == 0 && (2 * LY) % 32 == 0, "whole warps in the z stage");
+  static_assert((ROWS * 8) % 128 == 0, "128-byte aligned column regions (TMA destinations)");
 };
 __host__ __device__ constexpr long long plane_ks_stride(int Kzh, int Kyh) { return ((6LL * Kzh * Kyh + 31) / 32) * 32; }
-
 // a[N] *= w_PZ^{+-N} for N < HZ (compile-time twiddles)
 template <bool INV, int PZ, int HZ, int N = 0>
 __device__ __forceinline__ void tw_rows(float2* a) {
@@ -790,34 +804,61 @@ __device__ __forceinline__ void tw_rows(float2* a) {
 
 template <int LY, int PZ>
 __global__ void __launch_bounds__(PlaneCfg<LY, PZ>::NT, 1)
-    k_plane(float2* __restrict__ X1, const float* __restrict__ KSP, const float2* __restrict__ tw, Geom g) {
+    k_plane(const __grid_constant__ CUtensorMap xmap, float2* __restrict__ X1, const float* __restrict__ KSP,
+            const float2* __restrict__ tw, Geom g) {
   using C = PlaneCfg<LY, PZ>;
   using T = typename C::T;
-  constexpr int HZ = C::HZ, NCOL = C::NCOL, NT = C::NT;
-  extern __shared__ float2 smem[];
+  constexpr int HZ = C::HZ, NCOLG = C::NCOLG, NT = C::NT, ROWS = C::ROWS, BY = C::BY;
+  extern __shared__ __align__(1024) unsigned char kp_raw[];
+  float2* smem = reinterpret_cast<float2*>(kp_raw);
+  float2* tws = smem + C::TILE;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::TILE + C::TWE);
   const int kx = blockIdx.x;
   const long long kss = plane_ks_stride(g.Kzh, g.Kyh);
   const float* ks = KSP + kx * kss;
+  const int nz = g.nz, ny = g.ny;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+  }
   pdl_trigger();
   pdl_wait();
-  // the KS slice into L2 while the y stage runs.  After the PDL wait: issued
-  // before it (the slice is constant), the graph-replayed step read garbage
-  // (measured: non-finite M after one step; eager launches were correct).
-  if (threadIdx.x == 0)
+  // X1 column pairs (kx & ~1, kx | 1) x BY rows of every (c, z < nz) land in the
+  // upper part of their own column region of the tile (rows >= ny zero-filled by
+  // the TMA unit); pass 0 of the y-FFT reads them from there
+  const int by = ny < BY ? ny : BY;  // the map's box rows (make_plane_tmap)
+  const int nb = (ny + by - 1) / by;
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(bar, (unsigned)(3 * nz * nb * by * 16));
+    for (int c = 0; c < 3; ++c)
+      for (int z = 0; z < nz; ++z)
+        for (int j = 0; j < nb; ++j)
+          tma_load_3d(smem + (size_t)(c * HZ + z) * ROWS + j * by * 2, &xmap, bar, kx & ~1, j * by, c * nz + z);
+    // the KS slice into L2 while the y stage runs (after the PDL wait: issued
+    // before it, the graph-replayed step read garbage -- measured, non-finite M)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(ks), "r"((unsigned)(kss * 4)) : "memory");
-  const int nz = g.nz, ny = g.ny;
-  const size_t ps = g.pitch1;
-  struct Ld {  // column b = c HZ + z of X1 [3][nz][ny][pitch1] at this kx; rows y >= ny and z >= nz are zero
-    __device__ static constexpr bool kSmem() { return false; }
-    const float2* p;
-    size_t ps;
-    int nz, ny;
-    __device__ float2 operator()(int b, int, int ib, int Cc) const {
-      const int y = ib + Cc, c = b / HZ, z = b - c * HZ;
-      return (y < ny && z < nz) ? __ldg(p + ((size_t)(c * nz + z) * ny + y) * ps) : make_float2(0.f, 0.f);
-    }
-  } ld{X1 + kx, ps, nz, ny};
-  fft_tile<LY, NCOL, NT, false, false, true, false>(smem, ld, SmemSt<LY, NCOL, false>{smem}, tw, g.Lmax / LY);
+  }
+  // per-pass twiddles of the y plan in smem (the global table's scattered 8-byte
+  // reads were the kernel's largest L2 sector traffic)
+  fill_pass_twiddles<typename C::PL, LY>(tws, tw, g.Lmax / LY, threadIdx.x, NT);
+  __syncthreads();
+  mbar_wait(bar, 0);
+  const int odd = kx & 1;
+#pragma unroll 1
+  for (int grp = 0; grp < C::G; ++grp) {
+    float2* tile = smem + (size_t)grp * NCOLG * ROWS;
+    struct Ld {  // column b of the group: y row i of (c, z), from the staged pair
+      __device__ static constexpr bool kSmem() { return true; }
+      const float2* s;
+      int b0, odd, nz, ny;
+      __device__ float2 operator()(int b, int, int ib, int Cc) const {
+        const int y = ib + Cc, bb = b0 + b, c = bb / HZ, z = bb - c * HZ;
+        return (y < ny && z < nz) ? s[b * ROWS + 2 * y + odd] : make_float2(0.f, 0.f);
+      }
+    } ld{tile, grp * NCOLG, odd, nz, ny};
+    if (grp) __syncthreads();
+    fft_tile<LY, NCOLG, NT, false, false, true, false, 1, false, true>(tile, ld, SmemSt<LY, NCOLG, false>{tile}, tws, 1);
+  }
   __syncthreads();
   // z stage: unit u = (pencil ky = u / 2, half h = u % 2)
   const int Kyh = g.Kyh, Kzh = g.Kzh;
@@ -830,7 +871,7 @@ __global__ void __launch_bounds__(PlaneCfg<LY, PZ>::NT, 1)
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
-      for (int n = 0; n < HZ; ++n) a[c][n] = smem[T::at(c * HZ + n, ky)];
+      for (int n = 0; n < HZ; ++n) a[c][n] = smem[(c * HZ + n) * ROWS + ky];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       if (h) tw_rows<false, PZ, HZ>(a[c]);  // a[n] w_Pz^n
@@ -862,21 +903,27 @@ __global__ void __launch_bounds__(PlaneCfg<LY, PZ>::NT, 1)
       for (int n = 0; n < HZ; ++n) {
         const float2 v = a[c][n];
         const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, v.x, 1), __shfl_xor_sync(0xffffffffu, v.y, 1));
-        if ((n & 1) == h) smem[T::at(c * HZ + n, ky)] = cadd(v, o);  // rows n >= nz are never stored to X1
+        if ((n & 1) == h) smem[(c * HZ + n) * ROWS + ky] = cadd(v, o);  // rows n >= nz are never stored to X1
       }
   }
   __syncthreads();
-  struct St {
-    __device__ static constexpr bool kSmem() { return false; }
-    float2* p;
-    size_t ps;
-    int nz, ny;
-    __device__ void operator()(int b, int, int ib, int Cc, float2 v) const {
-      const int y = ib + Cc, c = b / HZ, z = b - c * HZ;
-      if (y < ny && z < nz) p[((size_t)(c * nz + z) * ny + y) * ps] = v;
-    }
-  } st{X1 + kx, ps, nz, ny};
-  fft_tile<LY, NCOL, NT, false, true, false, true>(smem, SmemLd<LY, NCOL, false>{smem}, st, tw, g.Lmax / LY);
+  const size_t ps = g.pitch1;
+#pragma unroll 1
+  for (int grp = 0; grp < C::G; ++grp) {
+    float2* tile = smem + (size_t)grp * NCOLG * ROWS;
+    struct St {
+      __device__ static constexpr bool kSmem() { return false; }
+      float2* p;
+      size_t ps;
+      int b0, nz, ny;
+      __device__ void operator()(int b, int, int ib, int Cc, float2 v) const {
+        const int y = ib + Cc, bb = b0 + b, c = bb / HZ, z = bb - c * HZ;
+        if (y < ny && z < nz) p[((size_t)(c * nz + z) * ny + y) * ps] = v;
+      }
+    } st{X1 + kx, ps, grp * NCOLG, nz, ny};
+    if (grp) __syncthreads();
+    fft_tile<LY, NCOLG, NT, false, true, false, true, 1, false, true>(tile, SmemLd<LY, NCOLG, false>{tile}, st, tws, 1);
+  }
 }
 
 // KSP [kx][6][Kzh][Kyh] (stride plane_ks_stride per kx) from KS [6][Kzh][Kyh][KSp].
@@ -1699,6 +1746,17 @@ static cudaError_t encode_map(TmapBlob* out, CUtensorMapDataType dtype, int rank
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// KP's input: X1 [3 nz][ny][pitch1] complex (8-byte elements), boxes of one column
+// pair x BY rows x one (c, z) row set.
+cudaError_t make_plane_tmap(const Geom& g, const float2* X1, TmapBlob* map) {
+  const unsigned long long p1 = 8ull * g.pitch1;
+  const unsigned long long d[3] = {(unsigned long long)g.Kx, (unsigned long long)g.ny, 3ull * g.nz};
+  const unsigned long long str[2] = {p1, p1 * g.ny};
+  const unsigned by = (unsigned)(g.ny < 256 ? g.ny : 256);
+  const unsigned box[3] = {2, by, 1};
+  return encode_map(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, X1, d, str, box);
+}
+
 template <int L>
 static cudaError_t ky_maps(const Geom& g, const float2* k2_in, const float2* x2, TmapBlob* k2map, TmapBlob* k4map) {
   constexpr int NCOL = ytma_ncol<L>();
@@ -1912,8 +1970,8 @@ cudaError_t launch_k2f(const Geom& g, float2* X1, const float* KS, const float2*
 #undef CASE
 }
 
-// KP eligibility: single GPU (unblocked kx), 2 <= nz with Pz <= 16, Py an
-// instantiated length whose plane fits one CTA.
+// KP eligibility: GRACE_PLANE=1, single GPU (unblocked kx), 2 <= nz with
+// Pz <= 16, Py an instantiated length whose plane fits one CTA.
 template <int LY, int PZ>
 static constexpr bool plane_fits() {
   return LY >= 256 && LY <= 4096 && PlaneCfg<LY, PZ>::SMEM <= 227 * 1024;
@@ -1930,7 +1988,8 @@ static bool plane_fits_rt(int LY) {
   }
 }
 bool plane_ok(const Geom& g) {
-  if (getenv("GRACE_NO_PLANE") || g.kb != 0 || g.Kc != g.Kx || g.nz < 2 || g.Px < 2) return false;
+  const char* on = getenv("GRACE_PLANE");  // opt-in: measured slower than K2..K4 on B200
+  if (!on || on[0] != '1' || g.kb != 0 || g.Kc != g.Kx || g.nz < 2 || g.Px < 2) return false;
   if (g.Pz == 4) return plane_fits_rt<4>(g.Py);
   if (g.Pz == 8) return plane_fits_rt<8>(g.Py);
   if (g.Pz == 16) return plane_fits_rt<16>(g.Py);
@@ -1942,33 +2001,39 @@ cudaError_t launch_plane_ks(const Geom& g, float* KSP, const float* KS, cudaStre
   return cudaGetLastError();
 }
 template <int LY, int PZ>
-static cudaError_t kplane_launch(const Geom& g, float2* X1, const float* KSP, const float2* tw, cudaStream_t st) {
+static cudaError_t kplane_launch(const Geom& g, float2* X1, const float* KSP, const float2* tw, cudaStream_t st,
+                                 const TmapBlob* map) {
   if constexpr (plane_fits<LY, PZ>()) {
     using C = PlaneCfg<LY, PZ>;
     auto kern = k_plane<LY, PZ>;
     cudaError_t e = prep(kern, C::SMEM);
     if (e != cudaSuccess) return e;
-    GRACE_TRY(launch_k(2, kern, g.Kx, C::NT, C::SMEM, st, X1, KSP, tw, g));
+    CUtensorMap xm;
+    std::memcpy(&xm, map->b, sizeof xm);
+    GRACE_TRY(launch_k(2, kern, g.Kx, C::NT, C::SMEM, st, xm, X1, KSP, tw, g));
     return cudaGetLastError();
   } else {
     return cudaErrorInvalidValue;
   }
 }
 template <int PZ>
-static cudaError_t kplane_launch_z(const Geom& g, float2* X1, const float* KSP, const float2* tw, cudaStream_t st) {
+static cudaError_t kplane_launch_z(const Geom& g, float2* X1, const float* KSP, const float2* tw, cudaStream_t st,
+                                   const TmapBlob* map) {
   switch (g.Py) {
-    case 256: return kplane_launch<256, PZ>(g, X1, KSP, tw, st);
-    case 512: return kplane_launch<512, PZ>(g, X1, KSP, tw, st);
-    case 1024: return kplane_launch<1024, PZ>(g, X1, KSP, tw, st);
-    case 2048: return kplane_launch<2048, PZ>(g, X1, KSP, tw, st);
-    case 4096: return kplane_launch<4096, PZ>(g, X1, KSP, tw, st);
+    case 256: return kplane_launch<256, PZ>(g, X1, KSP, tw, st, map);
+    case 512: return kplane_launch<512, PZ>(g, X1, KSP, tw, st, map);
+    case 1024: return kplane_launch<1024, PZ>(g, X1, KSP, tw, st, map);
+    case 2048: return kplane_launch<2048, PZ>(g, X1, KSP, tw, st, map);
+    case 4096: return kplane_launch<4096, PZ>(g, X1, KSP, tw, st, map);
     default: return cudaErrorInvalidValue;
   }
 }
-cudaError_t launch_kplane(const Geom& g, float2* X1, const float* KSP, const float2* tw, cudaStream_t st) {
-  if (g.Pz == 4) return kplane_launch_z<4>(g, X1, KSP, tw, st);
-  if (g.Pz == 8) return kplane_launch_z<8>(g, X1, KSP, tw, st);
-  if (g.Pz == 16) return kplane_launch_z<16>(g, X1, KSP, tw, st);
+cudaError_t launch_kplane(const Geom& g, float2* X1, const float* KSP, const float2* tw, cudaStream_t st,
+                          const TmapBlob* map) {
+  if (!map) return cudaErrorInvalidValue;
+  if (g.Pz == 4) return kplane_launch_z<4>(g, X1, KSP, tw, st, map);
+  if (g.Pz == 8) return kplane_launch_z<8>(g, X1, KSP, tw, st, map);
+  if (g.Pz == 16) return kplane_launch_z<16>(g, X1, KSP, tw, st, map);
   return cudaErrorInvalidValue;
 }
 
@@ -1998,6 +2063,7 @@ cudaError_t launch_k5(const Geom& g, const float2* X1, float* Hd, const float2* 
   GRACE_L_SWITCH(L, CASE)
 #undef CASE
 }
+
 
 // ---------------------------------------------------------------------------
 // Utilities.
