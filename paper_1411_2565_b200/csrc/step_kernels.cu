@@ -1508,9 +1508,14 @@ struct ZCfg {  // K3 and K2'
 // without PDL: the programmatic edge would tie it to the preceding kernel only.
 static thread_local bool t_no_pdl = false;
 void set_pdl_blocked(bool b) { t_no_pdl = b; }
+// kid | 64: a kernel of the nz = 1 (K2') step, where every boundary is latency:
+// there K6 behind K5 gains too (SP4 10.4 -> 10.0 us/step, refined 13.2 -> 12.7;
+// profiles/r02_sweeps.md), so the default mask for those launches is 63.
 static bool pdl_on(int kid) {
-  static const int mask = getenv("GRACE_NO_PDL") ? 0 : (getenv("GRACE_PDL_MASK") ? atoi(getenv("GRACE_PDL_MASK")) : 23);
-  return !t_no_pdl && (mask & kid) != 0;
+  static const char* env = getenv("GRACE_PDL_MASK");
+  static const int mask = getenv("GRACE_NO_PDL") ? 0 : (env ? atoi(env) : 23);
+  static const int mask1 = getenv("GRACE_NO_PDL") ? 0 : (env ? atoi(env) : 63);
+  return !t_no_pdl && (((kid & 64) ? mask1 : mask) & kid & 63) != 0;
 }
 // Step-kernel launch with programmatic stream serialization (PDL, see pdl_wait).
 template <class... E, class... A>
@@ -1926,12 +1931,13 @@ static cudaError_t k6_launch(const Geom& g, int mode, const float* Hd, const flo
   const bool vec = g.nx % 4 == 0;
   const long long threads = vec ? N / 4 : N;
   const unsigned grid = (unsigned)((threads + 255) / 256);
+  const int k6kid = fused_y_path(g) ? 32 | 64 : 32;
   if (vec) {
-    if (g.kb) GRACE_TRY(launch_k(32, k6_llg<true, true, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi, aerr));
-    else GRACE_TRY(launch_k(32, k6_llg<true, false, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi, aerr));
+    if (g.kb) GRACE_TRY(launch_k(k6kid, k6_llg<true, true, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi, aerr));
+    else GRACE_TRY(launch_k(k6kid, k6_llg<true, false, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi, aerr));
   } else {
-    if (g.kb) GRACE_TRY(launch_k(32, k6_llg<false, true, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi, aerr));
-    else GRACE_TRY(launch_k(32, k6_llg<false, false, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi, aerr));
+    if (g.kb) GRACE_TRY(launch_k(k6kid, k6_llg<false, true, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi, aerr));
+    else GRACE_TRY(launch_k(k6kid, k6_llg<false, false, HEUN, MASK>, grid, 256, 0, st, Hd, M, Mn, Hout, g, prm, flag, mode, Hlo, Hhi, aerr));
   }
   return cudaGetLastError();
 }
