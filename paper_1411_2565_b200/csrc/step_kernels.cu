@@ -1928,7 +1928,10 @@ static cudaError_t k6_launch(const Geom& g, int mode, const float* Hd, const flo
                              const StepParams* prm, unsigned long long* flag, cudaStream_t st, const float* Hlo,
                              const float* Hhi, unsigned* aerr) {
   const long long N = (long long)g.nzl * g.ny * g.nx;
-  const bool vec = g.nx % 4 == 0;
+#ifndef GRACE_K6_VEC_MIN
+#define GRACE_K6_VEC_MIN 16384  // cells below which K6 runs one cell per thread: 4x the CTAs on tiny grids (SP4 10.5 -> 9.1 us/step; 32^3 is 4 % slower scalar)
+#endif
+  const bool vec = g.nx % 4 == 0 && N >= GRACE_K6_VEC_MIN;
   const long long threads = vec ? N / 4 : N;
   const unsigned grid = (unsigned)((threads + 255) / 256);
   const int k6kid = fused_y_path(g) ? 32 | 64 : 32;
