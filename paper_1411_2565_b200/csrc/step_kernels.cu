@@ -1062,9 +1062,12 @@ struct XbSt {
 #ifndef GRACE_XB_MINB
 #define GRACE_XB_MINB 4  // resident x-kernel CTAs per SM (scripts/sweep_x2.sh: 8192 x 1 -> 2048 x 4: slab K1 0.348 -> 0.288, K5 0.296 -> 0.275 ms; SP4 19.3 -> 11.3 us/step)
 #endif
-template <int L>
+#ifndef GRACE_XB_ELEMS_TINY
+#define GRACE_XB_ELEMS_TINY 512  // tiles of tiny grids (fewer default tiles than half the SMs): SP4 9.1 -> 8.2 us/step
+#endif
+template <int L, int E = GRACE_XB_ELEMS>
 struct XBulk {
-  static constexpr int RB = GRACE_XB_ELEMS / L > 0 ? GRACE_XB_ELEMS / L : 1;  // rows per tile
+  static constexpr int RB = E / L > 0 ? E / L : 1;  // rows per tile
   static constexpr int NT = RB * (L / 16);
   using T = TileIdx<L, RB, false>;
   static constexpr int TB = ((T::ELEMS * 8 + 1023) / 1024) * 1024;
@@ -1075,11 +1078,11 @@ struct XBulk {
 };
 constexpr int kXBulkMinL = 64, kXBulkMaxL = 4096;
 
-template <int L, bool FWD, bool DIST>
-__global__ void __launch_bounds__(XBulk<L>::NT, GRACE_XB_MINB)
+template <int L, bool FWD, bool DIST, int E = GRACE_XB_ELEMS>
+__global__ void __launch_bounds__(XBulk<L, E>::NT, GRACE_XB_MINB)
     k_x_bulk(const void* __restrict__ in, void* __restrict__ out, const float2* __restrict__ tw, Geom g,
              StepParams* bump) {
-  using X = XBulk<L>;
+  using X = XBulk<L, E>;
   using T = typename X::T;
   constexpr int RB = X::RB, NT = X::NT;
   extern __shared__ __align__(1024) unsigned char smraw[];
@@ -1558,11 +1561,16 @@ static bool xbulk_ok(const Geom& g, bool fwd) {
   return g.pitch1 % 2 == 0 && g.pitch1 >= L + 2 && ROWS >= L + 2;
 }
 
-template <int L, bool FWD, bool DIST>
+template <int L, bool FWD, bool DIST, int E = GRACE_XB_ELEMS>
 static cudaError_t xbulk_launch(const Geom& g, const void* in, void* out, const float2* tw, StepParams* bump,
                                 cudaStream_t st) {
-  using X = XBulk<L>;
-  auto kern = k_x_bulk<L, FWD, DIST>;
+  using X = XBulk<L, E>;
+  if constexpr (E == GRACE_XB_ELEMS && GRACE_XB_ELEMS_TINY < GRACE_XB_ELEMS && L <= GRACE_XB_ELEMS_TINY / 2) {
+    // tiny grids: shorter tiles, more CTAs (each CTA's chain is one tile either way)
+    if ((g.nc * g.nzl * g.ny + X::RB - 1) / X::RB < g.nsm / 2)
+      return xbulk_launch<L, FWD, DIST, GRACE_XB_ELEMS_TINY>(g, in, out, tw, bump, st);
+  }
+  auto kern = k_x_bulk<L, FWD, DIST, E>;
   cudaError_t e = prep(kern, X::SMEM);
   if (e != cudaSuccess) return e;
   const int ntiles = (g.nc * g.nzl * g.ny + X::RB - 1) / X::RB;
