@@ -354,6 +354,9 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? (YTma<L, NCOL>::N
 // staged rows into registers and writes the work tile; as soon as every thread
 // is past it, the next tile's TMA load goes into the staging buffer and overlaps
 // the remaining passes.  Twiddles from the global table (no room for smem ones).
+#ifndef GRACE_YSTAGE_1024
+#define GRACE_YSTAGE_1024 0  // columns of a staged K2 at L = 1024 (0: the double-buffered TMA kernel)
+#endif
 #ifndef GRACE_YSTAGE_2048
 #define GRACE_YSTAGE_2048 8  // columns of the staged K2 at L = 2048 (0: the double-buffered TMA kernel; 0.68 -> 0.61 ms)
 #endif
@@ -365,7 +368,8 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? (YTma<L, NCOL>::N
 #endif
 template <int L>
 struct YStage {
-  static constexpr int NCOL = (L == 2048 && GRACE_YSTAGE_2048) ? GRACE_YSTAGE_2048 : 4;
+  static constexpr int NCOL = (L == 2048 && GRACE_YSTAGE_2048) ? GRACE_YSTAGE_2048
+                             : ((L == 1024 && GRACE_YSTAGE_1024) ? GRACE_YSTAGE_1024 : 4);
   using T = TileIdx<L, NCOL, true>;
   using PL = Plan<L, false, 4>;
   static constexpr int WB = ((T::ELEMS * 8 + 1023) / 1024) * 1024;  // work tile bytes
@@ -1681,6 +1685,7 @@ cudaError_t launch_k2(const Geom& g, const float2* X1, float2* X2, const float2*
 #ifndef GRACE_NO_YSTAGE
   if (tmap != nullptr && g.Py == 4096) return ky_stage_launch<4096>(g, X2, tw, st, tmap);
   if (GRACE_YSTAGE_2048 && tmap != nullptr && g.Py == 2048) return ky_stage_launch<2048>(g, X2, tw, st, tmap);
+  if (GRACE_YSTAGE_1024 && tmap != nullptr && g.Py == 1024) return ky_stage_launch<1024>(g, X2, tw, st, tmap);
 #endif
   // The TMA tiles hold GRACE_YT_ELEMS / L columns; below 4 (L >= 4096) K2's row
   // stores are 16-byte half sectors and cost L2 read-modify-writes (block
@@ -1781,7 +1786,9 @@ static cudaError_t ky_maps(const Geom& g, const float2* k2_in, const float2* x2,
   const unsigned long long s2[4] = {p1, p1 * g.ny, p1 * g.ny * g.nzl, p1 * g.ny * g.nzl * 3};
   // K2's map: 4-column boxes for the staged long-pencil kernel (k_y_stage)
 #ifndef GRACE_NO_YSTAGE
-  constexpr int NCOL2 = (L == 4096 || (L == 2048 && GRACE_YSTAGE_2048)) ? YStage<(L >= 2048 ? L : 2048)>::NCOL : NCOL;
+  constexpr int NCOL2 = (L == 4096 || (L == 2048 && GRACE_YSTAGE_2048) || (L == 1024 && GRACE_YSTAGE_1024))
+                            ? YStage<(L >= 1024 ? L : 1024)>::NCOL
+                            : NCOL;
 #else
   constexpr int NCOL2 = NCOL;
 #endif
