@@ -211,7 +211,8 @@ int grace_kernel_spectrum_f64(int nx, int ny, int nz, double dx, double dy, doub
 
 /* Per-kernel timing.  grace_set_profiling(h, 1) makes grace_step launch the kernels
  * eagerly with a CUDA event pair around each; grace_kernel_times returns, per kernel
- * of the step (order K1, K2, K3, K4, K5, K6 or K1, K2', K5, K6), the summed milliseconds and
+ * of the step (order K1, K2, K3, K4, K5, K6; K1, K2', K5, K6 for nz = 1; K1, KP, K5, K6 on the
+ * opt-in plane-fused thin-film path, GRACE_PLANE=1), the summed milliseconds and
  * the launch count since the last reset (reset = 1 clears after reading).  nk in:
  * capacity of ms[]/launches[]; out: number of kernels per step. */
 int grace_set_profiling(grace_ctx *h, int on);
