@@ -121,6 +121,8 @@ HEFF_CASES = [
     ((3, 2, 200), (1e-9, 1e-9, 1e-9), 1e6, 1e-11, 0.0, (0, 0, 0)),     # Pz = 512: 8-column tiles
     ((2, 2, 300), (1e-9, 1e-9, 1e-9), 1e6, 1e-11, 0.0, (0, 0, 0)),     # Pz = 1024
     ((4, 2048, 2), (1e-9, 1e-9, 1e-9), 1e6, 1e-11, 0.0, (0, 0, 0)),    # Py = 4096: staged K2, partial tile
+    ((16, 200, 1), (1e-9, 1e-9, 1e-9), 8e5, 1.3e-11, 0.0, (0, 0, 0)),  # nz = 1, Py = 512: K2' with smem twiddles
+    ((24, 100, 1), (2e-9, 1e-9, 1e-9), 8e5, 1.3e-11, 0.0, (0, 0, 0)),  # nz = 1, Py = 256
 ]
 
 
