@@ -1647,7 +1647,11 @@ template <int L, bool INV>
 static cudaError_t ky_tma_launch(const Geom& g, float2* out, const float2* tw, cudaStream_t st, int n_out,
                                  const TmapBlob* tmap) {
   constexpr int NCOL = ytma_ncol<L>();
-  constexpr int NB = (INV && L == 2048) ? GRACE_YT_NB_INV : 2;  // single-buffered slower elsewhere (block K4 27.6 vs 8.0 ms)
+#ifndef GRACE_YT_NB1_1024
+#define GRACE_YT_NB1_1024 0  // K4 at L = 1024 single-buffered (two CTAs per SM) as at 2048
+#endif
+  constexpr int NB = (INV && (L == 2048 || (L == 1024 && GRACE_YT_NB1_1024))) ? GRACE_YT_NB_INV
+                                                                            : 2;  // single-buffered slower elsewhere (block K4 27.6 vs 8.0 ms)
   using Y = YTma<L, NCOL, NB>;
   auto kern = k_y_tma<L, NCOL, INV, NB>;
   cudaError_t e = prep(kern, Y::SMEM);
