@@ -150,6 +150,8 @@ struct Rank {
   unsigned char* mask = nullptr;       // geometry mask [nzl][ny][nx] (grace_set_geometry; null: none)
   bool tma = false;                    // TMA descriptors of the K2 / K4 inputs built
   TmapBlob k2map{}, k4map{};
+  bool tma4s = false;  // K4's TMA-store map of X1 built (single GPU)
+  TmapBlob k4out{};
   bool tma3 = false;                   // TMA descriptors of the K3 pencils and KS slices built
   TmapBlob k3x{}, k3k{};
   float2* tw3 = nullptr;               // K3's twiddle tables in their smem layout
@@ -435,7 +437,7 @@ struct grace_ctx {
         CE(launch_k3(rk.g, rk.X2, rk.KS, tw, s, rk.tma3 ? &rk.k3x : nullptr, rk.tma3 ? &rk.k3k : nullptr, rk.tw3));
         rec(5);
         rec(6);
-        CE(launch_k4(rk.g, rk.X2, rk.A, tw, s, rk.tma ? &rk.k4map : nullptr));
+        CE(launch_k4(rk.g, rk.X2, rk.A, tw, s, rk.tma ? &rk.k4map : nullptr, rk.tma4s ? &rk.k4out : nullptr));
         rec(7);
       }
       return cudaSuccess;
@@ -806,7 +808,9 @@ int create_impl(int nx, int ny, int nz, double dx, double dy, double dz, double 
       return bail(fail(GRACE_ECUDA, "plane path: TMA descriptor of X1 failed"));
   if (!h->fused && !h->plane && !getenv("GRACE_NO_TMA"))
     for (auto& rk : h->ranks) {
-      rk.tma = make_ky_tmaps(rk.g, dlay ? rk.B : rk.A, rk.X2, &rk.k2map, &rk.k4map) == cudaSuccess;
+      rk.tma = make_ky_tmaps(rk.g, dlay ? rk.B : rk.A, rk.X2, &rk.k2map, &rk.k4map,
+                             (dlay || getenv("GRACE_NO_TMA_STORE")) ? nullptr : &rk.k4out) == cudaSuccess;
+      rk.tma4s = rk.tma && !dlay && !getenv("GRACE_NO_TMA_STORE");
       rk.tma3 = rk.X2 && make_k3_tmaps(rk.g, rk.X2, rk.KS, &rk.k3x, &rk.k3k) == cudaSuccess;
     }
   cudaGetLastError();

@@ -81,7 +81,9 @@ struct alignas(64) TmapBlob {
   unsigned char b[128];
 };
 // Tensor maps of the K2 input (x-row layout) and the K4 input (X2) for TMA loads.
-cudaError_t make_ky_tmaps(const Geom& g, const float2* k2_in, const float2* x2, TmapBlob* k2map, TmapBlob* k4map);
+// k4out (nullable, single GPU): the K4 output map for TMA stores into X1.
+cudaError_t make_ky_tmaps(const Geom& g, const float2* k2_in, const float2* x2, TmapBlob* k2map, TmapBlob* k4map,
+                          TmapBlob* k4out = nullptr);
 cudaError_t launch_k2(const Geom& g, const float2* X1, float2* X2, const float2* tw, cudaStream_t st,
                       const TmapBlob* tmap = nullptr);
 // K3 tensor maps (X2 pencils, KS slices) for the TMA-fed kernel; cudaErrorNotSupported
@@ -93,7 +95,7 @@ cudaError_t launch_k3(const Geom& g, float2* X2, const float* KS, const float2* 
                       const TmapBlob* xmap = nullptr, const TmapBlob* kmap = nullptr, const float2* tw3 = nullptr);
 cudaError_t make_k3_twiddles(const Geom& g, const float2* tw, float2** out, cudaStream_t st);
 cudaError_t launch_k4(const Geom& g, const float2* X2, float2* X1, const float2* tw, cudaStream_t st,
-                      const TmapBlob* tmap = nullptr);
+                      const TmapBlob* tmap = nullptr, const TmapBlob* tout = nullptr);
 cudaError_t launch_k2f(const Geom& g, float2* X1, const float* KS, const float2* tw, cudaStream_t st);
 // K5: inverse x C2R of X1 -> H_demag Hd [3][nzl][ny][nx].
 cudaError_t launch_k5(const Geom& g, const float2* X1, float* Hd, const float2* tw, cudaStream_t st);

@@ -90,6 +90,17 @@ __device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, unsigned byte
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 
+// TMA tensor store from shared memory (bulk async-group completion) and its waits
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3,
+                                             int c4) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];\n" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
@@ -259,10 +270,14 @@ struct YTma {
 #ifndef GRACE_YT_NB_INV
 #define GRACE_YT_NB_INV 1  // K4 tile buffers per CTA (1: two single-buffered CTAs per SM, 0.596 -> 0.585 ms; 2: double-buffered)
 #endif
-template <int L, int NCOL, bool INV, int NB = 2>
+// TST (K4, single GPU): the inverse's last pass writes the tile's linear layout in
+// place and one thread stores rows y < n_out with TMA boxes (tout), overlapping
+// the next tile's load and passes; the buffer is reloaded once the store has read it.
+template <int L, int NCOL, bool INV, int NB = 2, bool TST = false>
 __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? (YTma<L, NCOL>::NT <= 512 ? 2 : 1) : GRACE_YT_MINB)
-    k_y_tma(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, const float2* __restrict__ tw, Geom g,
-            int n_out) {
+    k_y_tma(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+            float2* __restrict__ out, const float2* __restrict__ tw, Geom g, int n_out) {
+  static_assert(!TST || INV, "TMA stores on the inverse (K4) only");
   using Y = YTma<L, NCOL, NB>;
   constexpr int NT = Y::NT;
   constexpr int ROWS = Y::rows_in(INV);
@@ -323,12 +338,14 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? (YTma<L, NCOL>::N
     if (t + (int)gridDim.x < ntiles && t + 2 * (int)gridDim.x >= ntiles) pdl_trigger();  // last tile next
     if constexpr (NB == 2) {
       if (threadIdx.x == 0 && t + (int)gridDim.x < ntiles) {
+        if constexpr (TST) bulk_wait_read0();  // the other buffer's store has read it
         fence_proxy_async();
         issue(t + gridDim.x, reinterpret_cast<float2*>(smraw + ((k + 1) & 1) * Y::TB), bar + ((k + 1) & 1));
       }
       mbar_wait(bar + (k & 1), (k >> 1) & 1);
     } else {
       if (threadIdx.x == 0) {
+        if constexpr (TST) bulk_wait_read0();  // the previous tile's store has read the buffer
         fence_proxy_async();
         issue(t, cur, bar);
       }
@@ -338,6 +355,18 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? (YTma<L, NCOL>::N
     const int kx0 = xt * NCOL;
     float2* o = (INV ? xrow_dst(g, out, slab) : out + (size_t)slab * g.Py * g.pitch2) + kx0;
     const int pitch = INV ? g.pitch1 : g.pitch2;
+    if constexpr (TST) {
+      fft_tile<L, NCOL, NT, true, INV, !INV, INV, 1, false, true>(cur, SmemLd<L, NCOL, true>{cur},
+                                                                   SmemSt<L, NCOL, true>{cur}, tws, 1);
+      fence_proxy_async();  // this thread's tile writes -> the async proxy
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int c = slab / g.nz, z = slab - c * g.nz;
+        for (int y0 = 0; y0 < n_out; y0 += BR) tma_store_5d(&tout, cur + y0 * NCOL, kx0, y0, z, c, 0);
+        bulk_commit();
+      }
+      continue;
+    }
     if (g.Kc - kx0 >= NCOL && n_out >= (INV ? L / 2 : L))
       fft_tile<L, NCOL, NT, true, INV, !INV, INV, 1, false, true>(cur, SmemLd<L, NCOL, true>{cur}, StFull{o, pitch},
                                                                    tws, 1);
@@ -345,6 +374,9 @@ __global__ void __launch_bounds__(YTma<L, NCOL>::NT, NB == 1 ? (YTma<L, NCOL>::N
       fft_tile<L, NCOL, NT, true, INV, !INV, INV, 1, false, true>(cur, SmemLd<L, NCOL, true>{cur},
                                                                    St{o, pitch, n_out, g.Kc - kx0}, tws, 1);
     __syncthreads();
+  }
+  if constexpr (TST) {
+    if (threadIdx.x == 0) bulk_wait0();  // the stores land before the grid completes (K5 waits on it)
   }
 }
 
@@ -1645,7 +1677,7 @@ constexpr int kTmaMinL = 64;
 
 template <int L, bool INV>
 static cudaError_t ky_tma_launch(const Geom& g, float2* out, const float2* tw, cudaStream_t st, int n_out,
-                                 const TmapBlob* tmap) {
+                                 const TmapBlob* tmap, const TmapBlob* tout = nullptr) {
   constexpr int NCOL = ytma_ncol<L>();
 #ifndef GRACE_YT_NB1_1024
 #define GRACE_YT_NB1_1024 0  // K4 at L = 1024 single-buffered (two CTAs per SM) as at 2048
@@ -1653,7 +1685,10 @@ static cudaError_t ky_tma_launch(const Geom& g, float2* out, const float2* tw, c
   constexpr int NB = (INV && (L == 2048 || (L == 1024 && GRACE_YT_NB1_1024))) ? GRACE_YT_NB_INV
                                                                             : 2;  // single-buffered slower elsewhere (block K4 27.6 vs 8.0 ms)
   using Y = YTma<L, NCOL, NB>;
-  auto kern = k_y_tma<L, NCOL, INV, NB>;
+  // TMA stores where they measured faster: the single-buffered K4 (slab: 0.63 -> 0.59 ms);
+  // the double-buffered one (film, L = 1024) lost 5 % to the read-wait before each reload
+  const bool tst = INV && NB == 1 && tout != nullptr && g.kb == 0 && !g.p2p;
+  auto kern = tst ? k_y_tma<L, NCOL, INV, NB, INV && NB == 1> : k_y_tma<L, NCOL, INV, NB, false>;
   cudaError_t e = prep(kern, Y::SMEM);
   if (e != cudaSuccess) return e;
   const int ntiles = ((g.Kc + NCOL - 1) / NCOL) * g.nc * g.nz;
@@ -1661,10 +1696,11 @@ static cudaError_t ky_tma_launch(const Geom& g, float2* out, const float2* tw, c
   const int per_sm = (int)(220 * 1024 / Y::SMEM) < want ? (int)(220 * 1024 / Y::SMEM) : want;
   const int cap = g.nsm * (per_sm > 0 ? per_sm : 1);
   const int grid = ntiles < cap ? ntiles : cap;
-  CUtensorMap map;
+  CUtensorMap map, omap;
   static_assert(sizeof(CUtensorMap) == sizeof(TmapBlob), "tensor map size");
   memcpy(&map, tmap->b, sizeof map);
-  GRACE_TRY(launch_k(INV ? 8 : 2, kern, grid, Y::NT, Y::SMEM, st, map, out, tw, g, n_out));
+  memcpy(&omap, (tst ? tout : tmap)->b, sizeof omap);
+  GRACE_TRY(launch_k(INV ? 8 : 2, kern, grid, Y::NT, Y::SMEM, st, map, omap, out, tw, g, n_out));
   return cudaGetLastError();
 }
 
@@ -1706,9 +1742,9 @@ cudaError_t launch_k2(const Geom& g, const float2* X1, float2* X2, const float2*
 }
 
 cudaError_t launch_k4(const Geom& g, const float2* X2, float2* X1, const float2* tw, cudaStream_t st,
-                      const TmapBlob* tmap) {
+                      const TmapBlob* tmap, const TmapBlob* tout) {
   if (tmap != nullptr && g.Py >= kTmaMinL) {
-#define CASE(v) case v: return (v >= kTmaMinL) ? ky_tma_launch<(v >= kTmaMinL ? v : kTmaMinL), true>(g, X1, tw, st, g.ny, tmap) : cudaErrorInvalidValue;
+#define CASE(v) case v: return (v >= kTmaMinL) ? ky_tma_launch<(v >= kTmaMinL ? v : kTmaMinL), true>(g, X1, tw, st, g.ny, tmap, tout) : cudaErrorInvalidValue;
     GRACE_L_SWITCH(g.Py, CASE)
 #undef CASE
   }
@@ -1780,7 +1816,8 @@ cudaError_t make_plane_tmap(const Geom& g, const float2* X1, TmapBlob* map) {
 }
 
 template <int L>
-static cudaError_t ky_maps(const Geom& g, const float2* k2_in, const float2* x2, TmapBlob* k2map, TmapBlob* k4map) {
+static cudaError_t ky_maps(const Geom& g, const float2* k2_in, const float2* x2, TmapBlob* k2map, TmapBlob* k4map,
+                           TmapBlob* k4out) {
   constexpr int NCOL = ytma_ncol<L>();
   using Y = YTma<L, NCOL>;
   const int nq = g.kb ? (g.nz / g.nzl) : 1;
@@ -1798,14 +1835,20 @@ static cudaError_t ky_maps(const Geom& g, const float2* k2_in, const float2* x2,
 #endif
   cudaError_t e = encode5(k2map, k2_in, d2, s2, NCOL2, Y::br(false));
   if (e != cudaSuccess) return e;
+  // K4's TMA stores into X1 (single GPU: one block): boxes of the K4 tile's columns
+  if (k4out != nullptr && g.kb == 0) {
+    e = encode5(k4out, k2_in, d2, s2, NCOL, Y::br(true));
+    if (e != cudaSuccess) return e;
+  }
   const unsigned long long d4[5] = {(unsigned long long)g.Kc, (unsigned long long)g.Py, (unsigned long long)g.nz, 3, 1};
   const unsigned long long s4[4] = {p2, p2 * g.Py, p2 * g.Py * g.nz, p2 * g.Py * g.nz * 3};
   return encode5(k4map, x2, d4, s4, NCOL, Y::br(true));
 }
 
-cudaError_t make_ky_tmaps(const Geom& g, const float2* k2_in, const float2* x2, TmapBlob* k2map, TmapBlob* k4map) {
+cudaError_t make_ky_tmaps(const Geom& g, const float2* k2_in, const float2* x2, TmapBlob* k2map, TmapBlob* k4map,
+                          TmapBlob* k4out) {
   if (g.Py < kTmaMinL || g.Kc < 1) return cudaErrorNotSupported;
-#define CASE(v) case v: return (v >= kTmaMinL) ? ky_maps<(v >= kTmaMinL ? v : kTmaMinL)>(g, k2_in, x2, k2map, k4map) : cudaErrorNotSupported;
+#define CASE(v) case v: return (v >= kTmaMinL) ? ky_maps<(v >= kTmaMinL ? v : kTmaMinL)>(g, k2_in, x2, k2map, k4map, k4out) : cudaErrorNotSupported;
   GRACE_L_SWITCH(g.Py, CASE)
 #undef CASE
 }

@@ -31,6 +31,9 @@ def label(name):
         return "K1" if m.group(1) in ("1", "true") else "K5"
     if "k1_fwd_x" in name:
         return "K1"
+    m = re.search(r"k_y_tma<(?:\(int\))?\d+, (?:\(int\))?\d+, (?:\(bool\))?(\w+)", name)
+    if m:  # k_y_tma<L, NCOL, INV, NB, TST>
+        return "K4" if m.group(1) in ("1", "true") else "K2"
     if "k_y" in name:
         return "K4" if re.search(r"(, 1>|true>|\(bool\)1>)", name) else "K2"
     if "k3_z" in name:

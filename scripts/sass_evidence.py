@@ -12,8 +12,8 @@ LIB = sys.argv[1] if len(sys.argv) > 1 else "paper_1411_2565_b200/libgrace.so"
 WATCH = ["UTMALDG", "UTMASTG", "UBLKCP", "SYNCS", "LDGSTS", "UTC", "HMMA", "LDS", "STS", "LDG", "STG", "FFMA",
          "FADD", "FMUL", "ACQBULK", "PREEXIT"]
 # the instantiations the slab 1024x1024x32 step runs (K1..K6), then SP4's K2' and the setup
-KERNELS = [r"k_x_bulk<1024, true, false>", r"k_y_stage<2048>", r"k3_z_tma<64, 4>", r"k_y_tma<2048, 4, true",
-           r"k_x_bulk<1024, false, false>", r"k6_llg<true, false, 0, false>", r"k6_llg<true, false, 5, false>",
+KERNELS = [r"k_x_bulk<1024, true, false, 2048>", r"k_y_stage<2048>", r"k3_z_tma<64, 4>", r"k_y_tma<2048, 4, true, 1, true>",
+           r"k_x_bulk<1024, false, false, 2048>", r"k6_llg<true, false, 0, false>", r"k6_llg<true, false, 5, false>",
            r"k2f_y_fused<64, ", r"k_small_step<128, 64, 8>", r"k_octant", r"k_fft64", r"k_diag_partial<false>"]
 
 out = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
@@ -37,7 +37,7 @@ print("sm_100a: TMA tensor loads are `UTMALDG`, 1-D bulk copies `UBLKCP`, mbarri
       "programmatic dependent launch `ACQBULK` (griddepcontrol.wait) / `PREEXIT` (launch_dependents); `LDGSTS` is "
       "cp.async (K3's KS slice).  No tensor-core instructions by design (no dense contraction on this path).  "
       "Rows: the slab step's kernels (K1 = k_x_bulk<1024, true>, K2 = k_y_stage<2048>, K3 = k3_z_tma<64, 4>, "
-      "K4 = k_y_tma<2048, 4, true>, K5 = k_x_bulk<1024, false>, K6 = k6_llg), SP4's K2', the tensor setup and the "
+      "K4 = k_y_tma<2048, 4, true, 1, true> (TMA loads and TMA stores, `UTMASTG`), K5 = k_x_bulk<1024, false>, K6 = k6_llg), SP4's K2', the tensor setup and the "
       "diagnostics reduction.\n")
 print("| kernel | " + " | ".join(WATCH) + " |")
 print("|---|" + "---|" * len(WATCH))
