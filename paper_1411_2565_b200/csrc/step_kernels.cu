@@ -97,6 +97,11 @@ __device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, const void*
                "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
                : "memory");
 }
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];\n" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
@@ -613,6 +618,9 @@ struct Z3Tma {
   static constexpr size_t SMEM = TWOFF + TWB + 64;
 };
 
+#ifndef GRACE_K3_TMA_STORE
+#define GRACE_K3_TMA_STORE 0  // 1: K3 pencils stored by TMA from the work tile (measured slower: slab K3 0.933 vs 0.905 ms; profiles/r02_sweeps.md)
+#endif
 template <int L, int MINB>
 __global__ void __launch_bounds__(Z3Tma<L>::NT, MINB)
     k3_z_tma(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
@@ -682,6 +690,20 @@ __global__ void __launch_bounds__(Z3Tma<L>::NT, MINB)
       if (i < nz && b < nvalid) p[c * cs + (b + i * zs)] = v;
     }
   };
+  // TST: the inverse's last pass writes the work tile (linear [c][z][b]) and one
+  // thread stores the pencils with TMA boxes of the same map (z >= nz and
+  // kx >= Kc clipped by the unit); the tile is reused once the store has read it
+  constexpr bool TST = GRACE_K3_TMA_STORE;
+  auto store = [&](int ky) {
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) tma_store_4d(&xmap, work + c * Z::T::ELEMS, kx0, ky, 0, c);
+      bulk_commit();
+    }
+  };
+  const SmemSt<L, B, true> sst{work};
   for (int rep = 0; rep < nky; ++rep) {
     const int ky = rep == 0 ? kyf : g.Py - kyf;
     const St st{X2 + (size_t)ky * g.pitch2 + kx0, zstride, cstride, g.nz, nvalid};
@@ -690,20 +712,35 @@ __global__ void __launch_bounds__(Z3Tma<L>::NT, MINB)
     };
     if (rep == 0) {
       mbar_wait(bar + 1, 0);
-      pencil_conv<L, B, NT, Z::TWS>(work, SmemLd<L, B, true>{work}, st, kss, Z::KZH, twp, twstr, g.Py, ky, false, kw);
+      if constexpr (TST)
+        pencil_conv<L, B, NT, Z::TWS>(work, SmemLd<L, B, true>{work}, sst, kss, Z::KZH, twp, twstr, g.Py, ky, false, kw);
+      else
+        pencil_conv<L, B, NT, Z::TWS>(work, SmemLd<L, B, true>{work}, st, kss, Z::KZH, twp, twstr, g.Py, ky, false, kw);
     } else if constexpr (Z::PRE) {
+      if (TST && threadIdx.x == 0) bulk_wait_read0();
       __syncthreads();  // the work tile is free
       mbar_wait(bar + 2, 0);
-      pencil_conv<L, B, NT, Z::TWS>(work, StageLd{stage}, st, kss, Z::KZH, twp, twstr, g.Py, ky, false, kw);
+      if constexpr (TST)
+        pencil_conv<L, B, NT, Z::TWS>(work, StageLd{stage}, sst, kss, Z::KZH, twp, twstr, g.Py, ky, false, kw);
+      else
+        pencil_conv<L, B, NT, Z::TWS>(work, StageLd{stage}, st, kss, Z::KZH, twp, twstr, g.Py, ky, false, kw);
     } else {
       __syncthreads();
       if (threadIdx.x == 0) {
+        if constexpr (TST) bulk_wait_read0();
         fence_proxy_async();
         issue(work, ky, bar + 1, Z::T::ELEMS);
       }
       mbar_wait(bar + 1, 1);
-      pencil_conv<L, B, NT, Z::TWS>(work, SmemLd<L, B, true>{work}, st, kss, Z::KZH, twp, twstr, g.Py, ky, false, kw);
+      if constexpr (TST)
+        pencil_conv<L, B, NT, Z::TWS>(work, SmemLd<L, B, true>{work}, sst, kss, Z::KZH, twp, twstr, g.Py, ky, false, kw);
+      else
+        pencil_conv<L, B, NT, Z::TWS>(work, SmemLd<L, B, true>{work}, st, kss, Z::KZH, twp, twstr, g.Py, ky, false, kw);
     }
+    if constexpr (TST) store(ky);
+  }
+  if constexpr (TST) {
+    if (threadIdx.x == 0) bulk_wait0();  // the stores land before the grid completes (K4 waits on it)
   }
 }
 
