@@ -418,10 +418,13 @@ struct YStage {
   static constexpr int BR = 256;
 };
 
+#ifndef GRACE_K2_TMA_STORE
+#define GRACE_K2_TMA_STORE 0  // 1: X2 rows by TMA stores from the work tile (measured slower: slab K2 0.627 vs 0.549 ms)
+#endif
 template <int L>
 __global__ void __launch_bounds__(YStage<L>::NT, (L == 2048 ? GRACE_YSTAGE_MINB : 1))
-    k_y_stage(const __grid_constant__ CUtensorMap tin, float2* __restrict__ out, const float2* __restrict__ tw, Geom g,
-              int n_out) {
+    k_y_stage(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+              float2* __restrict__ out, const float2* __restrict__ tw, Geom g, int n_out) {
   using Y = YStage<L>;
   constexpr int NCOL = Y::NCOL, NT = Y::NT, ROWS = L / 2, NBOX = ROWS / Y::BR;
   constexpr unsigned TX = NCOL * ROWS * 8;
@@ -469,8 +472,13 @@ __global__ void __launch_bounds__(YStage<L>::NT, (L == 2048 ? GRACE_YSTAGE_MINB 
   using PL = Plan<L, false, 4>;
   constexpr int IFACE0 = TileIdx<L, NCOL, true, PL::R(0)>::PAD ? kPad : kLin;
   const ThreadMap<L, NCOL, NT, true> tm;
+  constexpr bool TST = GRACE_K2_TMA_STORE;  // X2 rows from the work tile by TMA stores
   for (int k = 0; t < ntiles; ++k, t += gridDim.x) {
     mbar_wait(bar, k & 1);
+    if constexpr (TST) {
+      if (threadIdx.x == 0) bulk_wait_read0();  // the previous tile's store has read the work tile
+      __syncthreads();
+    }
     const int slab = slab0 + t / ntx, xt = t - (t / ntx) * ntx;
     const int kx0 = xt * NCOL;
     const St st{out + (size_t)slab * g.Py * g.pitch2 + kx0, g.pitch2, g.Kc - kx0};
@@ -482,9 +490,25 @@ __global__ void __launch_bounds__(YStage<L>::NT, (L == 2048 ? GRACE_YSTAGE_MINB 
       fence_proxy_async();
       issue(t + gridDim.x);
     }
-    fft_passes<L, 1, false, NCOL, NT, true, 1, false, true, false, kExt, kExt, Y::TWS>(tm, work, StageLd{stage}, st,
-                                                                                         twp, tws_stride);
-    __syncthreads();
+    if constexpr (TST) {
+      fft_passes<L, 1, false, NCOL, NT, true, 1, false, true, false, kExt, kExt, Y::TWS>(
+          tm, work, StageLd{stage}, SmemSt<L, NCOL, true>{work}, twp, tws_stride);
+      fence_proxy_async();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int c = slab / g.nz, z = slab - c * g.nz;
+#pragma unroll 1
+        for (int y0 = 0; y0 < L; y0 += Y::BR) tma_store_5d(&tout, work + y0 * NCOL, kx0, y0, z, c, 0);
+        bulk_commit();
+      }
+    } else {
+      fft_passes<L, 1, false, NCOL, NT, true, 1, false, true, false, kExt, kExt, Y::TWS>(tm, work, StageLd{stage}, st,
+                                                                                           twp, tws_stride);
+      __syncthreads();
+    }
+  }
+  if constexpr (TST) {
+    if (threadIdx.x == 0) bulk_wait0();
   }
   (void)n_out;
 }
@@ -1741,6 +1765,8 @@ static cudaError_t ky_tma_launch(const Geom& g, float2* out, const float2* tw, c
   return cudaGetLastError();
 }
 
+static cudaError_t encode5(TmapBlob* out, const void* base, const unsigned long long dims[5],
+                           const unsigned long long strides[4], unsigned box_cols, unsigned box_rows);
 template <int L>
 static cudaError_t ky_stage_launch(const Geom& g, float2* out, const float2* tw, cudaStream_t st,
                                    const TmapBlob* tmap) {
@@ -1753,7 +1779,16 @@ static cudaError_t ky_stage_launch(const Geom& g, float2* out, const float2* tw,
   const int grid = ntiles < cap ? ntiles : cap;
   CUtensorMap map;
   memcpy(&map, tmap->b, sizeof map);
-  GRACE_TRY(launch_k(2, kern, grid, Y::NT, Y::SMEM, st, map, out, tw, g, g.Py));
+  CUtensorMap omap = map;
+  if constexpr (GRACE_K2_TMA_STORE) {  // X2 [3][nz][Py][pitch2]: boxes of the tile's columns x BR rows
+    const unsigned long long p2 = 8ull * g.pitch2;
+    const unsigned long long d[5] = {(unsigned long long)g.Kc, (unsigned long long)g.Py, (unsigned long long)g.nz, 3, 1};
+    const unsigned long long sd[4] = {p2, p2 * g.Py, p2 * g.Py * g.nz, p2 * g.Py * g.nz * 3};
+    TmapBlob ob;
+    GRACE_TRY(encode5(&ob, out, d, sd, Y::NCOL, Y::BR));
+    memcpy(&omap, ob.b, sizeof omap);
+  }
+  GRACE_TRY(launch_k(2, kern, grid, Y::NT, Y::SMEM, st, map, omap, out, tw, g, g.Py));
   return cudaGetLastError();
 }
 
