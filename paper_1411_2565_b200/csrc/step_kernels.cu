@@ -1157,7 +1157,7 @@ struct XbSt {
 #define GRACE_XB_ELEMS 2048  // complex values per x tile (L = 1024: 2 rows, 128 threads at 16 elements each)
 #endif
 #ifndef GRACE_XB_MINB
-#define GRACE_XB_MINB 4  // resident x-kernel CTAs per SM (scripts/sweep_x2.sh: 8192 x 1 -> 2048 x 4: slab K1 0.348 -> 0.288, K5 0.296 -> 0.275 ms; SP4 19.3 -> 11.3 us/step)
+#define GRACE_XB_MINB 6  // resident x-kernel CTAs per SM (8192 x 1 -> 2048 x 4: slab K1 0.348 -> 0.288, K5 0.296 -> 0.275 ms, SP4 19.3 -> 11.3 us/step; 4 -> 6: film 0.204 -> 0.199, 128^3 0.291 -> 0.285 ms/step in the graph, where the early-launched K5 co-resides with K4, slab neutral)
 #endif
 #ifndef GRACE_XB_ELEMS_TINY
 #define GRACE_XB_ELEMS_TINY 512  // tiles of tiny grids (fewer default tiles than half the SMs): SP4 9.1 -> 8.2 us/step
